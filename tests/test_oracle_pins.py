@@ -1,0 +1,340 @@
+"""Pins for the CPU oracle (SURVEY 8c "What pins each part").
+
+Each test checks the oracle against something other than itself: a closed form,
+an invariant, a worked example printed in the paper/SPEC (tests/golden), finite
+differences, or a library routine.  The aim is that any plausible mistake in
+oracle/cce_oracle.c (dropped term, sign, index, transposed operand, wrong
+divisor, missing max-shift) fails at least one of them.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workload
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def _rand_problem(N, D, V, seed, ignore_n=0, scale_w=1.0):
+    rng = np.random.default_rng(seed)
+    H = rng.standard_normal((N, D))
+    W = rng.standard_normal((V, D)) * scale_w / math.sqrt(D)
+    y = rng.integers(0, V, N).astype(np.int32)
+    if ignore_n:
+        y[rng.permutation(N)[:ignore_n]] = -100
+    return H, W, y
+
+
+# ---------------------------------------------------------------- worked examples
+def test_golden_online_softmax_examples():
+    """printed LSE values through the online (m,d) recursion."""
+    for key in ("online_lse_123", "lse_00", "lse_big"):
+        g = GOLD[key]
+        assert abs(oracle.online_lse(g["x"]) - g["lse"]) <= g["tol"], key
+    # any order ("in any order")
+    for perm in ([3.0, 1.0, 2.0], [2.0, 3.0, 1.0]):
+        assert abs(oracle.online_lse(perm) - GOLD["online_lse_123"]["lse"]) <= 5e-5
+
+
+def test_golden_zero_logits_loss():
+    """all-zero logits, V=97 -> loss ln 97 for any target; P:236 Qwen vocab."""
+    for key in ("zero_logits_V97",):
+        g = GOLD[key]
+        V = g["V"]
+        H = np.ones((3, 8))
+        W = np.zeros((V, 8))
+        y = np.array([0, 5, V - 1], np.int32)
+        r = oracle.cce(H, W, y)
+        assert abs(r["loss"] - g["loss"]) <= g["tol"]
+
+
+def test_golden_paper_arithmetic():
+    """P:487-490 (4.97 GB of fp32 logits) and P:583 (37x) -- the quantities the
+    bench's memory report uses to show no N x V buffer is allocated."""
+    g = GOLD["logit_memory_bytes"]
+    assert abs(g["B"] * g["N"] * g["V"] * 4 / 1e9 - g["GB"]) <= g["tol"]
+    g = GOLD["cce_reduction_factor"]
+    assert abs(g["V"] / g["C"] - g["factor"]) <= 0.1
+
+
+# ---------------------------------------------------------------- pin 1: W = 0
+@pytest.mark.parametrize("V", [1000, 151936])
+def test_pin1_W_zero(V):
+    N, D = 6, 16
+    rng = np.random.default_rng(1)
+    H = rng.standard_normal((N, D))
+    W = np.zeros((V, D))
+    y = np.array([0, 3, -100, 3, V - 1, 7], np.int32)
+    r = oracle.cce(H, W, y, dloss=1.0, grads=(V <= 1000))
+    lnV = math.log(V)
+    valid = y != -100
+    assert r["n_valid"] == 5
+    assert abs(r["loss"] - lnV) <= 1e-12
+    assert np.all(np.abs(r["lse"][valid] - lnV) <= 1e-12)
+    assert np.all(r["lse"][~valid] == 0.0)
+    if V == 151936:
+        assert abs(r["loss"] - GOLD["zero_logits_qwen_vocab"]["loss"]) <= 5e-10
+        return
+    assert np.all(r["dH"] == 0.0)
+    # closed form dW[v] = s * ((1/V) sum_valid h_n - sum_{valid n: y_n = v} h_n)
+    s = 1.0 / 5
+    ref = np.tile(H[valid].sum(0) / V, (V, 1))
+    for n in np.nonzero(valid)[0]:
+        ref[y[n]] -= H[n]
+    ref *= s
+    np.testing.assert_allclose(r["dW"], ref, rtol=0, atol=1e-13)
+
+
+# ---------------------------------------------------------------- pin 2: H = 0
+def test_pin2_H_zero():
+    N, D, V = 5, 12, 300
+    rng = np.random.default_rng(2)
+    H = np.zeros((N, D))
+    W = rng.standard_normal((V, D))
+    y = np.array([4, -100, 299, 0, 4], np.int32)
+    r = oracle.cce(H, W, y, dloss=0.5)
+    assert abs(r["loss"] - math.log(V)) <= 1e-12
+    assert np.all(r["dW"] == 0.0)
+    s = 0.5 / 4
+    for n in range(N):
+        if y[n] == -100:
+            assert np.all(r["dH"][n] == 0.0)
+        else:
+            np.testing.assert_allclose(r["dH"][n], s * (W.mean(0) - W[y[n]]), atol=1e-13)
+
+
+# ---------------------------------------------------------------- pins 3,4,5: G
+def test_pin3_gradient_is_softmax_minus_onehot_fd():
+    """dL/dz = softmax - onehot, checked by central differences of the
+    per-row loss with respect to the logits (independent computation)."""
+    N, D, V = 3, 5, 11
+    H, W, y = _rand_problem(N, D, V, 3)
+    G = oracle.dlogits(H, W, y, dloss=1.0)
+    z = H @ W.T
+    eps = 1e-6
+    for n in range(N):
+        for v in range(V):
+            zp = z[n].copy(); zp[v] += eps
+            zm = z[n].copy(); zm[v] -= eps
+            lp = np.log(np.sum(np.exp(zp))) - zp[y[n]]
+            lm = np.log(np.sum(np.exp(zm))) - zm[y[n]]
+            fd = (lp - lm) / (2 * eps) / N
+            assert abs(G[n, v] - fd) <= 1e-8
+
+
+def test_pin4_rows_sum_to_zero_and_dW_column_sums():
+    N, D, V = 16, 24, 500
+    H, W, y = _rand_problem(N, D, V, 4, ignore_n=3)
+    G = oracle.dlogits(H, W, y, dloss=1.0)
+    assert np.max(np.abs(G.sum(1))) <= 1e-12 * V
+    r = oracle.cce(H, W, y)
+    assert np.max(np.abs(r["dW"].sum(0))) <= 1e-12 * np.abs(r["dW"]).max() * V
+
+
+def test_pin5_gradient_bound():
+    """||grad_z L||_inf <= 1 per row; with the mean, <= |dloss|/n_valid."""
+    N, D, V = 20, 16, 257
+    H, W, y = _rand_problem(N, D, V, 5, ignore_n=4, scale_w=8.0)
+    dloss = -2.5
+    G = oracle.dlogits(H, W, y, dloss=dloss)
+    assert np.max(np.abs(G)) <= abs(dloss) / 16 + 1e-15
+
+
+# ---------------------------------------------------------------- pin 6: all ignored
+def test_pin6_all_ignored():
+    H, W, _ = _rand_problem(8, 8, 50, 6)
+    y = np.full(8, -100, np.int32)
+    r = oracle.cce(H, W, y)
+    assert r["n_valid"] == 0 and r["loss"] == 0.0
+    assert np.all(r["dH"] == 0.0) and np.all(r["dW"] == 0.0) and np.all(r["lse"] == 0.0)
+
+
+# ---------------------------------------------------------------- pin 7: online merge
+def _merge(parts):
+    """The (m, d) merge of P:1157-1163 / P:521-541, written out for the test."""
+    m = -np.inf
+    d = 0.0
+    for mi, di in parts:
+        if di == 0.0:
+            continue
+        mn = max(m, mi)
+        d = (d * math.exp(m - mn) if d > 0 else 0.0) + di * math.exp(mi - mn)
+        m = mn
+    return m + math.log(d)
+
+
+@pytest.mark.parametrize("width", [1, 7, 64, 128, 1005])
+def test_pin7_online_equals_two_pass(width):
+    rng = np.random.default_rng(width)
+    for _ in range(50):
+        x = rng.standard_normal(1000) * 5
+        x[rng.integers(0, 1000, 3)] = x.max()           # duplicated maxima
+        two_pass = x.max() + math.log(np.sum(np.exp(x - x.max())))
+        assert abs(oracle.online_lse(x) - two_pass) <= 1e-12 * abs(two_pass) + 1e-12
+        assert abs(oracle.online_lse(rng.permutation(x)) - two_pass) <= 1e-12 * abs(two_pass) + 1e-12
+        parts = []
+        for s in range(0, len(x), width):
+            c = x[s:s + width]
+            parts.append((c.max(), float(np.sum(np.exp(c - c.max())))))
+        assert abs(_merge(parts) - two_pass) <= 1e-12 * abs(two_pass) + 1e-12
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_pin7_sharded_partial_stats_merge(P):
+    """Vocabulary shards: per-shard (m, d, z_y) merged in rank order
+    equal the unsharded oracle (lse and loss), including uneven and empty shards."""
+    N, D, V = 12, 16, 1000
+    H, W, y = _rand_problem(N, D, V, 70 + P, ignore_n=2)
+    full = oracle.cce(H, W, y, grads=False)
+    bounds = np.linspace(0, V, P + 1).astype(int)
+    if P == 3:
+        bounds = np.array([0, 0, 517, V])      # an empty shard and an uneven split
+    stats = [oracle.partial_stats(H, W[bounds[r]:bounds[r + 1]], y, bounds[r]) for r in range(len(bounds) - 1)]
+    for n in range(N):
+        if y[n] == -100:
+            continue
+        lse = _merge([(s[0][n], s[1][n]) for s in stats])
+        zy = sum(s[2][n] for s in stats)
+        assert abs(lse - full["lse"][n]) <= 1e-12 * abs(lse)
+        assert abs(zy - (H[n] @ W[y[n]])) <= 1e-12
+
+
+# ---------------------------------------------------------------- pin 8: finite differences
+@pytest.mark.parametrize("shape", [(4, 8, 50), (7, 16, 333)])
+def test_pin8_finite_differences(shape):
+    N, D, V = shape
+    H, W, y = _rand_problem(N, D, V, 8 + N, ignore_n=1)
+    r = oracle.cce(H, W, y, dloss=1.0)
+    eps = 1e-6
+
+    def loss(Hx, Wx):
+        return oracle.cce(Hx, Wx, y, grads=False)["loss"]
+
+    rng = np.random.default_rng(0)
+    fdH = np.zeros_like(H)
+    for n in range(N):
+        for d in range(D):
+            Hp = H.copy(); Hp[n, d] += eps
+            Hm = H.copy(); Hm[n, d] -= eps
+            fdH[n, d] = (loss(Hp, W) - loss(Hm, W)) / (2 * eps)
+    assert np.linalg.norm(fdH - r["dH"]) <= 1e-6 * np.linalg.norm(r["dH"])
+    vs = list(rng.choice(V, 12, replace=False)) + [int(y[0]) if y[0] >= 0 else int(y[1])]
+    for v in vs:
+        fd = np.zeros(D)
+        for d in range(D):
+            Wp = W.copy(); Wp[v, d] += eps
+            Wm = W.copy(); Wm[v, d] -= eps
+            fd[d] = (loss(H, Wp) - loss(H, Wm)) / (2 * eps)
+        assert np.linalg.norm(fd - r["dW"][v]) <= 1e-6 * max(np.linalg.norm(r["dW"][v]), 1e-3)
+
+
+# ---------------------------------------------------------------- pin 9: shift invariance
+def test_pin9_shift_invariance():
+    """Append a constant column: H' = [H, 1], W' = [W, c] (c = 80, exact in bf16):
+    lse' = lse + c; loss, dH[:, :D], dW[:, :D] unchanged (exercises the max shift)."""
+    N, D, V = 10, 15, 400
+    H, W, y = _rand_problem(N, D, V, 9, ignore_n=2)
+    c = 80.0
+    H2 = np.concatenate([H, np.ones((N, 1))], 1)
+    W2 = np.concatenate([W, np.full((V, 1), c)], 1)
+    a = oracle.cce(H, W, y)
+    b = oracle.cce(H2, W2, y)
+    valid = y != -100
+    np.testing.assert_allclose(b["lse"][valid], a["lse"][valid] + c, rtol=1e-13)
+    assert abs(a["loss"] - b["loss"]) <= 1e-11
+    np.testing.assert_allclose(b["dH"][:, :D], a["dH"], atol=1e-12)
+    np.testing.assert_allclose(b["dW"][:, :D], a["dW"], atol=1e-12)
+
+
+# ---------------------------------------------------------------- pin 10: V = 2
+def test_pin10_two_classes_softplus():
+    N, D = 9, 6
+    H, W, y = _rand_problem(N, D, 2, 10)
+    r = oracle.cce(H, W, y, grads=False)
+    z = H @ W.T
+    ref = np.mean([np.logaddexp(0.0, z[n, 1 - y[n]] - z[n, y[n]]) for n in range(N)])
+    assert abs(r["loss"] - ref) <= 1e-13
+
+
+# ---------------------------------------------------------------- pin 11: linearity in dloss
+def test_pin11_linear_in_dloss():
+    H, W, y = _rand_problem(6, 8, 90, 11, ignore_n=1)
+    a = oracle.cce(H, W, y, dloss=1.0)
+    b = oracle.cce(H, W, y, dloss=0.37)
+    z = oracle.cce(H, W, y, dloss=0.0)
+    np.testing.assert_allclose(b["dH"], 0.37 * a["dH"], rtol=1e-12, atol=1e-16)
+    np.testing.assert_allclose(b["dW"], 0.37 * a["dW"], rtol=1e-12, atol=1e-16)
+    assert np.all(z["dH"] == 0) and np.all(z["dW"] == 0)
+    assert a["loss"] == b["loss"]
+
+
+# ---------------------------------------------------------------- pin 12: library routine
+@pytest.mark.parametrize("seed", [0, 1])
+def test_pin12_matches_torch_fp64(seed):
+    torch = pytest.importorskip("torch")
+    N, D, V = 24, 32, 777
+    H, W, y = _rand_problem(N, D, V, 120 + seed, ignore_n=5)
+    Ht = torch.tensor(H, requires_grad=True)
+    Wt = torch.tensor(W, requires_grad=True)
+    lt = torch.nn.functional.cross_entropy(Ht @ Wt.T, torch.tensor(y, dtype=torch.long), ignore_index=-100)
+    lt.backward()
+    r = oracle.cce(H, W, y)
+    assert abs(r["loss"] - lt.item()) <= 1e-12
+    np.testing.assert_allclose(r["dH"], Ht.grad.numpy(), rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(r["dW"], Wt.grad.numpy(), rtol=1e-10, atol=1e-14)
+
+
+# ---------------------------------------------------------------- pin 13: sanity bounds
+def test_pin13_bounds_on_workload_inputs():
+    p = workload.make_config("tiny", seed=3)
+    r = oracle.cce(p["H"], p["W"], p["labels"])
+    Hf = oracle._bits(p["H"]); Wf = oracle._bits(p["W"])
+    z = Hf @ Wf.T
+    valid = p["labels"] != -100
+    for n in np.nonzero(valid)[0]:
+        zy = z[n, p["labels"][n]]
+        assert zy <= r["lse"][n] + 1e-12
+        assert z[n].max() <= r["lse"][n] <= z[n].max() + math.log(z.shape[1]) + 1e-12
+    assert r["loss"] >= 0
+
+
+# ---------------------------------------------------------------- errors, sampled entry points
+def test_label_range_error():
+    H, W, y = _rand_problem(4, 4, 10, 12)
+    y[2] = 10
+    with pytest.raises(oracle.OracleError):
+        oracle.cce(H, W, y)
+    y[2] = -1
+    with pytest.raises(oracle.OracleError):
+        oracle.cce(H, W, y)
+
+
+def test_rows_and_dW_rows_agree_with_full():
+    p = workload.make_config("tiny", seed=4)
+    full = oracle.cce(p["H"], p["W"], p["labels"], dloss=1.0)
+    valid_rows = np.nonzero(p["labels"] != -100)[0]
+    s = 1.0 / len(valid_rows)
+    lse, zy, dH = oracle.rows(p["H"], p["W"], p["labels"], valid_rows[:9], scale=s)
+    np.testing.assert_allclose(lse, full["lse"][valid_rows[:9]], rtol=1e-14)
+    np.testing.assert_allclose(dH, full["dH"][valid_rows[:9]], rtol=1e-12, atol=1e-15)
+    vr = np.array([0, 1, 17, 999])
+    dW = oracle.dW_rows(p["H"], p["W"], p["labels"], full["lse"], s, vr)
+    np.testing.assert_allclose(dW, full["dW"][vr], rtol=1e-12, atol=1e-15)
+
+
+# ---------------------------------------------------------------- the generator
+def test_workload_packed_padding_recipe():
+    for seed in range(3):
+        m = workload.valid_mask(seed, 8, 1024, "packed40")
+        assert m.sum() == 4915 and (~m).sum() == 3277
+    m = workload.valid_mask(0, 1, 64, "exact6")
+    assert (~m).sum() == 6
+    x = workload.normal_f64(7, 1, 0, 200000)
+    assert abs(x.mean()) < 0.01 and abs(x.std() - 1) < 0.01
+    a = workload.normal_bf16(1, 2, 3, 5, 1.0)
+    b = workload.normal_bf16(1, 2, 3, 5, 1.0, chunk_elems=4)
+    assert np.array_equal(a, b)
