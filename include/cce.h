@@ -1,0 +1,168 @@
+/*
+ * cce.h -- C ABI of the B200-native fused linear cross-entropy library
+ * ("Cut Cross-Entropy", arxiv 2601.02609 "Chronicals", section "Cut
+ * Cross-Entropy: Memory-Efficient Loss Computation").
+ *
+ * The library computes, for hidden states H[N,D] (bf16), an LM-head weight
+ * (shard) W[V_local,D] (bf16) and labels y[N] (int32, ignore_index allowed):
+ *
+ *   z[n,v] = H[n,:] . W[v,:]                       (Alg. "Chunked Cross-Entropy
+ *                                                   Forward Pass")
+ *   lse_n  = log sum_v exp(z[n,v])                  (Def. Online Softmax / Theorem,
+ *                                                   P:511-541; stable form P:3528-3543)
+ *   loss   = (1/n_valid) sum_{y_n != ignore} (lse_n - z[n,y_n])
+ *                                                  (Def. Cross-Entropy Loss P:243-248;
+ *                                                   mean over non-ignored rows P:899)
+ *   G[n,v] = (dloss/n_valid) (softmax(z_n)_v - 1[v = y_n])
+ *                                                  (Prop. CE Gradient P:254-258;
+ *                                                   Thm. CCE Backward P:645-650)
+ *   dH = G W,  dW = G^T H                           (Alg. "CCE Triton Backward Kernel",
+ *                                                   P:652-670, lines 666-667)
+ *
+ * without ever allocating an [N x V] buffer (Def. Memory Bottleneck).
+ * Readings where the paper is silent or garbled are listed in DESIGN.md.
+ *
+ * Conventions (all functions):
+ *  - Pointers are DEVICE pointers unless the parameter name ends in _host.
+ *    bf16 tensors are passed as `void*` to raw 2-byte IEEE bfloat16 storage;
+ *    `stream` is a cudaStream_t passed as `void*` (NULL = legacy default stream).
+ *  - Layout: H is row-major with row stride `ldh` elements (ldh >= D), W is
+ *    row-major with row stride `ldw` (ldw >= D).  dH [N,D] and dW [V_local,D]
+ *    outputs are dense row-major (row stride D).  H, W must be 16-byte aligned
+ *    and ldh*2, ldw*2 multiples of 16 bytes.  D must be a multiple of 64.
+ *  - Ownership: the caller owns every buffer, including `workspace`.  The
+ *    handle owns only host-side state (the pointers saved between forward and
+ *    backward).  H, W, labels and workspace must stay alive and unmodified
+ *    from cce_forward until the matching cce_backward has been enqueued.
+ *    The library never allocates device memory on the hot path.
+ *  - Errors: host-detectable errors return a status immediately and enqueue
+ *    nothing.  Device-detected label errors (a label that is neither
+ *    ignore_index nor in [0, vocab_total)) set a sticky device flag and make
+ *    `loss` NaN; they are reported by cce_get_error (the only synchronising
+ *    call besides cce_step_host).
+ *  - No host synchronisation inside cce_forward / cce_backward.
+ *  - Determinism: outputs are bit-reproducible run to run (no atomics on
+ *    outputs, fixed-order reductions).
+ *  - Threading: a handle is single-stream and not thread-safe; one
+ *    forward/backward pair in flight per handle.  Handles are independent.
+ */
+#ifndef CCE_H_
+#define CCE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cce_handle cce_handle;
+
+typedef enum {
+  CCE_OK = 0,
+  CCE_ERR_INVALID_VALUE = 1,  /* NULL pointer, N < 0, D <= 0, V_local < 0, ld < D, bad rank/world */
+  CCE_ERR_UNSUPPORTED = 2,    /* D % 64 != 0, misaligned pointer/stride, no sm_100 device */
+  CCE_ERR_LABEL_RANGE = 3,    /* device-detected, sticky; reported by cce_get_error */
+  CCE_ERR_NO_FORWARD = 4,     /* cce_backward without a matching cce_forward on this handle */
+  CCE_ERR_WORKSPACE = 5,      /* workspace NULL or smaller than cce_workspace_bytes() */
+  CCE_ERR_CUDA = 6,           /* a CUDA runtime/driver call failed */
+  CCE_ERR_NCCL = 7            /* NCCL unavailable or an NCCL call failed */
+} cce_status;
+
+/* flags */
+#define CCE_FLAG_NONE 0u
+
+typedef struct {
+  int32_t ignore_index;   /* label value that marks a skipped row; -100 in the paper */
+  int64_t vocab_total;    /* global vocabulary size V, for the label range check */
+  int64_t vocab_offset;   /* first global vocabulary id owned by this rank (0 if unsharded) */
+  int32_t rank;           /* this rank, 0 if unsharded */
+  int32_t world;          /* number of vocabulary shards (ranks), 1 if unsharded */
+  void *nccl_comm;        /* ncclComm_t from cce_nccl_comm_init when world > 1, else NULL */
+  uint32_t flags;         /* CCE_FLAG_* */
+} cce_config;
+
+/* Fill `cfg` with defaults: ignore_index=-100, vocab_total=0 (must be set),
+ * offset 0, rank 0, world 1, no comm, no flags. */
+void cce_config_default(cce_config *cfg);
+
+/* Create / destroy a handle.  cce_create validates cfg (vocab_total > 0,
+ * 0 <= rank < world, comm present iff world > 1) and queries the current
+ * device (must be compute capability 10.x for the sm_100a kernels). */
+cce_status cce_create(cce_handle **out, const cce_config *cfg);
+cce_status cce_destroy(cce_handle *h);
+
+/* Bytes of device workspace needed for a problem of N rows, D hidden, V_local
+ * vocabulary rows on this rank.  O(N*D + N*ceil(V_local/256) + N*chunk); never
+ * O(N*V).  Returns 0 for invalid arguments. */
+size_t cce_workspace_bytes(const cce_handle *h, int64_t N, int64_t D, int64_t V_local);
+
+/*
+ * Forward: mean loss over non-ignored rows, per-row global log-sum-exp.
+ *   H      [N, D] bf16, row stride ldh          (hidden states)
+ *   W      [V_local, D] bf16, row stride ldw     (this rank's LM-head rows [off, off+V_local))
+ *   labels [N] int32, global ids or ignore_index
+ *   loss   device float scalar                   (mean over valid rows; 0 if none; NaN on label error)
+ *   lse    [N] device float, may be NULL         (global LSE; 0.0f for ignored rows)
+ *   n_valid device int32 scalar, may be NULL     (number of non-ignored rows)
+ * World > 1: every rank passes the same H/labels and its own W shard; loss
+ * and lse come out identical on every rank (NCCL allgather of per-row
+ * (max, sum-exp, target-logit) partials, merged in rank order).
+ */
+cce_status cce_forward(cce_handle *h,
+                       const void *H, int64_t N, int64_t D, int64_t ldh,
+                       const void *W, int64_t V_local, int64_t ldw,
+                       const int32_t *labels,
+                       float *loss, float *lse, int32_t *n_valid,
+                       void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Backward of the mean loss w.r.t. H and this rank's W shard.
+ *   dloss  device float scalar, the upstream gradient of `loss`
+ *   dH     [N, D] bf16 output, overwritten; ignored rows are written as 0
+ *          (world > 1: the full dH, summed over ranks by NCCL all-reduce)
+ *   dW     [V_local, D] bf16 output, overwritten (stays local to the rank)
+ * Uses the inputs and workspace saved by the last cce_forward on `h`.
+ */
+cce_status cce_backward(cce_handle *h, const float *dloss, void *dH, void *dW, void *stream);
+
+/* Synchronises `stream` and returns CCE_ERR_LABEL_RANGE if any forward on
+ * this handle saw an out-of-range label since the last call (then clears
+ * the flag), else CCE_OK. */
+cce_status cce_get_error(cce_handle *h, void *stream);
+
+/*
+ * End-to-end step with HOST inputs: copies H_host [N,D] (dense, pinned
+ * recommended) and labels_host [N] to the device, runs forward + backward
+ * with dloss = 1, copies the loss back to *loss_host and synchronises
+ * `stream`.  W, dH, dW, the device staging buffer `dev_inputs` (at least
+ * cce_host_staging_bytes(N, D) bytes) and workspace are device memory.
+ */
+size_t cce_host_staging_bytes(int64_t N, int64_t D);
+cce_status cce_step_host(cce_handle *h,
+                         const void *H_host, int64_t N, int64_t D,
+                         const int32_t *labels_host,
+                         const void *W, int64_t V_local, int64_t ldw,
+                         float *loss_host, void *dH, void *dW,
+                         void *dev_inputs, size_t dev_inputs_bytes,
+                         void *workspace, size_t workspace_bytes, void *stream);
+
+/* NCCL plumbing for world > 1 (NCCL is resolved at run time with dlopen; the
+ * library does not link it).  The 128-byte unique id is produced on rank 0 and
+ * broadcast by the caller (e.g. over torch.distributed). */
+cce_status cce_nccl_unique_id(void *id_out_128_bytes_host);
+cce_status cce_nccl_comm_init(void **comm_out, int32_t world, const void *id_128_bytes_host, int32_t rank);
+cce_status cce_nccl_comm_destroy(void *comm);
+
+/* Human-readable status. */
+const char *cce_status_string(cce_status s);
+
+/* Library introspection: number of kernels launched by this handle so far
+ * (forward + backward), for the bench's launch count; build string. */
+int64_t cce_kernel_launches(const cce_handle *h);
+const char *cce_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CCE_H_ */

@@ -1,0 +1,277 @@
+"""B200-native fused linear cross-entropy (Cut Cross-Entropy, arxiv 2601.02609).
+
+Thin Python binding over the C ABI in ``include/cce.h`` (``libcce.so``).  This
+module only marshals arguments: every step of the forward and backward runs in
+the library's sm_100a kernels.  PyTorch is used for device memory, streams and
+process groups only.  There is no CPU fallback: if the extension is missing or
+no sm_100 device is present, calls raise.
+
+Public API
+  cce_create / cce_destroy / cce_workspace_bytes / cce_forward / cce_backward /
+  cce_get_error / cce_step_host / cce_nccl_*      -- same names as the C ABI
+  CCEHandle                                        -- owns a handle + workspace
+  linear_cross_entropy(H, W, labels, ...)          -- autograd entry point
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libcce.so")
+
+CCE_OK = 0
+STATUS = {0: "CCE_OK", 1: "CCE_ERR_INVALID_VALUE", 2: "CCE_ERR_UNSUPPORTED", 3: "CCE_ERR_LABEL_RANGE",
+          4: "CCE_ERR_NO_FORWARD", 5: "CCE_ERR_WORKSPACE", 6: "CCE_ERR_CUDA", 7: "CCE_ERR_NCCL"}
+
+# every symbol include/cce.h declares
+EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_bytes", "cce_forward", "cce_backward",
+           "cce_get_error", "cce_host_staging_bytes", "cce_step_host", "cce_nccl_unique_id", "cce_nccl_comm_init",
+           "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info"]
+
+
+class CCEError(RuntimeError):
+    def __init__(self, status: int, where: str = ""):
+        self.status = status
+        super().__init__(f"{where}: {STATUS.get(status, status)}")
+
+
+class cce_config(ctypes.Structure):
+    _fields_ = [("ignore_index", ctypes.c_int32), ("vocab_total", ctypes.c_int64), ("vocab_offset", ctypes.c_int64),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
+                ("flags", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libcce.so (build it first with paper_2601_02609_b200.build.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        p, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+        st = ctypes.c_int
+        L.cce_config_default.argtypes = [ctypes.POINTER(cce_config)]
+        L.cce_config_default.restype = None
+        L.cce_create.argtypes = [ctypes.POINTER(p), ctypes.POINTER(cce_config)]
+        L.cce_create.restype = st
+        L.cce_destroy.argtypes = [p]
+        L.cce_destroy.restype = st
+        L.cce_workspace_bytes.argtypes = [p, i64, i64, i64]
+        L.cce_workspace_bytes.restype = sz
+        L.cce_forward.argtypes = [p, p, i64, i64, i64, p, i64, i64, p, p, p, p, p, sz, p]
+        L.cce_forward.restype = st
+        L.cce_backward.argtypes = [p, p, p, p, p]
+        L.cce_backward.restype = st
+        L.cce_get_error.argtypes = [p, p]
+        L.cce_get_error.restype = st
+        L.cce_host_staging_bytes.argtypes = [i64, i64]
+        L.cce_host_staging_bytes.restype = sz
+        L.cce_step_host.argtypes = [p, p, i64, i64, p, p, i64, i64, p, p, p, p, sz, p, sz, p]
+        L.cce_step_host.restype = st
+        L.cce_nccl_unique_id.argtypes = [p]
+        L.cce_nccl_unique_id.restype = st
+        L.cce_nccl_comm_init.argtypes = [ctypes.POINTER(p), i32, p, i32]
+        L.cce_nccl_comm_init.restype = st
+        L.cce_nccl_comm_destroy.argtypes = [p]
+        L.cce_nccl_comm_destroy.restype = st
+        L.cce_status_string.argtypes = [st]
+        L.cce_status_string.restype = ctypes.c_char_p
+        L.cce_kernel_launches.argtypes = [p]
+        L.cce_kernel_launches.restype = i64
+        L.cce_build_info.argtypes = []
+        L.cce_build_info.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(status: int, where: str):
+    if status != CCE_OK:
+        raise CCEError(status, where)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+# ----------------------------------------------------------------- C-ABI mirrors
+def cce_create(vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0, rank: int = 0, world: int = 1,
+               nccl_comm=None) -> ctypes.c_void_p:
+    cfg = cce_config()
+    lib().cce_config_default(ctypes.byref(cfg))
+    cfg.ignore_index = ignore_index
+    cfg.vocab_total = vocab_total
+    cfg.vocab_offset = vocab_offset
+    cfg.rank = rank
+    cfg.world = world
+    cfg.nccl_comm = nccl_comm
+    h = ctypes.c_void_p()
+    _check(lib().cce_create(ctypes.byref(h), ctypes.byref(cfg)), "cce_create")
+    return h
+
+
+def cce_destroy(h):
+    _check(lib().cce_destroy(h), "cce_destroy")
+
+
+def cce_workspace_bytes(h, N: int, D: int, V_local: int) -> int:
+    return int(lib().cce_workspace_bytes(h, N, D, V_local))
+
+
+def cce_forward(h, H, W, labels, loss, lse, n_valid, workspace, stream=None):
+    N, D = H.shape
+    V_local = W.shape[0]
+    _check(lib().cce_forward(h, _ptr(H), N, D, H.stride(0), _ptr(W), V_local, W.stride(0), _ptr(labels), _ptr(loss),
+                             _ptr(lse), _ptr(n_valid), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                             _stream(stream)), "cce_forward")
+
+
+def cce_backward(h, dloss, dH, dW, stream=None):
+    _check(lib().cce_backward(h, _ptr(dloss), _ptr(dH), _ptr(dW), _stream(stream)), "cce_backward")
+
+
+def cce_get_error(h, stream=None) -> int:
+    return int(lib().cce_get_error(h, _stream(stream)))
+
+
+def cce_host_staging_bytes(N: int, D: int) -> int:
+    return int(lib().cce_host_staging_bytes(N, D))
+
+
+def cce_step_host(h, H_host, labels_host, W, dH, dW, staging, workspace, stream=None) -> float:
+    N, D = H_host.shape
+    out = ctypes.c_float()
+    _check(lib().cce_step_host(h, ctypes.c_void_p(H_host.data_ptr()), N, D, ctypes.c_void_p(labels_host.data_ptr()),
+                               _ptr(W), W.shape[0], W.stride(0), ctypes.byref(out), _ptr(dH), _ptr(dW),
+                               _ptr(staging), staging.numel() * staging.element_size(), _ptr(workspace),
+                               workspace.numel() * workspace.element_size(), _stream(stream)), "cce_step_host")
+    return out.value
+
+
+def cce_kernel_launches(h) -> int:
+    return int(lib().cce_kernel_launches(h))
+
+
+def cce_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().cce_nccl_unique_id(buf), "cce_nccl_unique_id")
+    return buf.raw
+
+
+def cce_nccl_comm_init(world: int, uid: bytes, rank: int) -> ctypes.c_void_p:
+    comm = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(lib().cce_nccl_comm_init(ctypes.byref(comm), world, buf, rank), "cce_nccl_comm_init")
+    return comm
+
+
+def cce_nccl_comm_destroy(comm):
+    _check(lib().cce_nccl_comm_destroy(comm), "cce_nccl_comm_destroy")
+
+
+# ----------------------------------------------------------------- convenience
+class CCEHandle:
+    """A library handle plus a cached device workspace (torch-allocated)."""
+
+    def __init__(self, vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0, rank: int = 0,
+                 world: int = 1, nccl_comm=None):
+        self.h = cce_create(vocab_total, ignore_index, vocab_offset, rank, world, nccl_comm)
+        self.vocab_total = vocab_total
+        self.ignore_index = ignore_index
+        self._ws = None
+
+    def workspace(self, N, D, V_local, device):
+        import torch
+        need = cce_workspace_bytes(self.h, N, D, V_local)
+        if self._ws is None or self._ws.numel() < need or self._ws.device != device:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=device)
+        return self._ws
+
+    def forward(self, H, W, labels, want_lse=True, stream=None):
+        import torch
+        N, D = H.shape
+        ws = self.workspace(N, D, W.shape[0], H.device)
+        loss = torch.empty((), dtype=torch.float32, device=H.device)
+        lse = torch.empty(N, dtype=torch.float32, device=H.device) if want_lse else None
+        nv = torch.empty((), dtype=torch.int32, device=H.device)
+        cce_forward(self.h, H, W, labels, loss, lse, nv, ws, stream)
+        return loss, lse, nv
+
+    def backward(self, dloss, dH, dW, stream=None):
+        cce_backward(self.h, dloss, dH, dW, stream)
+
+    def launches(self) -> int:
+        return cce_kernel_launches(self.h)
+
+    def close(self):
+        if self.h is not None:
+            cce_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _check_inputs(H, W, labels):
+    import torch
+    if not (H.is_cuda and W.is_cuda and labels.is_cuda):
+        raise ValueError("linear_cross_entropy: tensors must be on a CUDA device (no CPU fallback)")
+    if H.dtype != torch.bfloat16 or W.dtype != torch.bfloat16 or labels.dtype != torch.int32:
+        raise TypeError("linear_cross_entropy: H, W must be bfloat16 and labels int32")
+
+
+def _make_function():
+    import torch
+
+    class CCEFunction(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, H, W, labels, handle):
+            loss, lse, nv = handle.forward(H, W, labels)
+            ctx.handle = handle
+            ctx.shapes = (H.shape, W.shape)
+            ctx.save_for_backward(H, W, labels)
+            ctx.mark_non_differentiable(lse, nv)
+            return loss, lse, nv
+
+        @staticmethod
+        def backward(ctx, dloss, _dlse, _dnv):
+            import torch
+            (H, W, labels) = ctx.saved_tensors
+            dH = torch.empty_like(H) if H.stride(0) == H.shape[1] else torch.empty(H.shape, dtype=H.dtype, device=H.device)
+            dW = torch.empty(W.shape, dtype=W.dtype, device=W.device)
+            if dloss is None:
+                dloss = torch.zeros((), dtype=torch.float32, device=H.device)
+            ctx.handle.backward(dloss.contiguous().float(), dH, dW)
+            return dH, dW, None, None
+
+    return CCEFunction
+
+
+_CCEFunction = None
+
+
+def linear_cross_entropy(H, W, labels, ignore_index: int = -100, handle: CCEHandle | None = None,
+                         return_lse: bool = False):
+    """Mean cross-entropy of softmax(H W^T) against labels, fused and never
+    materialising the [N, V] logits.  H [N,D] bf16, W [V,D] bf16, labels [N] int32."""
+    global _CCEFunction
+    _check_inputs(H, W, labels)
+    if _CCEFunction is None:
+        _CCEFunction = _make_function()
+    if handle is None:
+        handle = CCEHandle(vocab_total=W.shape[0], ignore_index=ignore_index)
+    loss, lse, nv = _CCEFunction.apply(H, W, labels, handle)
+    return (loss, lse) if return_lse else loss

@@ -1,0 +1,483 @@
+// cce_api.cu -- host side of the C ABI declared in include/cce.h: argument
+// validation, workspace layout, TMA tensor maps, kernel launches and the
+// vocabulary-sharded NCCL combine.  No host synchronisation on the hot path.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/cce.h"
+#include "cce_aux.cuh"
+#include "cce_gemm.cuh"
+
+using namespace cce;
+
+#ifndef CCE_CHUNK
+#define CCE_CHUNK 8192  // vocabulary rows per backward chunk (Gbuf = Npad x CCE_CHUNK bf16)
+#endif
+
+// ------------------------------------------------------------------ handle
+struct cce_handle {
+  cce_config cfg;
+  int device = 0;
+  int num_sms = 148;
+  // state saved by the forward for the backward (like autograd-saved tensors)
+  bool have_fwd = false;
+  const void* W = nullptr;
+  int64_t N = 0, D = 0, V_local = 0, ldw = 0;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  int64_t launches = 0;
+  int* err_host_flag_dev = nullptr;  // points into the saved workspace
+};
+
+// ------------------------------------------------------------------ driver entry points
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major matrix [rows][cols] with row stride
+// `ld` elements, box {64 (cols), box_rows}, 128-byte swizzle, zero OOB fill.
+static bool make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                     uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct NcclId {
+  char internal[128];
+};
+typedef int (*nccl_get_id_t)(NcclId*);
+typedef int (*nccl_init_t)(void**, int, NcclId, int);
+typedef int (*nccl_destroy_t)(void*);
+typedef int (*nccl_allgather_t)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+struct Nccl {
+  bool ok = false;
+  nccl_get_id_t get_id;
+  nccl_init_t init;
+  nccl_destroy_t destroy;
+  nccl_allgather_t allgather;
+  nccl_allreduce_t allreduce;
+};
+const int kNcclFloat32 = 7, kNcclSum = 0;
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the one torch already loaded
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    n.get_id = (nccl_get_id_t)dlsym(h, "ncclGetUniqueId");
+    n.init = (nccl_init_t)dlsym(h, "ncclCommInitRank");
+    n.destroy = (nccl_destroy_t)dlsym(h, "ncclCommDestroy");
+    n.allgather = (nccl_allgather_t)dlsym(h, "ncclAllGather");
+    n.allreduce = (nccl_allreduce_t)dlsym(h, "ncclAllReduce");
+    n.ok = n.get_id && n.init && n.destroy && n.allgather && n.allreduce;
+  });
+  return n;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ workspace layout
+namespace {
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  int64_t Npad, Tv, C;
+  size_t scal, pos, idx, labels_c, Hc, part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32, total;
+};
+
+Layout layout(int64_t N, int64_t D, int64_t V_local, int world) {
+  Layout L;
+  L.Npad = align_up((size_t)(N > 0 ? N : 1), 128);
+  L.Tv = (V_local + BN - 1) / BN;
+  if (L.Tv < 1) L.Tv = 1;
+  int64_t C = CCE_CHUNK;
+  const int64_t vr = (int64_t)align_up((size_t)(V_local > 0 ? V_local : 1), BN);
+  if (vr < C) C = vr;
+  L.C = C;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  L.scal = take(64);
+  L.pos = take((size_t)(N > 0 ? N : 1) * 4);
+  L.idx = take((size_t)L.Npad * 4);
+  L.labels_c = take((size_t)L.Npad * 4);
+  L.Hc = take((size_t)L.Npad * D * 2);
+  L.part = take((size_t)L.Tv * L.Npad * 8);
+  L.zy_c = take((size_t)L.Npad * 4);
+  L.stats = take((size_t)L.Npad * 16);
+  L.stats_all = take((size_t)world * L.Npad * 16);
+  L.lse_c = take((size_t)L.Npad * 4);
+  L.loss_rows = take((size_t)L.Npad * 4);
+  L.gbuf = take((size_t)L.Npad * L.C * 2);
+  L.dH32 = take((size_t)L.Npad * D * 4);
+  L.total = o;
+  return L;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int grid_for(long long work, int threads, int cap) {
+  long long g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+template <int MODE>
+cce_status launch_gemm(cce_handle* h, const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
+                       cudaStream_t s) {
+  static bool attr_set[4] = {false, false, false, false};
+  if (!attr_set[MODE]) {
+    if (cudaFuncSetAttribute(cce_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES) !=
+        cudaSuccess)
+      return CCE_ERR_CUDA;
+    attr_set[MODE] = true;
+  }
+  cce_gemm_kernel<MODE><<<h->num_sms, GEMM_THREADS, GEMM_SMEM_BYTES, s>>>(a, b, p);
+  h->launches++;
+  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ API
+extern "C" {
+
+void cce_config_default(cce_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->ignore_index = -100;
+  cfg->vocab_total = 0;
+  cfg->vocab_offset = 0;
+  cfg->rank = 0;
+  cfg->world = 1;
+  cfg->nccl_comm = nullptr;
+  cfg->flags = CCE_FLAG_NONE;
+}
+
+const char* cce_status_string(cce_status s) {
+  switch (s) {
+    case CCE_OK: return "CCE_OK";
+    case CCE_ERR_INVALID_VALUE: return "CCE_ERR_INVALID_VALUE";
+    case CCE_ERR_UNSUPPORTED: return "CCE_ERR_UNSUPPORTED";
+    case CCE_ERR_LABEL_RANGE: return "CCE_ERR_LABEL_RANGE";
+    case CCE_ERR_NO_FORWARD: return "CCE_ERR_NO_FORWARD";
+    case CCE_ERR_WORKSPACE: return "CCE_ERR_WORKSPACE";
+    case CCE_ERR_CUDA: return "CCE_ERR_CUDA";
+    case CCE_ERR_NCCL: return "CCE_ERR_NCCL";
+  }
+  return "CCE_ERR_UNKNOWN";
+}
+
+const char* cce_build_info(void) {
+  return "cce sm_100a tcgen05/TMA engine BM=128 BN=256 BK=64 stages=4 chunk=" "8192";
+}
+
+cce_status cce_create(cce_handle** out, const cce_config* cfg) {
+  if (!out || !cfg) return CCE_ERR_INVALID_VALUE;
+  *out = nullptr;
+  if (cfg->vocab_total <= 0 || cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world ||
+      cfg->vocab_offset < 0 || cfg->vocab_offset > cfg->vocab_total)
+    return CCE_ERR_INVALID_VALUE;
+  if ((cfg->world > 1) != (cfg->nccl_comm != nullptr)) return CCE_ERR_INVALID_VALUE;
+  if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return CCE_ERR_UNSUPPORTED;
+  int major = 0, sms = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return CCE_ERR_CUDA;
+  if (major != 10) return CCE_ERR_UNSUPPORTED;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cce_handle* h = new cce_handle();
+  h->cfg = *cfg;
+  h->device = dev;
+  h->num_sms = sms > 0 ? sms : 148;
+  *out = h;
+  return CCE_OK;
+}
+
+cce_status cce_destroy(cce_handle* h) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  delete h;
+  return CCE_OK;
+}
+
+size_t cce_workspace_bytes(const cce_handle* h, int64_t N, int64_t D, int64_t V_local) {
+  if (!h || N < 0 || D <= 0 || V_local < 0) return 0;
+  return layout(N, D, V_local, h->cfg.world).total;
+}
+
+int64_t cce_kernel_launches(const cce_handle* h) { return h ? h->launches : 0; }
+
+cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64_t ldh, const void* W,
+                       int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
+                       int32_t* n_valid, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!h || !loss) return CCE_ERR_INVALID_VALUE;
+  if (N < 0 || D <= 0 || V_local < 0 || ldh < D || ldw < D) return CCE_ERR_INVALID_VALUE;
+  if (N > 0 && (!H || !labels)) return CCE_ERR_INVALID_VALUE;
+  if (V_local > 0 && !W) return CCE_ERR_INVALID_VALUE;
+  if (h->cfg.vocab_offset + V_local > h->cfg.vocab_total) return CCE_ERR_INVALID_VALUE;
+  if (D % 64 != 0 || N > (1LL << 30) || V_local > (1LL << 30)) return CCE_ERR_UNSUPPORTED;
+  if ((N > 0 && !aligned16(H)) || (V_local > 0 && !aligned16(W)) || (ldh * 2) % 16 || (ldw * 2) % 16)
+    return CCE_ERR_UNSUPPORTED;
+  const Layout L = layout(N, D, V_local, h->cfg.world);
+  if (!workspace || workspace_bytes < L.total || !aligned16(workspace)) return CCE_ERR_WORKSPACE;
+  if (!get_encode()) return CCE_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  void* ws = workspace;
+  int* nvp = at<int>(ws, L.scal);
+  int* errp = nvp + 1;
+
+  // a0: label scan + compaction
+  // clear n_valid only: the error word is sticky until cce_get_error
+  if (cudaMemsetAsync(nvp, 0, 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+  if (cudaMemsetAsync(at<float>(ws, L.zy_c), 0, (size_t)L.Npad * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+  if (N > 0) {
+    k_label_scan<<<1, 1024, 0, s>>>(labels, (int)N, h->cfg.ignore_index, (long long)h->cfg.vocab_total,
+                                    at<int>(ws, L.pos), at<int>(ws, L.idx), at<int>(ws, L.labels_c), nvp, errp);
+    h->launches++;
+    k_gather_rows<<<grid_for((long long)L.Npad * D / 8, 256, 4 * h->num_sms), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(H), ldh, (int)D, (int)L.Npad, at<int>(ws, L.idx), nvp,
+        at<__nv_bfloat16>(ws, L.Hc));
+    h->launches++;
+  }
+
+  // a1 + a2: tcgen05 logit tiles with the online-softmax epilogue
+  if (N > 0 && V_local > 0) {
+    CUtensorMap tA, tB;
+    if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, BM)) return CCE_ERR_CUDA;
+    if (!make_map(&tB, W, D, V_local, ldw, BN)) return CCE_ERR_CUDA;
+    GemmParams p{};
+    p.D = (int)D;
+    p.V_local = (int)V_local;
+    p.Npad = (int)L.Npad;
+    p.c0 = 0;
+    p.width = (int)V_local;
+    p.C = (int)L.C;
+    p.vocab_offset = (int)h->cfg.vocab_offset;
+    p.n_valid = nvp;
+    p.labels_c = at<int>(ws, L.labels_c);
+    p.part = at<float2>(ws, L.part);
+    p.zy_c = at<float>(ws, L.zy_c);
+    cce_status st = launch_gemm<MODE_FWD>(h, tA, tB, p, s);
+    if (st != CCE_OK) return st;
+  }
+
+  // a4: merge tiles -> per-rank stats; a9: allgather across vocabulary shards
+  float4* stats = at<float4>(ws, L.stats);
+  if (N > 0) {
+    // an empty shard (V_local == 0) merges zero tiles: (m=-inf, d=0, z_y=0) for every row
+    k_merge_tiles<<<grid_for(L.Npad, 256, 8 * h->num_sms), 256, 0, s>>>(
+        at<float2>(ws, L.part), V_local > 0 ? (int)L.Tv : 0, (int)L.Npad, at<float>(ws, L.zy_c), nvp, stats);
+    h->launches++;
+  }
+  const float4* stats_all = stats;
+  if (h->cfg.world > 1) {
+    Nccl& n = nccl();
+    if (!n.ok) return CCE_ERR_NCCL;
+    if (n.allgather(stats, at<float4>(ws, L.stats_all), (size_t)L.Npad * 4, kNcclFloat32, h->cfg.nccl_comm, s) != 0)
+      return CCE_ERR_NCCL;
+    stats_all = at<float4>(ws, L.stats_all);
+  }
+  if (N > 0) {
+    k_finalize<<<grid_for(N, 256, 8 * h->num_sms), 256, 0, s>>>(stats_all, h->cfg.world, (int)L.Npad,
+                                                                at<int>(ws, L.pos), (int)N, lse, at<float>(ws, L.lse_c),
+                                                                at<float>(ws, L.loss_rows));
+    h->launches++;
+  }
+  k_loss<<<1, 1024, 0, s>>>(at<float>(ws, L.loss_rows), nvp, errp, loss, n_valid);
+  h->launches++;
+  if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
+
+  h->have_fwd = true;
+  h->W = W;
+  h->N = N;
+  h->D = D;
+  h->V_local = V_local;
+  h->ldw = ldw;
+  h->ws = workspace;
+  h->ws_bytes = workspace_bytes;
+  return CCE_OK;
+}
+
+cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, void* stream) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  if (!h->have_fwd) return CCE_ERR_NO_FORWARD;
+  if (!dloss || (h->N > 0 && !dH) || (h->V_local > 0 && !dW)) return CCE_ERR_INVALID_VALUE;
+  if ((dH && !aligned16(dH)) || (dW && !aligned16(dW))) return CCE_ERR_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t N = h->N, D = h->D, V_local = h->V_local;
+  const Layout L = layout(N, D, V_local, h->cfg.world);
+  void* ws = h->ws;
+  int* nvp = at<int>(ws, L.scal);
+  float* dH32 = at<float>(ws, L.dH32);
+
+  if (V_local > 0 && N > 0) {
+    CUtensorMap mHcK, mWK, mHcMN, mGMN, mWMN, mGK;
+    void* Hc = at<void>(ws, L.Hc);
+    void* G = at<void>(ws, L.gbuf);
+    if (!make_map(&mHcK, Hc, D, L.Npad, D, BM) || !make_map(&mWK, h->W, D, V_local, h->ldw, BN) ||
+        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, L.Npad, L.C, 64) ||
+        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, L.Npad, L.C, BN))
+      return CCE_ERR_CUDA;
+    GemmParams p{};
+    p.D = (int)D;
+    p.V_local = (int)V_local;
+    p.Npad = (int)L.Npad;
+    p.C = (int)L.C;
+    p.vocab_offset = (int)h->cfg.vocab_offset;
+    p.n_valid = nvp;
+    p.labels_c = at<int>(ws, L.labels_c);
+    p.lse_c = at<float>(ws, L.lse_c);
+    p.dloss = dloss;
+    p.gbuf = at<__nv_bfloat16>(ws, L.gbuf);
+    p.dW = static_cast<__nv_bfloat16*>(dW);
+    p.dH32 = dH32;
+    for (int64_t c0 = 0; c0 < V_local; c0 += L.C) {
+      p.c0 = (int)c0;
+      p.width = (int)((V_local - c0) < L.C ? (V_local - c0) : L.C);
+      p.dh_accumulate = c0 > 0 ? 1 : 0;
+      cce_status st;
+      // a5 + a6: recompute the logit tile, G = s (softmax - onehot) in the epilogue -> Gbuf (bf16)
+      if ((st = launch_gemm<MODE_G>(h, mHcK, mWK, p, s)) != CCE_OK) return st;
+      // a7: dW[chunk] = G^T Hc
+      if ((st = launch_gemm<MODE_DW>(h, mHcMN, mGMN, p, s)) != CCE_OK) return st;
+      // a8: dH += G W[chunk]   (fp32, chunk order)
+      if ((st = launch_gemm<MODE_DH>(h, mWMN, mGK, p, s)) != CCE_OK) return st;
+    }
+  } else if (V_local > 0 && N == 0) {
+    // no rows: dW = 0
+    if (cudaMemsetAsync(dW, 0, (size_t)V_local * D * 2, s) != cudaSuccess) return CCE_ERR_CUDA;
+  }
+  if (N > 0) {
+    if (V_local == 0 && cudaMemsetAsync(dH32, 0, (size_t)L.Npad * D * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+    if (h->cfg.world > 1) {
+      // a10: dH partials summed over the vocabulary shards
+      Nccl& n = nccl();
+      if (!n.ok) return CCE_ERR_NCCL;
+      if (n.allreduce(dH32, dH32, (size_t)L.Npad * D, kNcclFloat32, kNcclSum, h->cfg.nccl_comm, s) != 0)
+        return CCE_ERR_NCCL;
+    }
+    k_scatter_dH<<<grid_for((long long)N * D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(dH32, at<int>(ws, L.pos), (int)N,
+                                                                                     (int)D,
+                                                                                     static_cast<__nv_bfloat16*>(dH));
+    h->launches++;
+  }
+  if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
+  return CCE_OK;
+}
+
+cce_status cce_get_error(cce_handle* h, void* stream) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!h->ws) return CCE_OK;
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world);
+  int* errp = at<int>(h->ws, L.scal) + 1;
+  int err = 0;
+  if (cudaMemcpyAsync(&err, errp, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CCE_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return CCE_ERR_CUDA;
+  if (err) {
+    if (cudaMemsetAsync(errp, 0, 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+    return CCE_ERR_LABEL_RANGE;
+  }
+  return CCE_OK;
+}
+
+size_t cce_host_staging_bytes(int64_t N, int64_t D) {
+  if (N < 0 || D <= 0) return 0;
+  return align_up((size_t)N * D * 2, 256) + align_up((size_t)(N > 0 ? N : 1) * 4, 256) + 256;
+}
+
+cce_status cce_step_host(cce_handle* h, const void* H_host, int64_t N, int64_t D, const int32_t* labels_host,
+                         const void* W, int64_t V_local, int64_t ldw, float* loss_host, void* dH, void* dW,
+                         void* dev_inputs, size_t dev_inputs_bytes, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  if (!h || !loss_host || (N > 0 && (!H_host || !labels_host))) return CCE_ERR_INVALID_VALUE;
+  if (N < 0 || D <= 0) return CCE_ERR_INVALID_VALUE;
+  if (!dev_inputs || dev_inputs_bytes < cce_host_staging_bytes(N, D) || !aligned16(dev_inputs))
+    return CCE_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(dev_inputs);
+  void* Hd = base;
+  int32_t* yd = reinterpret_cast<int32_t*>(base + align_up((size_t)N * D * 2, 256));
+  float* scal = reinterpret_cast<float*>(base + align_up((size_t)N * D * 2, 256) + align_up((size_t)(N > 0 ? N : 1) * 4, 256));
+  float* loss_d = scal;
+  float* dloss_d = scal + 1;
+  if (N > 0) {
+    if (cudaMemcpyAsync(Hd, H_host, (size_t)N * D * 2, cudaMemcpyHostToDevice, s) != cudaSuccess) return CCE_ERR_CUDA;
+    if (cudaMemcpyAsync(yd, labels_host, (size_t)N * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return CCE_ERR_CUDA;
+  }
+  cce_status st = cce_forward(h, N > 0 ? Hd : nullptr, N, D, D, W, V_local, ldw, N > 0 ? yd : nullptr, loss_d, nullptr,
+                              nullptr, workspace, workspace_bytes, stream);
+  if (st != CCE_OK) return st;
+  k_set_scalar<<<1, 1, 0, s>>>(dloss_d, 1.0f);
+  h->launches++;
+  st = cce_backward(h, dloss_d, dH, dW, stream);
+  if (st != CCE_OK) return st;
+  if (cudaMemcpyAsync(loss_host, loss_d, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CCE_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return CCE_ERR_CUDA;
+  return CCE_OK;
+}
+
+cce_status cce_nccl_unique_id(void* id_out) {
+  if (!id_out) return CCE_ERR_INVALID_VALUE;
+  Nccl& n = nccl();
+  if (!n.ok) return CCE_ERR_NCCL;
+  return n.get_id(static_cast<NcclId*>(id_out)) == 0 ? CCE_OK : CCE_ERR_NCCL;
+}
+
+cce_status cce_nccl_comm_init(void** comm_out, int32_t world, const void* id, int32_t rank) {
+  if (!comm_out || !id || world < 1 || rank < 0 || rank >= world) return CCE_ERR_INVALID_VALUE;
+  Nccl& n = nccl();
+  if (!n.ok) return CCE_ERR_NCCL;
+  NcclId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  return n.init(comm_out, world, uid, rank) == 0 ? CCE_OK : CCE_ERR_NCCL;
+}
+
+cce_status cce_nccl_comm_destroy(void* comm) {
+  if (!comm) return CCE_ERR_INVALID_VALUE;
+  Nccl& n = nccl();
+  if (!n.ok) return CCE_ERR_NCCL;
+  return n.destroy(comm) == 0 ? CCE_OK : CCE_ERR_NCCL;
+}
+
+}  // extern "C"

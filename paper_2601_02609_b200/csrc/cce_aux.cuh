@@ -1,0 +1,191 @@
+// cce_aux.cuh -- the non-GEMM steps of the CCE hot path (SURVEY 8a rows a0, a4,
+// a8-scatter): label scan + compaction, row gather, the online-softmax merge of
+// per-tile partials, the deterministic mean loss and the dH scatter.
+// All are O(N*D) or O(N*V/256) HBM-bound helpers around the tensor-core engine.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace cce {
+
+// a0: range check + stable compaction of the non-ignored rows (P:2076-2079:
+// rows with y == ignore_index are skipped; the mean divides by their count,
+// P:899).  One block of 1024 threads, each owning a contiguous segment of the
+// labels, so the compact order equals the original row order.
+// Out-of-range labels set err and are treated as ignored.
+__global__ void __launch_bounds__(1024) k_label_scan(const int32_t* __restrict__ labels, int N, int ignore_index,
+                                                     long long vocab_total, int* __restrict__ pos,
+                                                     int* __restrict__ idx, int* __restrict__ labels_c,
+                                                     int* __restrict__ n_valid_out, int* __restrict__ err_out) {
+  __shared__ int warp_tot[32];
+  const int t = threadIdx.x;
+  const int per = (N + 1023) / 1024;
+  const int b = min(N, t * per), e = min(N, b + per);
+  int cnt = 0, bad = 0;
+  for (int n = b; n < e; ++n) {
+    const int y = labels[n];
+    if (y == ignore_index) continue;
+    if (y < 0 || (long long)y >= vocab_total) { bad = 1; continue; }
+    ++cnt;
+  }
+  // block exclusive scan of cnt
+  const int lane = t & 31, w = t >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int s = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += v;
+    }
+    warp_tot[lane] = s;  // inclusive over warps
+  }
+  __syncthreads();
+  int off = incl - cnt + (w > 0 ? warp_tot[w - 1] : 0);
+  for (int n = b; n < e; ++n) {
+    const int y = labels[n];
+    const bool v = (y != ignore_index) && y >= 0 && (long long)y < vocab_total;
+    if (v) {
+      pos[n] = off;
+      idx[off] = n;
+      labels_c[off] = y;
+      ++off;
+    } else {
+      pos[n] = -1;
+    }
+  }
+  const int any_bad = __syncthreads_or(bad);
+  if (t == 0) {
+    *n_valid_out = warp_tot[31];
+    if (any_bad) atomicOr(err_out, 1);
+  }
+}
+
+// Gather the valid rows of H into the compact, dense, 16-byte aligned Hc so TMA
+// tiles are contiguous; rows [n_valid, round_up(n_valid,128)) are zeroed (they
+// are read as K-padding by the dW contraction).  Ignored rows of H are never read.
+__global__ void k_gather_rows(const __nv_bfloat16* __restrict__ H, long long ldh, int D, int Npad,
+                              const int* __restrict__ idx, const int* __restrict__ n_valid,
+                              __nv_bfloat16* __restrict__ Hc) {
+  const int nv = *n_valid;
+  const int rows = min(Npad, ((nv + 127) / 128) * 128);
+  const int vec_per_row = D / 8;
+  const long long total = (long long)rows * vec_per_row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / vec_per_row), c = (int)(i % vec_per_row);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < nv) v = *reinterpret_cast<const uint4*>(H + (long long)idx[r] * ldh + c * 8);
+    *reinterpret_cast<uint4*>(Hc + (long long)r * D + c * 8) = v;
+  }
+}
+
+// a4 (local part): merge the per-vocabulary-tile (m, d) partials of each valid
+// row in tile order with the online-softmax merge:
+// m = max_t m_t, d = sum_t d_t exp(m_t - m).  Out: (m, d, z_y) per compact row.
+__global__ void k_merge_tiles(const float2* __restrict__ part, int Tv, int Npad, const float* __restrict__ zy_c,
+                              const int* __restrict__ n_valid, float4* __restrict__ stats) {
+  const int nv = *n_valid;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
+    float m = -INFINITY;
+    for (int t = 0; t < Tv; ++t) m = fmaxf(m, part[(size_t)t * Npad + i].x);
+    float d = 0.f;
+    if (m > -INFINITY) {
+      for (int t = 0; t < Tv; ++t) {
+        const float2 pd = part[(size_t)t * Npad + i];
+        d += pd.y * expf(pd.x - m);
+      }
+    }
+    stats[i] = make_float4(m, d, zy_c[i], 0.f);
+  }
+}
+
+// a4 (global part) + a9 combine: merge the per-rank stats in rank order (empty
+// shards contribute m=-inf, d=0), lse = m + log d (Theorem), per-row loss
+// lse - z_y.  Ignored rows get lse = 0 (reading R4).
+__global__ void k_finalize(const float4* __restrict__ stats_all, int world, int Npad, const int* __restrict__ pos,
+                           int N, float* __restrict__ lse_out, float* __restrict__ lse_c,
+                           float* __restrict__ loss_rows) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    const int i = pos[n];
+    if (i < 0) {
+      if (lse_out) lse_out[n] = 0.f;
+      continue;
+    }
+    float m = -INFINITY, zy = 0.f;
+    for (int r = 0; r < world; ++r) {
+      const float4 s = stats_all[(size_t)r * Npad + i];
+      m = fmaxf(m, s.x);
+      zy += s.z;
+    }
+    float d = 0.f;
+    for (int r = 0; r < world; ++r) {
+      const float4 s = stats_all[(size_t)r * Npad + i];
+      if (s.y > 0.f) d += s.y * expf(s.x - m);
+    }
+    const float lse = m + logf(d);
+    lse_c[i] = lse;
+    loss_rows[i] = lse - zy;
+    if (lse_out) lse_out[n] = lse;
+  }
+}
+
+// Mean loss over the valid rows in a fixed reduction order (deterministic).
+// loss = 0 when n_valid == 0 (reading R2); NaN when a label was out of range.
+__global__ void __launch_bounds__(1024) k_loss(const float* __restrict__ loss_rows, const int* __restrict__ n_valid,
+                                               const int* __restrict__ err, float* __restrict__ loss,
+                                               int32_t* __restrict__ n_valid_out) {
+  __shared__ float red[32];
+  const int nv = *n_valid;
+  float s = 0.f;
+  for (int i = threadIdx.x; i < nv; i += 1024) s += loss_rows[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = red[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+      float l = nv > 0 ? s / (float)nv : 0.f;
+      if (*err) l = __int_as_float(0x7fc00000);
+      *loss = l;
+      if (n_valid_out) *n_valid_out = nv;
+    }
+  }
+}
+
+// a8: dH rows back to the original positions in bf16; ignored rows are bit-zero.
+__global__ void k_scatter_dH(const float* __restrict__ dH32, const int* __restrict__ pos, int N, int D,
+                             __nv_bfloat16* __restrict__ dH) {
+  const int vec_per_row = D / 8;
+  const long long total = (long long)N * vec_per_row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(i / vec_per_row), c = (int)(i % vec_per_row);
+    const int r = pos[n];
+    uint4 out = make_uint4(0, 0, 0, 0);
+    if (r >= 0) {
+      const float4 a = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8);
+      const float4 b = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8 + 4);
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y), p1 = __floats2bfloat162_rn(a.z, a.w);
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(b.x, b.y), p3 = __floats2bfloat162_rn(b.z, b.w);
+      out.x = *reinterpret_cast<uint32_t*>(&p0);
+      out.y = *reinterpret_cast<uint32_t*>(&p1);
+      out.z = *reinterpret_cast<uint32_t*>(&p2);
+      out.w = *reinterpret_cast<uint32_t*>(&p3);
+    }
+    *reinterpret_cast<uint4*>(dH + (long long)n * D + c * 8) = out;
+  }
+}
+
+__global__ void k_set_scalar(float* p, float v) { *p = v; }
+
+}  // namespace cce

@@ -1,0 +1,155 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 CPU oracle, element
+by element on the same seeded inputs.  Tolerances are north_star's (loss abs
+2e-3, LSE rel 1e-3, dH/dW rel Frobenius 1e-2; n_valid and ignore masks exact)."""
+import numpy as np
+import pytest
+
+import oracle
+import workload
+from cce_testutil import assert_parity, run_gpu, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    return torch.device("cuda:0")
+
+
+def _check(p, dev, dloss=1.0):
+    H, W, y = to_dev(p, dev)
+    got = run_gpu(H, W, y, dloss=dloss)
+    ref = oracle.cce(p["H"], p["W"], p["labels"], dloss=dloss)
+    assert_parity(got, ref, p["labels"])
+    return got, ref
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4, 42])
+def test_tiny_config(dev, seed):
+    """configs[0]: N=64, D=64, V=1000 (tail tile of 232), 10% ignored."""
+    _check(workload.make_config("tiny", seed=seed), dev)
+
+
+@pytest.mark.parametrize("N,D,V,ign", [
+    (700, 128, 3000, "bern40"),        # ragged rows (5.5 tiles), ragged vocab (11.7 tiles)
+    (257, 64, 256, "none"),             # exactly one vocab tile, one ragged row
+    (129, 192, 20000, "bern30"),        # 3 backward chunks, ragged last chunk
+    (384, 896, 9000, "bern40"),         # Qwen hidden size, 2 chunks
+])
+def test_multi_tile_shapes(dev, N, D, V, ign):
+    p = workload.make_problem(N, D, V, seed=N + V, ignore=ign)
+    _check(p, dev)
+
+
+@pytest.mark.parametrize("regime", ["peaked", "extreme", "zero"])
+def test_value_regimes(dev, regime):
+    p = workload.make_problem(300, 128, 5000, seed=11, ignore="bern40", regime=regime)
+    _check(p, dev)
+
+
+def test_upstream_gradient_scaling(dev):
+    p = workload.make_problem(200, 64, 2000, seed=5, ignore="bern20")
+    _check(p, dev, dloss=0.37)
+
+
+def test_all_ignored(dev):
+    p = workload.make_problem(150, 64, 700, seed=6, ignore="all")
+    H, W, y = to_dev(p, dev)
+    got = run_gpu(H, W, y)
+    assert got["n_valid"] == 0 and got["loss"] == 0.0
+    assert np.all(got["dH_bits"] == 0) and np.all(got["dW_bits"] == 0) and np.all(got["lse_bits"] == 0)
+
+
+def test_single_valid_token(dev):
+    p = workload.make_problem(130, 64, 1500, seed=7, ignore="all")
+    p["labels"][77] = 1234
+    _check(p, dev)
+
+
+def test_nan_in_ignored_rows_does_not_leak(dev):
+    """Reading R14: ignored rows are never read -- NaN there leaves outputs bit-identical."""
+    p = workload.make_problem(300, 128, 2500, seed=8, ignore="bern40")
+    H, W, y = to_dev(p, dev)
+    a = run_gpu(H, W, y)
+    q = dict(p)
+    Hn = p["H"].copy()
+    Hn[p["labels"] == -100] = 0x7FC0          # bf16 NaN
+    q["H"] = Hn
+    H2, _, _ = to_dev(q, dev)
+    b = run_gpu(H2, W, y)
+    assert a["loss"] == b["loss"]
+    for k in ("lse_bits", "dH_bits", "dW_bits"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_deterministic(dev):
+    p = workload.make_problem(500, 128, 9000, seed=9, ignore="bern40")
+    H, W, y = to_dev(p, dev)
+    a = run_gpu(H, W, y)
+    b = run_gpu(H, W, y)
+    assert a["loss"] == b["loss"]
+    for k in ("lse_bits", "dH_bits", "dW_bits"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_shift_invariance_bigshift(dev):
+    """SURVEY pin 9 on the GPU: D = 895 + 1 constant column, c = 80."""
+    p = workload.make_problem(256, 896, 3000, seed=10, ignore="bern40")
+    H = p["H"].copy(); W = p["W"].copy()
+    H[:, -1] = 0x3F80          # 1.0
+    W[:, -1] = 0x42A0          # 80.0
+    q = {"H": H, "W": W, "labels": p["labels"]}
+    _check(q, dev)
+
+
+def test_label_out_of_range_reports_error(dev):
+    import torch
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(100, 64, 500, seed=12, ignore="bern10")
+    p["labels"][3] = 500
+    H, W, y = to_dev(p, dev)
+    h = cce.CCEHandle(vocab_total=500)
+    loss, lse, nv = h.forward(H, W, y)
+    assert cce.cce_get_error(h.h) == 3          # CCE_ERR_LABEL_RANGE
+    assert np.isnan(loss.item())
+    assert cce.cce_get_error(h.h) == 0          # cleared
+    h.close()
+
+
+def test_autograd_entry_point(dev):
+    import torch
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(200, 128, 3000, seed=13, ignore="bern40")
+    H, W, y = to_dev(p, dev)
+    H.requires_grad_(True); W.requires_grad_(True)
+    loss = cce.linear_cross_entropy(H, W, y)
+    (2.0 * loss).backward()
+    ref = oracle.cce(p["H"], p["W"], p["labels"], dloss=2.0)
+    from cce_testutil import bf16_to_f64, rel_fro
+    assert abs(loss.item() - ref["loss"]) <= 2e-3
+    assert rel_fro(bf16_to_f64(H.grad), ref["dH"]) <= 1e-2
+    assert rel_fro(bf16_to_f64(W.grad), ref["dW"]) <= 1e-2
+
+
+def test_step_host_matches_device_path(dev):
+    import torch
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(300, 128, 4000, seed=14, ignore="bern40")
+    _, W, _ = to_dev(p, dev)
+    Hh = torch.from_numpy(p["H"].view(np.int16)).view(torch.bfloat16).pin_memory()
+    yh = torch.from_numpy(p["labels"]).pin_memory()
+    h = cce.CCEHandle(vocab_total=4000)
+    ws = h.workspace(300, 128, 4000, dev)
+    st = torch.empty(cce.cce_host_staging_bytes(300, 128), dtype=torch.uint8, device=dev)
+    dH = torch.empty((300, 128), dtype=torch.bfloat16, device=dev)
+    dW = torch.empty((4000, 128), dtype=torch.bfloat16, device=dev)
+    loss = cce.cce_step_host(h.h, Hh, yh, W, dH, dW, st, ws)
+    ref = oracle.cce(p["H"], p["W"], p["labels"])
+    assert abs(loss - ref["loss"]) <= 2e-3
+    from cce_testutil import bf16_to_f64, rel_fro
+    assert rel_fro(bf16_to_f64(dH), ref["dH"]) <= 1e-2
+    assert rel_fro(bf16_to_f64(dW), ref["dW"]) <= 1e-2
+    h.close()
