@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Bench: fused linear cross-entropy forward+backward (Cut Cross-Entropy, arxiv
+2601.02609) at the Qwen2.5-0.5B head shape on B200, through the C ABI.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen05b] [--impl reference]
+
+One step = cce_forward + cce_backward (dloss = 1) over one batch of synthetic
+inputs already resident in HBM.  N > 1 (torchrun): the vocabulary is sharded
+(rank r owns W rows [off_r, off_r + V/N)); H and labels are replicated; per-row
+(max, sum-exp, target-logit) stats are allgathered and dH is all-reduced with
+NCCL inside the library.  Total work is fixed as N grows ("strong" scaling).
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on
+the launching stream, with a 256 MB L2 flush (outside the events) between
+steps; barrier + synchronize on both sides; max over ranks.
+Prints one JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused linear-CE fwd+bwd tokens/s and % BF16 tensor peak, V=151936, 1/2/4/8 GPU"
+WORKLOAD_DESC = {
+    "qwen05b": "Qwen2.5-0.5B head: N=8x1024=8192, D=896, V=151936 bf16, 40% packed padding ignored",
+    "tiny": "tiny CCE: N=64, D=64, V=1000, 10% ignore_index",
+    "mem": "paper memory example: N=4x4096=16384, D=2048, V=151936 bf16",
+    "llama8b": "Llama-3-8B head: N=16384, D=4096, V=128256 bf16",
+    "qwen7b": "Qwen2.5-7B head: N=32768, D=3584, V=152064 bf16",
+}
+
+
+def peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written), else the
+    profiling guide's fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return {"bf16_tflops": float(d["bf16_tflops"]), "bf16_tflops_sustained": float(d["bf16_tflops_sustained"]),
+                "hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_baseline(p, n_tokens_target_s=15.0):
+    """The oracle as it stands (fp64, OpenMP on all host cores) on a bounded
+    sample of the same workload: the first n tokens of the batch at full V, D."""
+    import numpy as np
+
+    import oracle
+    oracle.build()
+    lab = p["labels"]
+
+    def run(n):
+        t = time.perf_counter()
+        oracle.cce(p["H"][:n], p["W"], lab[:n], dloss=1.0)
+        return time.perf_counter() - t
+
+    n0 = 32
+    t0 = run(n0)
+    n = int(max(n0, min(len(lab), n0 * n_tokens_target_s / max(t0, 1e-3))))
+    t = run(n) if n != n0 else t0
+    nv = int((lab[:n] != -100).sum())
+    return {"value": n / t, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"first {n} tokens of the batch ({nv} valid) at full V={p['W'].shape[0]}, D={p['H'].shape[1]}: "
+                      f"fp64 forward+backward in {t:.1f} s",
+            "seconds": t}
+
+
+def reference_arm(args):
+    """--impl reference: the oracle (the reference arm for this tier), timed on the
+    host cores, on bounded samples of the same workload, rank 0 only."""
+    import numpy as np
+
+    import oracle
+    import workload
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    c = workload.CONFIGS[args.config]
+    p = workload.make_config(args.config, seed=args.seed)
+    oracle.build()
+    # size one step to ~3 s of CPU work
+    t = time.perf_counter()
+    oracle.cce(p["H"][:16], p["W"], p["labels"][:16])
+    t16 = time.perf_counter() - t
+    n = int(max(16, min(c.N, 16 * 3.0 / max(t16, 1e-3))))
+    for _ in range(args.warmup):
+        oracle.cce(p["H"][:n], p["W"], p["labels"][:n])
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.cce(p["H"][:n], p["W"], p["labels"][:n])
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    val = n * args.steps / tot
+    nv = int((p["labels"][:n] != -100).sum())
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD_DESC[args.config], "sample_tokens": n},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"each step: first {n} tokens ({nv} valid) at full V, D; fp64 fwd+bwd"},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="qwen05b")
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--flags", type=int, default=0, help="cce_config.flags (2 = per-chunk backward schedule)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_02609_b200 as cce
+    import workload
+    from paper_2601_02609_b200 import build as cce_build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            print(json.dumps({"error": "--gpus N > 1 must be launched with torchrun"}), flush=True)
+            return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        cce_build.build()
+    if world > 1:
+        dist.barrier()
+    cce.lib()
+
+    c = workload.CONFIGS[args.config]
+    lo = rank * c.V // world
+    hi = (rank + 1) * c.V // world
+    p = workload.make_config(args.config, seed=args.seed, w_rows=(lo, hi))
+    n_valid = int((p["labels"] != -100).sum())
+    H = torch.from_numpy(p["H"].view(np.int16)).view(torch.bfloat16).to(dev)
+    W = torch.from_numpy(p["W"].view(np.int16)).view(torch.bfloat16).to(dev)
+    y = torch.from_numpy(p["labels"]).to(dev)
+
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(cce.cce_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = cce.cce_nccl_comm_init(world, bytes(uid.cpu().numpy().tobytes()), rank)
+    h = cce.CCEHandle(vocab_total=c.V, vocab_offset=lo, rank=rank, world=world, nccl_comm=comm, flags=args.flags)
+    ws = h.workspace(c.N, c.D, hi - lo, dev)
+    loss = torch.empty((), dtype=torch.float32, device=dev)
+    lse = torch.empty(c.N, dtype=torch.float32, device=dev)
+    nvt = torch.empty((), dtype=torch.int32, device=dev)
+    dH = torch.empty((c.N, c.D), dtype=torch.bfloat16, device=dev)
+    dW = torch.empty((hi - lo, c.D), dtype=torch.bfloat16, device=dev)
+    one = torch.ones((), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        cce.cce_forward(h.h, H, W, y, loss, lse, nvt, ws, stream)
+        cce.cce_backward(h.h, one, dH, dW, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # sanity: finite loss, non-zero finite grads
+    assert math.isfinite(loss.item()) and int(nvt.item()) == n_valid
+    assert torch.isfinite(dW.float()).all() and dW.float().abs().sum().item() > 0
+
+    cce.cce_profile_enable(h.h, True)
+    cce.cce_profile_read(h.h, reset=True)
+    l0 = cce.cce_kernel_launches(h.h)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        if not args.no_flush:
+            flush.zero_()                     # L2 flush (256 MB > 126 MB L2), outside the events
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    launches = cce.cce_kernel_launches(h.h) - l0
+    prof = cce.cce_profile_read(h.h, reset=True)
+    cce.cce_profile_enable(h.h, False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+
+    pk = peaks()
+    credited = 6.0 * n_valid * c.D * c.V              # whole-job credited FLOPs per step
+    value = c.N * args.steps / (tot_ms / 1e3)           # all tokens per second, whole job
+    frac_credited = credited / (ms_per_step / 1e3) / (world * pk["bf16_tflops"] * 1e12)
+
+    # roofline of the dominant kernel class (largest share of the timed region)
+    V_local = hi - lo
+    per_gemm = 2.0 * n_valid * c.D * V_local
+    fused_bwd = prof["bwd_dW"][1] == 0 and prof["bwd_dH"][1] == 0
+    alg_flops = {"fwd_logits_lse": per_gemm, "bwd": (3.0 if fused_bwd else 1.0) * per_gemm,
+                 "bwd_dW": per_gemm, "bwd_dH": per_gemm}
+    dom = max(alg_flops, key=lambda k: prof[k][0])
+    dom_ms, dom_n = prof[dom]
+    per_launch_flops = alg_flops[dom] * args.steps / max(dom_n, 1)
+    achieved = per_launch_flops / (dom_ms / max(dom_n, 1) / 1e3) / 1e12
+    traffic = None
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = summ.get("per_class_dram_bytes_per_launch", {}).get(dom)
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"], "traffic": traffic,
+                "peak_source": pk["source"] + " bf16 burst",
+                "flops_per_launch": per_launch_flops, "avg_launch_ms": dom_ms / max(dom_n, 1),
+                "share_of_step": dom_ms / max(sum(v[0] for v in prof.values()), 1e-9)}
+
+    # end-to-end through the C ABI with HOST buffers (H, labels copied in; loss copied out)
+    e2e = None
+    if not args.no_e2e:
+        Hh = torch.from_numpy(p["H"].view(np.int16)).view(torch.bfloat16).pin_memory()
+        yh = torch.from_numpy(p["labels"]).pin_memory()
+        stage = torch.empty(cce.cce_host_staging_bytes(c.N, c.D), dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            cce.cce_step_host(h.h, Hh, yh, W, dH, dW, stage, ws, stream)
+        if world > 1:
+            dist.barrier()
+        e0 = time.perf_counter()
+        for _ in range(args.steps):
+            cce.cce_step_host(h.h, Hh, yh, W, dH, dW, stage, ws, stream)
+        te = torch.tensor([time.perf_counter() - e0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": c.N * args.steps / float(te.item()), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(Hh.numel() * 2 + yh.numel() * 4), "d2h_bytes_per_step": 4,
+               "note": "cce_step_host: pinned H + labels H2D, fwd+bwd, loss D2H, stream sync; W resident (a parameter)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(workload.make_config(args.config, seed=args.seed))
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC[args.config], "N": c.N, "D": c.D, "V": c.V, "n_valid": n_valid,
+                       "seed": args.seed, "parallelism": f"vocab-sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "256 MB L2 flush between timed steps" if not args.no_flush else "no flush"},
+            "frac_of_peak_credited": frac_credited,
+            "credited_tflops_per_gpu": credited / (ms_per_step / 1e3) / world / 1e12,
+            "credited_flops_per_step": credited,
+            "valid_tokens_per_s": n_valid * args.steps / (tot_ms / 1e3),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "wall_s_timed_region": wall,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if comm is not None:
+        cce.cce_nccl_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

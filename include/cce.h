@@ -37,9 +37,9 @@
  *    The library never allocates device memory on the hot path.
  *  - Errors: host-detectable errors return a status immediately and enqueue
  *    nothing.  Device-detected label errors (a label that is neither
- *    ignore_index nor in [0, vocab_total)) set a sticky device flag and make
- *    `loss` NaN; they are reported by cce_get_error (the only synchronising
- *    call besides cce_step_host).
+ *    ignore_index nor in [0, vocab_total)) set a device flag in the workspace
+ *    and make `loss` NaN; cce_get_error reports the flag of the most recent
+ *    forward (it is the only synchronising call besides cce_step_host).
  *  - No host synchronisation inside cce_forward / cce_backward.
  *  - Determinism: outputs are bit-reproducible run to run (no atomics on
  *    outputs, fixed-order reductions).
@@ -71,6 +71,10 @@ typedef enum {
 
 /* flags */
 #define CCE_FLAG_NONE 0u
+/* Backward schedule: 0 (default) = one persistent work-queue launch for all
+ * chunks; CCE_FLAG_BWD_PER_CHUNK = three launches per vocabulary chunk (the
+ * straightforward schedule, kept for A/B measurements and tests). */
+#define CCE_FLAG_BWD_PER_CHUNK 2u
 
 typedef struct {
   int32_t ignore_index;   /* label value that marks a skipped row; -100 in the paper */
@@ -126,9 +130,9 @@ cce_status cce_forward(cce_handle *h,
  */
 cce_status cce_backward(cce_handle *h, const float *dloss, void *dH, void *dW, void *stream);
 
-/* Synchronises `stream` and returns CCE_ERR_LABEL_RANGE if any forward on
- * this handle saw an out-of-range label since the last call (then clears
- * the flag), else CCE_OK. */
+/* Synchronises `stream` and returns CCE_ERR_LABEL_RANGE if the most recent
+ * cce_forward on this handle saw an out-of-range label (the offending rows are
+ * treated as ignored and loss is NaN), else CCE_OK.  Clears the flag. */
 cce_status cce_get_error(cce_handle *h, void *stream);
 
 /*
@@ -156,6 +160,17 @@ cce_status cce_nccl_comm_destroy(void *comm);
 
 /* Human-readable status. */
 const char *cce_status_string(cce_status s);
+
+/* Optional per-kernel-class timing for roofline reporting.  When enabled, every
+ * kernel the handle launches is bracketed by CUDA events on its stream (no host
+ * sync).  cce_profile_read synchronises on the recorded events and returns, per
+ * class, the summed device milliseconds and launch counts, then (if reset != 0)
+ * clears the record.  Classes: 0 forward logit GEMM (a1+a2), 1 backward
+ * recompute + dlogits GEMM (a5+a6), 2 dW GEMM (a7), 3 dH GEMM (a8), 4 all
+ * other (label scan, gather, merges, loss, scatter). */
+#define CCE_PROF_CLASSES 5
+cce_status cce_profile_enable(cce_handle *h, int32_t on);
+cce_status cce_profile_read(cce_handle *h, double *ms_out, int64_t *launches_out, int32_t reset);
 
 /* Library introspection: number of kernels launched by this handle so far
  * (forward + backward), for the bench's launch count; build string. */

@@ -27,7 +27,12 @@ STATUS = {0: "CCE_OK", 1: "CCE_ERR_INVALID_VALUE", 2: "CCE_ERR_UNSUPPORTED", 3: 
 # every symbol include/cce.h declares
 EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_bytes", "cce_forward", "cce_backward",
            "cce_get_error", "cce_host_staging_bytes", "cce_step_host", "cce_nccl_unique_id", "cce_nccl_comm_init",
-           "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info"]
+           "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info",
+           "cce_profile_enable", "cce_profile_read"]
+PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
+# "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
+# FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
+FLAG_BWD_PER_CHUNK = 2
 
 
 class CCEError(RuntimeError):
@@ -82,6 +87,10 @@ def lib():
         L.cce_status_string.restype = ctypes.c_char_p
         L.cce_kernel_launches.argtypes = [p]
         L.cce_kernel_launches.restype = i64
+        L.cce_profile_enable.argtypes = [p, i32]
+        L.cce_profile_enable.restype = st
+        L.cce_profile_read.argtypes = [p, p, p, i32]
+        L.cce_profile_read.restype = st
         L.cce_build_info.argtypes = []
         L.cce_build_info.restype = ctypes.c_char_p
         _lib = L
@@ -106,7 +115,7 @@ def _stream(stream):
 
 # ----------------------------------------------------------------- C-ABI mirrors
 def cce_create(vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0, rank: int = 0, world: int = 1,
-               nccl_comm=None) -> ctypes.c_void_p:
+               nccl_comm=None, flags: int = 0) -> ctypes.c_void_p:
     cfg = cce_config()
     lib().cce_config_default(ctypes.byref(cfg))
     cfg.ignore_index = ignore_index
@@ -115,6 +124,7 @@ def cce_create(vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0
     cfg.rank = rank
     cfg.world = world
     cfg.nccl_comm = nccl_comm
+    cfg.flags = flags
     h = ctypes.c_void_p()
     _check(lib().cce_create(ctypes.byref(h), ctypes.byref(cfg)), "cce_create")
     return h
@@ -162,6 +172,18 @@ def cce_kernel_launches(h) -> int:
     return int(lib().cce_kernel_launches(h))
 
 
+def cce_profile_enable(h, on: bool = True):
+    _check(lib().cce_profile_enable(h, 1 if on else 0), "cce_profile_enable")
+
+
+def cce_profile_read(h, reset: bool = True):
+    """{class: (ms, launches)} for the kernels recorded since the last reset (synchronises)."""
+    ms = (ctypes.c_double * len(PROF_CLASSES))()
+    n = (ctypes.c_int64 * len(PROF_CLASSES))()
+    _check(lib().cce_profile_read(h, ms, n, 1 if reset else 0), "cce_profile_read")
+    return {c: (ms[i], n[i]) for i, c in enumerate(PROF_CLASSES)}
+
+
 def cce_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().cce_nccl_unique_id(buf), "cce_nccl_unique_id")
@@ -184,8 +206,8 @@ class CCEHandle:
     """A library handle plus a cached device workspace (torch-allocated)."""
 
     def __init__(self, vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0, rank: int = 0,
-                 world: int = 1, nccl_comm=None):
-        self.h = cce_create(vocab_total, ignore_index, vocab_offset, rank, world, nccl_comm)
+                 world: int = 1, nccl_comm=None, flags: int = 0):
+        self.h = cce_create(vocab_total, ignore_index, vocab_offset, rank, world, nccl_comm, flags)
         self.vocab_total = vocab_total
         self.ignore_index = ignore_index
         self._ws = None

@@ -9,9 +9,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/cce.h"
 #include "cce_aux.cuh"
+#include "cce_bwd.cuh"
 #include "cce_gemm.cuh"
 
 using namespace cce;
@@ -32,7 +34,43 @@ struct cce_handle {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   int64_t launches = 0;
-  int* err_host_flag_dev = nullptr;  // points into the saved workspace
+  // profiling (cce_profile_enable): event pairs per launch, tagged with a class
+  bool prof = false;
+  struct Rec { cudaEvent_t a, b; int cls; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t ev() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+};
+
+// Brackets one kernel launch with events when profiling is on.
+struct ProfScope {
+  cce_handle* h;
+  cudaStream_t s;
+  int cls;
+  cudaEvent_t a = nullptr;
+  ProfScope(cce_handle* h_, cudaStream_t s_, int cls_) : h(h_), s(s_), cls(cls_) {
+    if (h->prof) {
+      a = h->ev();
+      cudaEventRecord(a, s);
+    }
+    h->launches++;
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = h->ev();
+      cudaEventRecord(b, s);
+      h->recs.push_back({a, b, cls});
+    }
+  }
 };
 
 // ------------------------------------------------------------------ driver entry points
@@ -114,7 +152,8 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
   int64_t Npad, Tv, C;
-  size_t scal, pos, idx, labels_c, Hc, part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32, total;
+  int64_t n_chunks, sched_ints;
+  size_t scal, pos, idx, labels_c, Hc, part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32, sched, total;
 };
 
 Layout layout(int64_t N, int64_t D, int64_t V_local, int world) {
@@ -143,8 +182,12 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world) {
   L.stats_all = take((size_t)world * L.Npad * 16);
   L.lse_c = take((size_t)L.Npad * 4);
   L.loss_rows = take((size_t)L.Npad * 4);
-  L.gbuf = take((size_t)L.Npad * L.C * 2);
+  L.gbuf = take((size_t)2 * L.Npad * L.C * 2);  // 2-slot ring of N x chunk dlogits (never N x V)
   L.dH32 = take((size_t)L.Npad * D * 4);
+  L.n_chunks = (V_local + L.C - 1) / L.C;
+  // backward work queue: head | g_done[n] | w_done[n] | dh_flag[tiles_d * ceil(Npad/BN)]
+  L.sched_ints = 1 + 2 * L.n_chunks + ((D + BM - 1) / BM) * ((L.Npad + BN - 1) / BN);
+  L.sched = take((size_t)L.sched_ints * 4);
   L.total = o;
   return L;
 }
@@ -173,8 +216,10 @@ cce_status launch_gemm(cce_handle* h, const CUtensorMap& a, const CUtensorMap& b
       return CCE_ERR_CUDA;
     attr_set[MODE] = true;
   }
-  cce_gemm_kernel<MODE><<<h->num_sms, GEMM_THREADS, GEMM_SMEM_BYTES, s>>>(a, b, p);
-  h->launches++;
+  {
+    ProfScope ps(h, s, MODE);
+    cce_gemm_kernel<MODE><<<h->num_sms, GEMM_THREADS, GEMM_SMEM_BYTES, s>>>(a, b, p);
+  }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
 }  // namespace
@@ -236,6 +281,11 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
 
 cce_status cce_destroy(cce_handle* h) {
   if (!h) return CCE_ERR_INVALID_VALUE;
+  for (auto& r : h->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : h->pool) cudaEventDestroy(e);
   delete h;
   return CCE_OK;
 }
@@ -246,6 +296,37 @@ size_t cce_workspace_bytes(const cce_handle* h, int64_t N, int64_t D, int64_t V_
 }
 
 int64_t cce_kernel_launches(const cce_handle* h) { return h ? h->launches : 0; }
+
+cce_status cce_profile_enable(cce_handle* h, int32_t on) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  h->prof = on != 0;
+  return CCE_OK;
+}
+
+cce_status cce_profile_read(cce_handle* h, double* ms_out, int64_t* launches_out, int32_t reset) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  double ms[CCE_PROF_CLASSES] = {0};
+  int64_t cnt[CCE_PROF_CLASSES] = {0};
+  for (auto& r : h->recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return CCE_ERR_CUDA;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return CCE_ERR_CUDA;
+    ms[r.cls] += t;
+    cnt[r.cls] += 1;
+  }
+  for (int i = 0; i < CCE_PROF_CLASSES; ++i) {
+    if (ms_out) ms_out[i] = ms[i];
+    if (launches_out) launches_out[i] = cnt[i];
+  }
+  if (reset) {
+    for (auto& r : h->recs) {
+      h->pool.push_back(r.a);
+      h->pool.push_back(r.b);
+    }
+    h->recs.clear();
+  }
+  return CCE_OK;
+}
 
 cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64_t ldh, const void* W,
                        int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
@@ -267,17 +348,17 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
   int* errp = nvp + 1;
 
   // a0: label scan + compaction
-  // clear n_valid only: the error word is sticky until cce_get_error
-  if (cudaMemsetAsync(nvp, 0, 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+  // clear n_valid and the label-error word (reported for this forward by cce_get_error)
+  if (cudaMemsetAsync(nvp, 0, 8, s) != cudaSuccess) return CCE_ERR_CUDA;
   if (cudaMemsetAsync(at<float>(ws, L.zy_c), 0, (size_t)L.Npad * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
   if (N > 0) {
+    { ProfScope ps(h, s, 4);
     k_label_scan<<<1, 1024, 0, s>>>(labels, (int)N, h->cfg.ignore_index, (long long)h->cfg.vocab_total,
-                                    at<int>(ws, L.pos), at<int>(ws, L.idx), at<int>(ws, L.labels_c), nvp, errp);
-    h->launches++;
+                                    at<int>(ws, L.pos), at<int>(ws, L.idx), at<int>(ws, L.labels_c), nvp, errp); }
+    { ProfScope ps(h, s, 4);
     k_gather_rows<<<grid_for((long long)L.Npad * D / 8, 256, 4 * h->num_sms), 256, 0, s>>>(
         static_cast<const __nv_bfloat16*>(H), ldh, (int)D, (int)L.Npad, at<int>(ws, L.idx), nvp,
-        at<__nv_bfloat16>(ws, L.Hc));
-    h->launches++;
+        at<__nv_bfloat16>(ws, L.Hc)); }
   }
 
   // a1 + a2: tcgen05 logit tiles with the online-softmax epilogue
@@ -305,9 +386,9 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
   float4* stats = at<float4>(ws, L.stats);
   if (N > 0) {
     // an empty shard (V_local == 0) merges zero tiles: (m=-inf, d=0, z_y=0) for every row
-    k_merge_tiles<<<grid_for(L.Npad, 256, 8 * h->num_sms), 256, 0, s>>>(
+    ProfScope ps(h, s, 4);
+    k_merge_tiles<<<(unsigned)((L.Npad + 31) / 32), 1024, 0, s>>>(
         at<float2>(ws, L.part), V_local > 0 ? (int)L.Tv : 0, (int)L.Npad, at<float>(ws, L.zy_c), nvp, stats);
-    h->launches++;
   }
   const float4* stats_all = stats;
   if (h->cfg.world > 1) {
@@ -318,13 +399,15 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
     stats_all = at<float4>(ws, L.stats_all);
   }
   if (N > 0) {
+    ProfScope ps(h, s, 4);
     k_finalize<<<grid_for(N, 256, 8 * h->num_sms), 256, 0, s>>>(stats_all, h->cfg.world, (int)L.Npad,
                                                                 at<int>(ws, L.pos), (int)N, lse, at<float>(ws, L.lse_c),
                                                                 at<float>(ws, L.loss_rows));
-    h->launches++;
   }
-  k_loss<<<1, 1024, 0, s>>>(at<float>(ws, L.loss_rows), nvp, errp, loss, n_valid);
-  h->launches++;
+  {
+    ProfScope ps(h, s, 4);
+    k_loss<<<1, 1024, 0, s>>>(at<float>(ws, L.loss_rows), nvp, errp, loss, n_valid);
+  }
   if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
 
   h->have_fwd = true;
@@ -355,8 +438,8 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     void* Hc = at<void>(ws, L.Hc);
     void* G = at<void>(ws, L.gbuf);
     if (!make_map(&mHcK, Hc, D, L.Npad, D, BM) || !make_map(&mWK, h->W, D, V_local, h->ldw, BN) ||
-        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, L.Npad, L.C, 64) ||
-        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, L.Npad, L.C, BN))
+        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, 2 * L.Npad, L.C, 64) ||
+        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, 2 * L.Npad, L.C, BN))
       return CCE_ERR_CUDA;
     GemmParams p{};
     p.D = (int)D;
@@ -371,17 +454,39 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     p.gbuf = at<__nv_bfloat16>(ws, L.gbuf);
     p.dW = static_cast<__nv_bfloat16*>(dW);
     p.dH32 = dH32;
-    for (int64_t c0 = 0; c0 < V_local; c0 += L.C) {
-      p.c0 = (int)c0;
-      p.width = (int)((V_local - c0) < L.C ? (V_local - c0) : L.C);
-      p.dh_accumulate = c0 > 0 ? 1 : 0;
-      cce_status st;
-      // a5 + a6: recompute the logit tile, G = s (softmax - onehot) in the epilogue -> Gbuf (bf16)
-      if ((st = launch_gemm<MODE_G>(h, mHcK, mWK, p, s)) != CCE_OK) return st;
-      // a7: dW[chunk] = G^T Hc
-      if ((st = launch_gemm<MODE_DW>(h, mHcMN, mGMN, p, s)) != CCE_OK) return st;
-      // a8: dH += G W[chunk]   (fp32, chunk order)
-      if ((st = launch_gemm<MODE_DH>(h, mWMN, mGK, p, s)) != CCE_OK) return st;
+    if (h->cfg.flags & CCE_FLAG_BWD_PER_CHUNK) {
+      // reference schedule: three launches per vocabulary chunk
+      for (int64_t c0 = 0; c0 < V_local; c0 += L.C) {
+        p.c0 = (int)c0;
+        p.width = (int)((V_local - c0) < L.C ? (V_local - c0) : L.C);
+        p.dh_accumulate = c0 > 0 ? 1 : 0;
+        cce_status st;
+        if ((st = launch_gemm<MODE_G>(h, mHcK, mWK, p, s)) != CCE_OK) return st;
+        if ((st = launch_gemm<MODE_DW>(h, mHcMN, mGMN, p, s)) != CCE_OK) return st;
+        if ((st = launch_gemm<MODE_DH>(h, mWMN, mGK, p, s)) != CCE_OK) return st;
+      }
+    } else {
+      // one persistent launch: all chunks' G / DW / DH tiles from a device work queue
+      static bool attr = false;
+      if (!attr) {
+        if (cudaFuncSetAttribute(cce_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
+            cudaSuccess)
+          return CCE_ERR_CUDA;
+        attr = true;
+      }
+      if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+      BwdParams bp;
+      bp.g = p;
+      bp.g.c0 = 0;
+      bp.g.width = 0;
+      bp.g.dh_accumulate = 0;
+      bp.n_chunks = (int)L.n_chunks;
+      bp.sched = at<int>(ws, L.sched);
+      {
+        ProfScope ps(h, s, 1);
+        cce_bwd_kernel<<<h->num_sms, GEMM_THREADS, BWD_SMEM_BYTES, s>>>(mHcK, mWK, mHcMN, mGMN, mWMN, mGK, bp);
+      }
+      if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
     }
   } else if (V_local > 0 && N == 0) {
     // no rows: dW = 0
@@ -396,10 +501,10 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
       if (n.allreduce(dH32, dH32, (size_t)L.Npad * D, kNcclFloat32, kNcclSum, h->cfg.nccl_comm, s) != 0)
         return CCE_ERR_NCCL;
     }
+    ProfScope ps(h, s, 4);
     k_scatter_dH<<<grid_for((long long)N * D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(dH32, at<int>(ws, L.pos), (int)N,
                                                                                      (int)D,
                                                                                      static_cast<__nv_bfloat16*>(dH));
-    h->launches++;
   }
   if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
   return CCE_OK;
@@ -448,8 +553,10 @@ cce_status cce_step_host(cce_handle* h, const void* H_host, int64_t N, int64_t D
   cce_status st = cce_forward(h, N > 0 ? Hd : nullptr, N, D, D, W, V_local, ldw, N > 0 ? yd : nullptr, loss_d, nullptr,
                               nullptr, workspace, workspace_bytes, stream);
   if (st != CCE_OK) return st;
-  k_set_scalar<<<1, 1, 0, s>>>(dloss_d, 1.0f);
-  h->launches++;
+  {
+    ProfScope ps(h, s, 4);
+    k_set_scalar<<<1, 1, 0, s>>>(dloss_d, 1.0f);
+  }
   st = cce_backward(h, dloss_d, dH, dW, stream);
   if (st != CCE_OK) return st;
   if (cudaMemcpyAsync(loss_host, loss_d, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CCE_ERR_CUDA;

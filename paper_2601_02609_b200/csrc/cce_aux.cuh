@@ -88,22 +88,42 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ H, long long ldh
 }
 
 // a4 (local part): merge the per-vocabulary-tile (m, d) partials of each valid
-// row in tile order with the online-softmax merge:
-// m = max_t m_t, d = sum_t d_t exp(m_t - m).  Out: (m, d, z_y) per compact row.
-__global__ void k_merge_tiles(const float2* __restrict__ part, int Tv, int Npad, const float* __restrict__ zy_c,
-                              const int* __restrict__ n_valid, float4* __restrict__ stats) {
+// row with the online-softmax merge:
+// m = max_t m_t, d = sum_t d_t exp(m_t - m).  Block = 32 rows x 32 tile-slices:
+// thread (lane, w) folds tiles t = w, w+32, ... of row i0+lane in a single pass
+// (coalesced: part is [tile][row]), then warp 0 folds the 32 slices in order.
+// Fixed order -> deterministic.  Out: (m, d, z_y) per compact row.
+__global__ void __launch_bounds__(1024) k_merge_tiles(const float2* __restrict__ part, int Tv, int Npad,
+                                                      const float* __restrict__ zy_c, const int* __restrict__ n_valid,
+                                                      float4* __restrict__ stats) {
+  __shared__ float2 red[32][33];
   const int nv = *n_valid;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
-    float m = -INFINITY;
-    for (int t = 0; t < Tv; ++t) m = fmaxf(m, part[(size_t)t * Npad + i].x);
-    float d = 0.f;
-    if (m > -INFINITY) {
-      for (int t = 0; t < Tv; ++t) {
-        const float2 pd = part[(size_t)t * Npad + i];
-        d += pd.y * expf(pd.x - m);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  float m = -INFINITY, d = 0.f;
+  if (i < nv) {
+    for (int t = w; t < Tv; t += 32) {
+      const float2 pd = part[(size_t)t * Npad + i];
+      if (pd.y > 0.f) {
+        const float mn = fmaxf(m, pd.x);
+        d = d * expf(m - mn) + pd.y * expf(pd.x - mn);
+        m = mn;
       }
     }
-    stats[i] = make_float4(m, d, zy_c[i], 0.f);
+  }
+  red[w][lane] = make_float2(m, d);
+  __syncthreads();
+  if (w == 0 && i < nv) {
+    float M = -INFINITY, S = 0.f;
+    for (int k = 0; k < 32; ++k) {
+      const float2 pd = red[k][lane];
+      if (pd.y > 0.f) {
+        const float mn = fmaxf(M, pd.x);
+        S = S * expf(M - mn) + pd.y * expf(pd.x - mn);
+        M = mn;
+      }
+    }
+    stats[i] = make_float4(M, S, zy_c[i], 0.f);
   }
 }
 

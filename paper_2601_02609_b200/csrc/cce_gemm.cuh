@@ -186,6 +186,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
       }
     }
   } else {  // MODE_DH
+    // fp32 accumulation across vocabulary chunks in chunk order: load the 32 old
+    // values first (independent L2 loads, .cg: another SM wrote them), then store.
     const int dcol = mt * BM + row_in_tile;
 #pragma unroll 1
     for (int j = 0; j < BN / 32; ++j) {
@@ -193,14 +195,17 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
       tmem_ld32(taddr + j * 32, v);
       const int t0 = nt * BN + j * 32;
       if (dcol < p.D) {
+        float* base = p.dH32 + (size_t)t0 * p.D + dcol;
+        if (p.dh_accumulate) {
+          float old[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int t = t0 + i;
-          if (t < nv) {
-            float* dst = p.dH32 + (size_t)t * p.D + dcol;
-            *dst = p.dh_accumulate ? (*dst + v[i]) : v[i];
-          }
+          for (int i = 0; i < 32; ++i) old[i] = (t0 + i < nv) ? __ldcg(base + (size_t)i * p.D) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += old[i];
         }
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (t0 + i < nv) __stcg(base + (size_t)i * p.D, v[i]);
       }
     }
   }

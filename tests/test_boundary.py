@@ -1,0 +1,92 @@
+"""The C-ABI boundary on CPU: the library builds, loads and exports every
+symbol include/cce.h declares; host-side validation paths that need no GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2601_02609_b200 as cce
+    return cce.lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "cce.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cce_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_expected_api():
+    syms = declared_symbols()
+    for s in ("cce_forward", "cce_backward", "cce_create", "cce_destroy", "cce_workspace_bytes", "cce_get_error",
+              "cce_step_host"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    import paper_2601_02609_b200 as cce
+    for s in declared_symbols():
+        assert hasattr(lib, s), f"libcce.so does not export {s}"
+    assert sorted(cce.EXPORTS) == declared_symbols()
+
+
+def test_sass_is_tcgen05_and_tma():
+    """The built kernels use tcgen05.mma (UTC*MMA), TMEM loads (LDTM) and TMA
+    (UTMALDG); no legacy HMMA tensor path."""
+    import shutil
+    import subprocess
+    import paper_2601_02609_b200 as cce
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", cce.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+    assert "HMMA." not in sass.replace("UTCHMMA", "")
+
+
+def test_host_validation_without_gpu(lib):
+    import paper_2601_02609_b200 as cce
+    # NULL handle / NULL config
+    assert lib.cce_create(None, None) == 1
+    h = ctypes.c_void_p()
+    cfg = cce.cce_config()
+    lib.cce_config_default(ctypes.byref(cfg))
+    assert cfg.ignore_index == -100 and cfg.world == 1 and cfg.rank == 0
+    assert lib.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 1        # vocab_total unset
+    cfg.vocab_total = 1000
+    cfg.world = 2                                                       # world > 1 without a comm
+    assert lib.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 1
+    assert lib.cce_forward(None, None, 0, 64, 64, None, 0, 64, None, None, None, None, None, 0, None) == 1
+    assert lib.cce_backward(None, None, None, None, None) == 1
+    assert lib.cce_workspace_bytes(None, 10, 64, 10) == 0
+    assert lib.cce_host_staging_bytes(-1, 64) == 0
+    assert lib.cce_status_string(3) == b"CCE_ERR_LABEL_RANGE"
+
+
+def test_create_needs_a_blackwell_device(lib):
+    import torch
+    import paper_2601_02609_b200 as cce
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg = cce.cce_config()
+    lib.cce_config_default(ctypes.byref(cfg))
+    cfg.vocab_total = 1000
+    h = ctypes.c_void_p()
+    assert lib.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 2      # CCE_ERR_UNSUPPORTED: no sm_100 device
+
+
+def test_python_entry_point_refuses_cpu_tensors():
+    import torch
+    import paper_2601_02609_b200 as cce
+    H = torch.zeros(4, 64, dtype=torch.bfloat16)
+    W = torch.zeros(10, 64, dtype=torch.bfloat16)
+    y = torch.zeros(4, dtype=torch.int32)
+    with pytest.raises(ValueError):
+        cce.linear_cross_entropy(H, W, y)

@@ -19,9 +19,9 @@ def dev():
     return torch.device("cuda:0")
 
 
-def _check(p, dev, dloss=1.0):
+def _check(p, dev, dloss=1.0, flags=0):
     H, W, y = to_dev(p, dev)
-    got = run_gpu(H, W, y, dloss=dloss)
+    got = run_gpu(H, W, y, dloss=dloss, flags=flags)
     ref = oracle.cce(p["H"], p["W"], p["labels"], dloss=dloss)
     assert_parity(got, ref, p["labels"])
     return got, ref
@@ -33,15 +33,17 @@ def test_tiny_config(dev, seed):
     _check(workload.make_config("tiny", seed=seed), dev)
 
 
+@pytest.mark.parametrize("flags", [0, 2], ids=["queue", "per_chunk"])
 @pytest.mark.parametrize("N,D,V,ign", [
     (700, 128, 3000, "bern40"),        # ragged rows (5.5 tiles), ragged vocab (11.7 tiles)
     (257, 64, 256, "none"),             # exactly one vocab tile, one ragged row
     (129, 192, 20000, "bern30"),        # 3 backward chunks, ragged last chunk
     (384, 896, 9000, "bern40"),         # Qwen hidden size, 2 chunks
+    (1000, 128, 41000, "bern40"),       # 6 chunks: Gbuf ring slots reused, dH accumulated 6x
 ])
-def test_multi_tile_shapes(dev, N, D, V, ign):
+def test_multi_tile_shapes(dev, N, D, V, ign, flags):
     p = workload.make_problem(N, D, V, seed=N + V, ignore=ign)
-    _check(p, dev)
+    _check(p, dev, flags=flags)
 
 
 @pytest.mark.parametrize("regime", ["peaked", "extreme", "zero"])
@@ -96,13 +98,25 @@ def test_deterministic(dev):
 
 
 def test_shift_invariance_bigshift(dev):
-    """SURVEY pin 9 on the GPU: D = 895 + 1 constant column, c = 80."""
+    """SURVEY pin 9 on the GPU: D = 895 + 1 constant column, c = 80, so every
+    logit is shifted by +80 (exercises the max shift in the online softmax).
+    Loss, LSE and the first 895 columns of dH / all of dW are held to the usual
+    tolerances.  The appended dH column is 80 * sum_v G[n,v], exactly 0 in fp64
+    but bf16-rounded G (the MMA operand) leaves
+    80 x rounding noise there, so it is only bounded, not compared."""
+    from cce_testutil import rel_fro
     p = workload.make_problem(256, 896, 3000, seed=10, ignore="bern40")
     H = p["H"].copy(); W = p["W"].copy()
     H[:, -1] = 0x3F80          # 1.0
     W[:, -1] = 0x42A0          # 80.0
     q = {"H": H, "W": W, "labels": p["labels"]}
-    _check(q, dev)
+    H_, W_, y_ = to_dev(q, dev)
+    got = run_gpu(H_, W_, y_)
+    ref = oracle.cce(q["H"], q["W"], q["labels"])
+    assert_parity(got, ref, q["labels"], check_grads=False)
+    assert rel_fro(got["dH"][:, :-1], ref["dH"][:, :-1]) <= 1e-2
+    assert rel_fro(got["dW"], ref["dW"]) <= 1e-2
+    assert np.abs(got["dH"][:, -1]).max() <= 0.05 * np.abs(ref["dH"]).max()
 
 
 def test_label_out_of_range_reports_error(dev):

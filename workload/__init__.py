@@ -95,13 +95,15 @@ def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
 
 
 def normal_bf16(seed: int, stream: int, rows: int, cols: int, std: float,
-                chunk_elems: int = 1 << 23) -> np.ndarray:
-    """[rows, cols] bf16 bit patterns of std * N(0,1)-ish draws (counter = row*cols+col)."""
+                chunk_elems: int = 1 << 23, row_start: int = 0) -> np.ndarray:
+    """[rows, cols] bf16 bit patterns of std * N(0,1)-ish draws (counter = row*cols+col),
+    for global rows [row_start, row_start+rows) -- a shard is generated directly."""
     total = rows * cols
+    base = row_start * cols
     out = np.empty(total, dtype=np.uint16)
     for s in range(0, total, chunk_elems):
         c = min(chunk_elems, total - s)
-        out[s:s + c] = f32_to_bf16_bits((normal_f64(seed, stream, s, c) * std).astype(np.float32))
+        out[s:s + c] = f32_to_bf16_bits((normal_f64(seed, stream, base + s, c) * std).astype(np.float32))
     return out.reshape(rows, cols)
 
 
@@ -211,8 +213,9 @@ def valid_mask(seed: int, n_rows: int, row_len: int, ignore: str) -> np.ndarray:
 
 def make_problem(N: int, D: int, V: int, seed: int = 42, valid: np.ndarray | None = None,
                  regime: str = "flat", n_rows: int = 1, ignore: str = "none",
-                 label_dist: str = "zipf"):
+                 label_dist: str = "zipf", w_rows: tuple | None = None):
     """Returns dict(H=[N,D] uint16 bf16 bits, W=[V,D] uint16, labels=[N] int32).
+    w_rows=(lo, hi) generates only the vocabulary shard W[lo:hi] (same values).
 
     regimes: flat (default), peaked (planted targets t~U[6,24]), extreme
     (t~U[16,26]), zero (W = 0), smallv (flat with planted t~U[4,20] for V~20k)."""
@@ -220,16 +223,18 @@ def make_problem(N: int, D: int, V: int, seed: int = 42, valid: np.ndarray | Non
         valid = valid_mask(seed, n_rows, N // n_rows, ignore)
     assert valid.shape == (N,)
     H = normal_bf16(seed, S_H, N, D, 1.0)
+    lo, hi = w_rows if w_rows is not None else (0, V)
     if regime == "zero":
-        W = np.zeros((V, D), dtype=np.uint16)
+        W = np.zeros((hi - lo, D), dtype=np.uint16)
     else:
-        W = normal_bf16(seed, S_W, V, D, 1.0 / math.sqrt(D))
+        W = normal_bf16(seed, S_W, hi - lo, D, 1.0 / math.sqrt(D), row_start=lo)
     if label_dist == "zipf":
         lab_all = zipf_labels(seed, N, V)
     else:
         lab_all = randint(seed, S_LABEL, 0, N, 0, V - 1).astype(np.int32)
     labels = np.where(valid, lab_all, IGNORE_INDEX).astype(np.int32)
     if regime in ("peaked", "extreme", "smallv"):
+        assert w_rows is None, "planted regimes need the full W"
         lo, hi = {"peaked": (6.0, 24.0), "extreme": (16.0, 26.0), "smallv": (4.0, 20.0)}[regime]
         t = lo + (hi - lo) * uniform01(seed, S_PLANT, 0, N)
         Hf = bf16_bits_to_f32(H).astype(np.float64)
@@ -241,7 +246,8 @@ def make_problem(N: int, D: int, V: int, seed: int = 42, valid: np.ndarray | Non
     return {"H": H, "W": W, "labels": labels}
 
 
-def make_config(name: str, seed: int = 42, regime: str = "flat", ignore: str | None = None):
+def make_config(name: str, seed: int = 42, regime: str = "flat", ignore: str | None = None,
+                w_rows: tuple | None = None):
     c = CONFIGS[name]
     return make_problem(c.N, c.D, c.V, seed=seed, regime=regime, n_rows=c.n_rows,
-                        ignore=ignore if ignore is not None else c.ignore)
+                        ignore=ignore if ignore is not None else c.ignore, w_rows=w_rows)
