@@ -172,6 +172,12 @@ const char *cce_status_string(cce_status s);
 cce_status cce_profile_enable(cce_handle *h, int32_t on);
 cce_status cce_profile_read(cce_handle *h, double *ms_out, int64_t *launches_out, int32_t reset);
 
+/* Debug: record a per-work-item timeline of the persistent backward kernel into
+ * the device buffer `dev_buf` (64 bytes per queue entry: {queue<<32|type<<16|chunk,
+ * smid, t_dequeue, t_deps_ready, t_epilogue_begin, t_epilogue_end, mt<<32|nt,
+ * num_kblocks}, globaltimer ns).  bytes = 0 disables.  Caller owns the buffer. */
+cce_status cce_debug_trace(cce_handle *h, void *dev_buf, size_t bytes);
+
 /* Library introspection: number of kernels launched by this handle so far
  * (forward + backward), for the bench's launch count; build string. */
 int64_t cce_kernel_launches(const cce_handle *h);

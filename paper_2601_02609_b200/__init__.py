@@ -28,7 +28,7 @@ STATUS = {0: "CCE_OK", 1: "CCE_ERR_INVALID_VALUE", 2: "CCE_ERR_UNSUPPORTED", 3: 
 EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_bytes", "cce_forward", "cce_backward",
            "cce_get_error", "cce_host_staging_bytes", "cce_step_host", "cce_nccl_unique_id", "cce_nccl_comm_init",
            "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info",
-           "cce_profile_enable", "cce_profile_read"]
+           "cce_profile_enable", "cce_profile_read", "cce_debug_trace"]
 PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 # "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
 # FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
@@ -91,6 +91,8 @@ def lib():
         L.cce_profile_enable.restype = st
         L.cce_profile_read.argtypes = [p, p, p, i32]
         L.cce_profile_read.restype = st
+        L.cce_debug_trace.argtypes = [p, p, sz]
+        L.cce_debug_trace.restype = st
         L.cce_build_info.argtypes = []
         L.cce_build_info.restype = ctypes.c_char_p
         _lib = L
@@ -182,6 +184,12 @@ def cce_profile_read(h, reset: bool = True):
     n = (ctypes.c_int64 * len(PROF_CLASSES))()
     _check(lib().cce_profile_read(h, ms, n, 1 if reset else 0), "cce_profile_read")
     return {c: (ms[i], n[i]) for i, c in enumerate(PROF_CLASSES)}
+
+
+def cce_debug_trace(h, buf=None):
+    """Record the next backward's per-item timeline into `buf` (uint8 CUDA tensor) or disable (None)."""
+    _check(lib().cce_debug_trace(h, _ptr(buf), 0 if buf is None else buf.numel() * buf.element_size()),
+           "cce_debug_trace")
 
 
 def cce_nccl_unique_id() -> bytes:

@@ -27,6 +27,7 @@ struct cce_handle {
   cce_config cfg;
   int device = 0;
   int num_sms = 148;
+  int64_t chunk = CCE_CHUNK;  // backward vocabulary chunk (env CCE_CHUNK overrides; multiple of 256)
   // state saved by the forward for the backward (like autograd-saved tensors)
   bool have_fwd = false;
   const void* W = nullptr;
@@ -34,6 +35,8 @@ struct cce_handle {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   int64_t launches = 0;
+  void* trace = nullptr;  // cce_debug_trace: per-item records of the next backward
+  size_t trace_bytes = 0;
   // profiling (cce_profile_enable): event pairs per launch, tagged with a class
   bool prof = false;
   struct Rec { cudaEvent_t a, b; int cls; };
@@ -156,12 +159,12 @@ struct Layout {
   size_t scal, pos, idx, labels_c, Hc, part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32, sched, total;
 };
 
-Layout layout(int64_t N, int64_t D, int64_t V_local, int world) {
+Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk) {
   Layout L;
   L.Npad = align_up((size_t)(N > 0 ? N : 1), 128);
   L.Tv = (V_local + BN - 1) / BN;
   if (L.Tv < 1) L.Tv = 1;
-  int64_t C = CCE_CHUNK;
+  int64_t C = chunk;
   const int64_t vr = (int64_t)align_up((size_t)(V_local > 0 ? V_local : 1), BN);
   if (vr < C) C = vr;
   L.C = C;
@@ -182,11 +185,11 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world) {
   L.stats_all = take((size_t)world * L.Npad * 16);
   L.lse_c = take((size_t)L.Npad * 4);
   L.loss_rows = take((size_t)L.Npad * 4);
-  L.gbuf = take((size_t)2 * L.Npad * L.C * 2);  // 2-slot ring of N x chunk dlogits (never N x V)
+  L.gbuf = take((size_t)GBUF_SLOTS * L.Npad * L.C * 2);  // ring of N x chunk dlogits (never N x V)
   L.dH32 = take((size_t)L.Npad * D * 4);
   L.n_chunks = (V_local + L.C - 1) / L.C;
   // backward work queue: head | g_done[n] | w_done[n] | dh_flag[tiles_d * ceil(Npad/BN)]
-  L.sched_ints = 1 + 2 * L.n_chunks + ((D + BM - 1) / BM) * ((L.Npad + BN - 1) / BN);
+  L.sched_ints = 2 + 2 * L.n_chunks + ((D + BM - 1) / BM) * ((L.Npad + BN - 1) / BN);
   L.sched = take((size_t)L.sched_ints * 4);
   L.total = o;
   return L;
@@ -275,6 +278,10 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
   h->cfg = *cfg;
   h->device = dev;
   h->num_sms = sms > 0 ? sms : 148;
+  if (const char* e = getenv("CCE_CHUNK")) {
+    const long long c = atoll(e);
+    if (c >= 256 && c % 256 == 0) h->chunk = c;
+  }
   *out = h;
   return CCE_OK;
 }
@@ -292,10 +299,17 @@ cce_status cce_destroy(cce_handle* h) {
 
 size_t cce_workspace_bytes(const cce_handle* h, int64_t N, int64_t D, int64_t V_local) {
   if (!h || N < 0 || D <= 0 || V_local < 0) return 0;
-  return layout(N, D, V_local, h->cfg.world).total;
+  return layout(N, D, V_local, h->cfg.world, h->chunk).total;
 }
 
 int64_t cce_kernel_launches(const cce_handle* h) { return h ? h->launches : 0; }
+
+cce_status cce_debug_trace(cce_handle* h, void* dev_buf, size_t bytes) {
+  if (!h || (bytes && !dev_buf)) return CCE_ERR_INVALID_VALUE;
+  h->trace = bytes ? dev_buf : nullptr;
+  h->trace_bytes = bytes;
+  return CCE_OK;
+}
 
 cce_status cce_profile_enable(cce_handle* h, int32_t on) {
   if (!h) return CCE_ERR_INVALID_VALUE;
@@ -339,7 +353,7 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
   if (D % 64 != 0 || N > (1LL << 30) || V_local > (1LL << 30)) return CCE_ERR_UNSUPPORTED;
   if ((N > 0 && !aligned16(H)) || (V_local > 0 && !aligned16(W)) || (ldh * 2) % 16 || (ldw * 2) % 16)
     return CCE_ERR_UNSUPPORTED;
-  const Layout L = layout(N, D, V_local, h->cfg.world);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk);
   if (!workspace || workspace_bytes < L.total || !aligned16(workspace)) return CCE_ERR_WORKSPACE;
   if (!get_encode()) return CCE_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -428,7 +442,7 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
   if ((dH && !aligned16(dH)) || (dW && !aligned16(dW))) return CCE_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t N = h->N, D = h->D, V_local = h->V_local;
-  const Layout L = layout(N, D, V_local, h->cfg.world);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk);
   void* ws = h->ws;
   int* nvp = at<int>(ws, L.scal);
   float* dH32 = at<float>(ws, L.dH32);
@@ -438,8 +452,8 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     void* Hc = at<void>(ws, L.Hc);
     void* G = at<void>(ws, L.gbuf);
     if (!make_map(&mHcK, Hc, D, L.Npad, D, BM) || !make_map(&mWK, h->W, D, V_local, h->ldw, BN) ||
-        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, 2 * L.Npad, L.C, 64) ||
-        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, 2 * L.Npad, L.C, BN))
+        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, GBUF_SLOTS * L.Npad, L.C, 64) ||
+        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, GBUF_SLOTS * L.Npad, L.C, BN))
       return CCE_ERR_CUDA;
     GemmParams p{};
     p.D = (int)D;
@@ -482,6 +496,12 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
       bp.g.dh_accumulate = 0;
       bp.n_chunks = (int)L.n_chunks;
       bp.sched = at<int>(ws, L.sched);
+      bp.trace = static_cast<TraceRec*>(h->trace);
+      bp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
+      bp.slots = GBUF_SLOTS;
+      bp.strict = 0;
+      if (const char* e = getenv("CCE_DEBUG_SLOTS")) bp.slots = atoi(e) >= 2 && atoi(e) <= GBUF_SLOTS ? atoi(e) : GBUF_SLOTS;
+      if (const char* e = getenv("CCE_DEBUG_STRICT")) bp.strict = atoi(e);
       {
         ProfScope ps(h, s, 1);
         cce_bwd_kernel<<<h->num_sms, GEMM_THREADS, BWD_SMEM_BYTES, s>>>(mHcK, mWK, mHcMN, mGMN, mWMN, mGK, bp);
@@ -514,7 +534,7 @@ cce_status cce_get_error(cce_handle* h, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!h->ws) return CCE_OK;
-  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk);
   int* errp = at<int>(h->ws, L.scal) + 1;
   int err = 0;
   if (cudaMemcpyAsync(&err, errp, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CCE_ERR_CUDA;

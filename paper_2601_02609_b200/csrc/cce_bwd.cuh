@@ -6,7 +6,7 @@
 // then grad_h += probs @ W[chunk] and grad_W[chunk] += probs^T @ h.  Here each
 // chunk c (CCE_CHUNK vocabulary rows) becomes three families of 128 x 256 tiles:
 //   G(c)   recompute S = Hc W_c^T, epilogue G = s (exp(S - lse) - onehot) -> bf16
-//          into the chunk's slot of a 2-slot ring buffer Gbuf (N x chunk, never N x V)
+//          into the chunk's slot of a 3-slot ring buffer Gbuf (N x chunk, never N x V)
 //   DW(c)  dW_c^T = Hc^T G_c      (tile: 128 hidden x 256 vocab, K = valid rows)
 //   DH(c)  dH^T  += W_c^T G_c^T   (tile: 128 hidden x 256 rows, K = chunk), fp32
 //          read-modify-write in chunk order (deterministic)
@@ -14,7 +14,8 @@
 //   G0, G1, W0, G2, W1, ..., G_{n-1}, W_{n-2}, W_{n-1}      (W_c = DH(c) then DW(c))
 // and each item's producer warp waits (acquire loads on global counters) only on
 // items that precede it in the queue, so the schedule cannot deadlock:
-//   G(c)        needs W(c-2) finished        (its Gbuf slot is free again)
+//   G(c)        needs W(c-3) finished        (its Gbuf slot is free again; W(c-3) was
+//               queued a whole phase before, so this wait is normally already satisfied)
 //   DW(c),DH(c) need every G(c) tile finished (G_c complete in Gbuf)
 //   DH(c,tile)  needs DH(c-1,tile) finished   (ordered fp32 accumulation)
 // One launch replaces 3 x n_chunks launches: no wave-quantisation tail per chunk,
@@ -28,16 +29,37 @@ namespace cce {
 enum ItemType : int { IT_G = 0, IT_DW = 1, IT_DH = 2, IT_END = 3 };
 
 struct Item {
-  int type, c, mt, nt, width, num_kb, tile_id;
+  int type, c, mt, nt, width, num_kb, tile_id, q;
+  unsigned long long t_deq, t_ready;  // globaltimer stamps (trace only)
 };
+
+// Optional per-item trace record (cce_debug_trace): 8 x u64 per queue position.
+struct TraceRec {
+  unsigned long long q_type_c, smid, t_deq, t_ready, t_epi0, t_epi1, tile, pad;
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
 
 struct BwdParams {
   GemmParams g;      // shared sizes/pointers (gbuf = slot 0 base)
   int n_chunks;
-  int* sched;        // zeroed before launch: [0] queue head | g_done[n] | w_done[n] | dh_flag[tiles]
+  int* sched;        // zeroed before launch: [0] queue head | [1] items done | g_done[n] | w_done[n] | dh_flag[tiles]
+  TraceRec* trace;   // optional (nullptr): one record per queue position
+  int trace_cap;
+  int slots;         // Gbuf ring slots (>= 2)
+  int strict;        // debug: every item waits for all earlier items to finish
 };
 
 constexpr int RING = 4;
+constexpr int GBUF_SLOTS = 3;  // ring of chunk dlogits buffers: G(c) reuses the slot of chunk c-3
 
 struct BwdCounts {
   int nv, tiles_tok, tiles_d, tiles_tok256, n_dh;
@@ -92,6 +114,7 @@ __device__ Item decode_item(const BwdParams& P, const BwdCounts& k, int q) {
   }
   Item e;
   e.type = IT_END; e.c = 0; e.mt = 0; e.nt = 0; e.width = 0; e.num_kb = 0; e.tile_id = 0;
+  e.q = 0; e.t_deq = 0; e.t_ready = 0;
   return e;
 }
 
@@ -105,9 +128,6 @@ __device__ __forceinline__ void wait_ge(const int* p, int target) {
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -128,20 +148,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* rempty_bar = rfull_bar + RING;
   Item* ring = reinterpret_cast<Item*>(rempty_bar + RING);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + RING);
+  float* xchg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 512);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   int* queue_head = P.sched;
-  int* g_done = P.sched + 1;
-  int* w_done = P.sched + 1 + P.n_chunks;
-  int* dh_flag = P.sched + 1 + 2 * P.n_chunks;
+  int* done_total = P.sched + 1;
+  int* g_done = P.sched + 2;
+  int* w_done = P.sched + 2 + P.n_chunks;
+  int* dh_flag = P.sched + 2 + 2 * P.n_chunks;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmHcK); tma_prefetch_desc(&tmWK); tma_prefetch_desc(&tmHcMN);
     tma_prefetch_desc(&tmGMN); tma_prefetch_desc(&tmWMN); tma_prefetch_desc(&tmGK);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 128); }
-    for (int r = 0; r < RING; ++r) { mbar_init(&rfull_bar[r], 1); mbar_init(&rempty_bar[r], 1 + 128); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], EPI_THREADS); }
+    for (int r = 0; r < RING; ++r) { mbar_init(&rfull_bar[r], 1); mbar_init(&rempty_bar[r], 1 + EPI_THREADS); }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -165,24 +187,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t rslot = 0, rphase = 0;
       while (true) {
         const int q = atomicAdd(queue_head, 1);
+        const unsigned long long t_deq = P.trace ? gtimer() : 0ull;
         Item it = decode_item(P, k, q);
+        it.q = q;
+        it.t_deq = t_deq;
         // dependencies (only on earlier queue entries)
         if (it.type == IT_G) {
-          if (it.c >= 2) {
-            const int wc = it.c - 2;
+          if (it.c >= P.slots) {
+            const int wc = it.c - P.slots;
             wait_ge(&w_done[wc], k.n_dh + n_dw_items(k, chunk_width(g, wc)));
           }
         } else if (it.type == IT_DW || it.type == IT_DH) {
           wait_ge(&g_done[it.c], n_g_items(k, it.width));
           if (it.type == IT_DH) wait_ge(&dh_flag[it.tile_id], it.c);
         }
+        if (P.strict && it.type != IT_END) wait_ge(done_total, q);  // debug: fully serialised dependencies
         fence_proxy_async_global();
+        if (P.trace) it.t_ready = gtimer();
         mbar_wait(&rempty_bar[rslot], rphase ^ 1);
         ring[rslot] = it;
         mbar_arrive(&rfull_bar[rslot]);
         if (++rslot == RING) { rslot = 0; rphase ^= 1; }
         if (it.type == IT_END) break;
-        const int slot_row0 = (it.c & 1) * slot_rows;
+        const int slot_row0 = (it.c % P.slots) * slot_rows;
         const int c0 = it.c * g.C;
         for (int kb = 0; kb < it.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -248,8 +275,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ===== epilogue (128 threads) =====
-    const int q = warp & 3;
-    const int row_in_tile = q * 32 + lane;
+    EpiCtx e;
+    e.q = warp & 3;
+    e.half = (warp - 4) >> 2;
+    e.row_in_tile = e.q * 32 + lane;
+    e.xchg = xchg;
+    const bool leader = (threadIdx.x == 128);  // exactly one epilogue thread publishes
     const float scale = k.nv > 0 ? (*g.dloss) / (float)k.nv : 0.f;
     uint32_t rslot = 0, rphase = 0;
     int acc_it = 0;
@@ -268,22 +299,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
       }
-      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(e.q * 32) << 16);
+      const unsigned long long t_epi0 = P.trace ? gtimer() : 0ull;
       GemmParams gp = g;
       gp.c0 = it.c * g.C;
       gp.width = it.width;
       if (it.type == IT_G) {
-        gp.gbuf = g.gbuf + (size_t)(it.c & 1) * slot_rows * g.C;
-        epilogue_tile<MODE_G>(gp, taddr, row_in_tile, it.mt, it.nt, k.nv, scale, true);
+        gp.gbuf = g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C;
+        epilogue_tile<MODE_G>(gp, taddr, e, it.mt, it.nt, k.nv, scale, true);
       } else if (it.type == IT_DW) {
-        epilogue_tile<MODE_DW>(gp, taddr, row_in_tile, it.mt, it.nt, k.nv, scale, have_acc);
+        epilogue_tile<MODE_DW>(gp, taddr, e, it.mt, it.nt, k.nv, scale, have_acc);
       } else {
         gp.dh_accumulate = it.c > 0 ? 1 : 0;
         // DH(c-1, tile) has published (the producer already waited on it; re-acquire
         // here so these threads' .cg loads are ordered after that release)
-        if (row_in_tile == 0) wait_ge(&dh_flag[it.tile_id], it.c);
-        named_bar(2, 128);
-        epilogue_tile<MODE_DH>(gp, taddr, row_in_tile, it.mt, it.nt, k.nv, scale, true);
+        if (leader) wait_ge(&dh_flag[it.tile_id], it.c);
+        named_bar_sync(2, EPI_THREADS);
+        epilogue_tile<MODE_DH>(gp, taddr, e, it.mt, it.nt, k.nv, scale, true);
       }
       if (have_acc) {
         tc_fence_before();
@@ -292,14 +324,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // publish completion: all 128 threads' global stores, then one release
       fence_proxy_async_global();
       __threadfence();
-      named_bar(1, 128);
-      if (row_in_tile == 0) {
+      named_bar_sync(1, EPI_THREADS);
+      if (leader && P.trace && it.q < P.trace_cap) {
+        TraceRec r;
+        r.q_type_c = ((unsigned long long)it.q << 32) | ((unsigned long long)it.type << 16) | (unsigned)it.c;
+        r.smid = smid();
+        r.t_deq = it.t_deq;
+        r.t_ready = it.t_ready;
+        r.t_epi0 = t_epi0;
+        r.t_epi1 = gtimer();
+        r.tile = ((unsigned long long)it.mt << 32) | (unsigned)it.nt;
+        r.pad = it.num_kb;
+        P.trace[it.q] = r;
+      }
+      if (leader) {
         if (it.type == IT_G) {
           atomicAdd(&g_done[it.c], 1);
         } else {
           if (it.type == IT_DH) atomicExch(&dh_flag[it.tile_id], it.c + 1);
           atomicAdd(&w_done[it.c], 1);
         }
+        atomicAdd(done_total, 1);
       }
     }
   }
@@ -310,6 +355,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem_base, TMEM_COLS);
 }
 
-constexpr int BWD_SMEM_BYTES = GEMM_SMEM_BYTES + 2 * RING * 8 + RING * (int)sizeof(Item) + 64;
+constexpr int BWD_SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers, ring*/ + 1024 /*xchg*/;
+static_assert(12 * 8 + 2 * RING * 8 + RING * sizeof(Item) + 4 <= 512, "bwd barrier area");
 
 }  // namespace cce

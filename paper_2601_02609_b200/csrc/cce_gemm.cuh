@@ -41,9 +41,9 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 128 + 8 * 32;  // 4 control warps + 8 epilogue warps
 constexpr int TMEM_COLS = 512;
-constexpr int GEMM_SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+constexpr int GEMM_SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/ + 1024 /*xchg*/;
 constexpr float LOG2E = 1.4426950408889634f;
 
 struct GemmParams {
@@ -90,24 +90,37 @@ __device__ __forceinline__ TileGeom tile_geom(const GemmParams& p, int nv) {
 }
 
 // ------------------------------------------------------------------ epilogues
-// Each epilogue thread owns TMEM lane `row_in_tile` of the 128 x 256 accumulator
-// at column base `tcol` (lane field already folded into taddr).
+// 8 epilogue warps: warp w (4..11) reads TMEM lane quarter q = w % 4 (rows
+// 32q..32q+31 of the tile) and column half h = (w - 4) / 4 (columns 128h..128h+127).
+// Each thread owns one accumulator row of its half.
+constexpr int EPI_WARPS = 8;
+constexpr int EPI_THREADS = EPI_WARPS * 32;
+constexpr int HALF = BN / 2;          // columns per epilogue warp
+constexpr int JCH = HALF / 32;        // 32-column chunks per warp
+
+struct EpiCtx {
+  int row_in_tile;  // TMEM lane == tile row
+  int q, half;
+  float* xchg;      // smem scratch [2][128] float2 for the FWD half merge
+};
 
 template <int MODE>
-__device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t taddr, int row_in_tile, int mt,
-                                              int nt, int nv, float scale, bool have_acc) {
+__device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t taddr, const EpiCtx& e, int mt, int nt,
+                                              int nv, float scale, bool have_acc) {
+  const int cbase = e.half * HALF;  // first column of this warp's half
   if (MODE == MODE_FWD) {
-    const int row = mt * BM + row_in_tile;
+    // Per-row online softmax over this half's 128 logits: running max m and sum-exp d
+    // (Def. "Online Softmax"), target logit captured when y falls here.
+    const int row = mt * BM + e.row_in_tile;
     const bool rv = row < nv;
     const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
-    float m = -INFINITY, d = 0.f, zy = 0.f;
-    bool own = false;
+    float m = -INFINITY, d = 0.f;
 #pragma unroll 1
-    for (int j = 0; j < BN / 32; ++j) {
+    for (int j = 0; j < JCH; ++j) {
       float v[32];
-      tmem_ld32(taddr + j * 32, v);
-      const int col0 = nt * BN + j * 32;
-      if (col0 >= p.V_local) break;  // whole remaining tile is past the vocabulary
+      tmem_ld32(taddr + cbase + j * 32, v);
+      const int col0 = nt * BN + cbase + j * 32;
+      if (col0 >= p.V_local) break;  // warp-uniform: rest of the half is past the vocabulary
       if (col0 + 32 > p.V_local) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -118,66 +131,85 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
       for (int i = 1; i < 32; ++i) cmax = fmaxf(cmax, v[i]);
       const float mn = fmaxf(m, cmax);
       const float ms = mn * LOG2E;
-      float s = 0.f;
+      float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) s += ex2(fmaf(v[i], LOG2E, -ms));
-      d = d * ex2((m - mn) * LOG2E) + s;  // m = -inf on the first chunk: ex2(-inf) = 0
+      for (int i = 0; i < 32; i += 2) {
+        s0 += ex2(fmaf(v[i], LOG2E, -ms));
+        s1 += ex2(fmaf(v[i + 1], LOG2E, -ms));
+      }
+      d = d * ex2((m - mn) * LOG2E) + (s0 + s1);  // first chunk: m = -inf -> ex2(-inf) = 0
       m = mn;
       const unsigned off = (unsigned)(y - col0);
       if (off < 32u) {
+        float zy = 0.f;
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           if (off == (unsigned)i) zy = v[i];
-        own = true;
+        p.zy_c[row] = zy;  // exactly one (tile, half, chunk) owns y
       }
     }
-    if (rv) {
-      p.part[(size_t)nt * p.Npad + row] = make_float2(m, d);
-      if (own) p.zy_c[row] = zy;
+    // merge the two halves of the row: half 1 hands (m, d) to half 0 through smem
+    float2* x = reinterpret_cast<float2*>(e.xchg);
+    if (e.half == 1) x[e.row_in_tile] = make_float2(m, d);
+    named_bar_sync(3 + e.q, 64);
+    if (e.half == 0) {
+      const float2 o = x[e.row_in_tile];
+      const float mn = fmaxf(m, o.x);
+      const float dd = (d > 0.f ? d * ex2((m - mn) * LOG2E) : 0.f) + (o.y > 0.f ? o.y * ex2((o.x - mn) * LOG2E) : 0.f);
+      if (rv) p.part[(size_t)nt * p.Npad + row] = make_float2(mn, dd);
     }
+    named_bar_sync(3 + e.q, 64);  // xchg reusable for the next tile
   } else if (MODE == MODE_G) {
-    const int row = mt * BM + row_in_tile;
+    // G = s (exp(S - lse) - 1[v = y]) with s = dloss / n_valid folded into
+    // the exponent: s exp(S - lse) = 2^(S log2e - lse log2e + log2 s).  Rows past
+    // n_valid use an exponent offset of +inf (-> 0); the vocab tail is masked per chunk.
+    const int row = mt * BM + e.row_in_tile;
     const bool rv = row < nv;
     const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
-    const float l2 = rv ? p.lse_c[row] * LOG2E : 0.f;
-    __nv_bfloat16* out = p.gbuf + (size_t)row * p.C + nt * BN;
+    const float off2 = rv ? (p.lse_c[row] * LOG2E - __log2f(fabsf(scale))) : INFINITY;
+    __nv_bfloat16* out = p.gbuf + (size_t)row * p.C + nt * BN + cbase;
 #pragma unroll 1
-    for (int j = 0; j < BN / 32; ++j) {
+    for (int j = 0; j < JCH; ++j) {
       float v[32];
-      tmem_ld32(taddr + j * 32, v);
-      const int lcol0 = nt * BN + j * 32;   // column within the chunk
-      const int col0 = p.c0 + lcol0;        // local vocabulary row
-      uint32_t pk[16];
+      tmem_ld32(taddr + cbase + j * 32, v);
+      const int lcol0 = nt * BN + cbase + j * 32;  // column within the chunk
+      const int col0 = p.c0 + lcol0;               // local vocabulary row
+      float g[32];
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        float g0 = ex2(fmaf(v[i], LOG2E, -l2));
-        float g1 = ex2(fmaf(v[i + 1], LOG2E, -l2));
-        if (col0 + i == y) g0 -= 1.f;
-        if (col0 + i + 1 == y) g1 -= 1.f;
-        g0 *= scale;
-        g1 *= scale;
-        if (!rv || lcol0 + i >= p.width) g0 = 0.f;
-        if (!rv || lcol0 + i + 1 >= p.width) g1 = 0.f;
-        pk[i / 2] = pack_bf16(g0, g1);
-      }
-      if (row < p.Npad && lcol0 < p.C) {
-        uint4* dst = reinterpret_cast<uint4*>(out + j * 32);
+      for (int i = 0; i < 32; ++i) g[i] = ex2(fmaf(v[i], LOG2E, -off2));
+      const unsigned toff = (unsigned)(y - col0);
+      if (scale < 0.f) {  // warp-uniform: negative upstream gradient
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        for (int i = 0; i < 32; ++i) g[i] = -g[i];
       }
+      if (toff < 32u) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (toff == (unsigned)i) g[i] -= scale;
+      }
+      if (lcol0 + 32 > p.width) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (lcol0 + i >= p.width) g[i] = 0.f;
+      }
+      uint4* dst = reinterpret_cast<uint4*>(out + j * 32);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        dst[q4] = make_uint4(pack_bf16(g[8 * q4], g[8 * q4 + 1]), pack_bf16(g[8 * q4 + 2], g[8 * q4 + 3]),
+                             pack_bf16(g[8 * q4 + 4], g[8 * q4 + 5]), pack_bf16(g[8 * q4 + 6], g[8 * q4 + 7]));
     }
   } else if (MODE == MODE_DW) {
-    const int dcol = mt * BM + row_in_tile;  // hidden index
+    const int dcol = mt * BM + e.row_in_tile;  // hidden index
 #pragma unroll 1
-    for (int j = 0; j < BN / 32; ++j) {
+    for (int j = 0; j < JCH; ++j) {
       float v[32];
       if (have_acc) {
-        tmem_ld32(taddr + j * 32, v);
+        tmem_ld32(taddr + cbase + j * 32, v);
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.f;
       }
-      const int lcol0 = nt * BN + j * 32;
+      const int lcol0 = nt * BN + cbase + j * 32;
       if (dcol < p.D) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -188,12 +220,12 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
   } else {  // MODE_DH
     // fp32 accumulation across vocabulary chunks in chunk order: load the 32 old
     // values first (independent L2 loads, .cg: another SM wrote them), then store.
-    const int dcol = mt * BM + row_in_tile;
+    const int dcol = mt * BM + e.row_in_tile;
 #pragma unroll 1
-    for (int j = 0; j < BN / 32; ++j) {
+    for (int j = 0; j < JCH; ++j) {
       float v[32];
-      tmem_ld32(taddr + j * 32, v);
-      const int t0 = nt * BN + j * 32;
+      tmem_ld32(taddr + cbase + j * 32, v);
+      const int t0 = nt * BN + cbase + j * 32;
       if (dcol < p.D) {
         float* base = p.dH32 + (size_t)t0 * p.D + dcol;
         if (p.dh_accumulate) {
@@ -229,6 +261,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  float* xchg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -242,7 +275,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 128);
+      mbar_init(&tempty_bar[b], EPI_THREADS);
     }
     fence_barrier_init();
   }
@@ -314,8 +347,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ===== epilogue =====
-    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-    const int row_in_tile = q * 32 + lane;
+    EpiCtx e;
+    e.q = warp & 3;  // TMEM lane quarter accessible to this warp
+    e.half = (warp - 4) >> 2;
+    e.row_in_tile = e.q * 32 + lane;
+    e.xchg = xchg;
     float scale = 0.f;
     if (MODE == MODE_G) scale = nv > 0 ? (*p.dloss) / (float)nv : 0.f;
     int it = 0;
@@ -327,8 +363,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
       }
-      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
-      epilogue_tile<MODE>(p, taddr, row_in_tile, mt, nt, nv, scale, have_acc);
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(e.q * 32) << 16);
+      epilogue_tile<MODE>(p, taddr, e, mt, nt, nv, scale, have_acc);
       if (have_acc) {
         tc_fence_before();
         mbar_arrive(&tempty_bar[acc]);
