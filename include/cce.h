@@ -75,6 +75,9 @@ typedef enum {
  * chunks; CCE_FLAG_BWD_PER_CHUNK = three launches per vocabulary chunk (the
  * straightforward schedule, kept for A/B measurements and tests). */
 #define CCE_FLAG_BWD_PER_CHUNK 2u
+/* Kernels: 0 (default) = CTA-pair kernels (tcgen05.mma.cta_group::2, 256-row
+ * tiles); CCE_FLAG_ONE_CTA = single-CTA 128x256-tile kernels (kept for A/B). */
+#define CCE_FLAG_ONE_CTA 4u
 
 typedef struct {
   int32_t ignore_index;   /* label value that marks a skipped row; -100 in the paper */
@@ -172,10 +175,13 @@ const char *cce_status_string(cce_status s);
 cce_status cce_profile_enable(cce_handle *h, int32_t on);
 cce_status cce_profile_read(cce_handle *h, double *ms_out, int64_t *launches_out, int32_t reset);
 
-/* Debug: record a per-work-item timeline of the persistent backward kernel into
- * the device buffer `dev_buf` (64 bytes per queue entry: {queue<<32|type<<16|chunk,
- * smid, t_dequeue, t_deps_ready, t_epilogue_begin, t_epilogue_end, mt<<32|nt,
- * num_kblocks}, globaltimer ns).  bytes = 0 disables.  Caller owns the buffer. */
+/* Debug: record a per-work-item timeline of the persistent kernels into the
+ * device buffer `dev_buf`: the first half holds backward items, the second half
+ * forward items, 128 bytes per queue entry: {queue<<32|type<<16|chunk, smid,
+ * t_dequeue, t_deps_ready, t_epilogue_begin, t_epilogue_end, m0<<32|n0,
+ * num_kblocks, t_first_tma, t_last_tma, t_first_mma, t_last_mma,
+ * ns_waiting_on_full_barriers, 0, 0, 0} (globaltimer ns; pair kernels fill all
+ * fields).  bytes = 0 disables.  Caller owns the buffer. */
 cce_status cce_debug_trace(cce_handle *h, void *dev_buf, size_t bytes);
 
 /* Library introspection: number of kernels launched by this handle so far

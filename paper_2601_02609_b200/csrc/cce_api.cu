@@ -15,6 +15,7 @@
 #include "cce_aux.cuh"
 #include "cce_bwd.cuh"
 #include "cce_gemm.cuh"
+#include "cce_pair.cuh"
 
 using namespace cce;
 
@@ -35,8 +36,10 @@ struct cce_handle {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   int64_t launches = 0;
-  void* trace = nullptr;  // cce_debug_trace: per-item records of the next backward
+  void* trace = nullptr;  // cce_debug_trace: per-item records of the backward
   size_t trace_bytes = 0;
+  void* fwd_trace = nullptr;  // ... and of the forward (second half of the buffer)
+  size_t fwd_trace_bytes = 0;
   // profiling (cce_profile_enable): event pairs per launch, tagged with a class
   bool prof = false;
   struct Rec { cudaEvent_t a, b; int cls; };
@@ -161,7 +164,7 @@ struct Layout {
 
 Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk) {
   Layout L;
-  L.Npad = align_up((size_t)(N > 0 ? N : 1), 128);
+  L.Npad = align_up((size_t)(N > 0 ? N : 1), 256);  // pair tiles are 256 rows
   L.Tv = (V_local + BN - 1) / BN;
   if (L.Tv < 1) L.Tv = 1;
   int64_t C = chunk;
@@ -222,6 +225,23 @@ cce_status launch_gemm(cce_handle* h, const CUtensorMap& a, const CUtensorMap& b
   {
     ProfScope ps(h, s, MODE);
     cce_gemm_kernel<MODE><<<h->num_sms, GEMM_THREADS, GEMM_SMEM_BYTES, s>>>(a, b, p);
+  }
+  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+}
+cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
+                       const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5,
+                       const pairk::PairParams& pp, cudaStream_t s, int prof_class) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(pairk::cce_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pairk::PSMEM) !=
+        cudaSuccess)
+      return CCE_ERR_CUDA;
+    attr = true;
+  }
+  const int grid = (h->num_sms / 2) * 2;  // whole CTA pairs
+  {
+    ProfScope ps(h, s, prof_class);
+    pairk::cce_pair_kernel<<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, pp);
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
@@ -306,8 +326,12 @@ int64_t cce_kernel_launches(const cce_handle* h) { return h ? h->launches : 0; }
 
 cce_status cce_debug_trace(cce_handle* h, void* dev_buf, size_t bytes) {
   if (!h || (bytes && !dev_buf)) return CCE_ERR_INVALID_VALUE;
+  // first half: backward items, second half: forward items
+  const size_t half = (bytes / 2) / sizeof(TraceRec) * sizeof(TraceRec);
   h->trace = bytes ? dev_buf : nullptr;
-  h->trace_bytes = bytes;
+  h->trace_bytes = half;
+  h->fwd_trace = bytes ? static_cast<char*>(dev_buf) + half : nullptr;
+  h->fwd_trace_bytes = half;
   return CCE_OK;
 }
 
@@ -377,9 +401,6 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
 
   // a1 + a2: tcgen05 logit tiles with the online-softmax epilogue
   if (N > 0 && V_local > 0) {
-    CUtensorMap tA, tB;
-    if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, BM)) return CCE_ERR_CUDA;
-    if (!make_map(&tB, W, D, V_local, ldw, BN)) return CCE_ERR_CUDA;
     GemmParams p{};
     p.D = (int)D;
     p.V_local = (int)V_local;
@@ -392,8 +413,29 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
     p.labels_c = at<int>(ws, L.labels_c);
     p.part = at<float2>(ws, L.part);
     p.zy_c = at<float>(ws, L.zy_c);
-    cce_status st = launch_gemm<MODE_FWD>(h, tA, tB, p, s);
-    if (st != CCE_OK) return st;
+    if (h->cfg.flags & CCE_FLAG_ONE_CTA) {
+      CUtensorMap tA, tB;
+      if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, BM)) return CCE_ERR_CUDA;
+      if (!make_map(&tB, W, D, V_local, ldw, BN)) return CCE_ERR_CUDA;
+      cce_status st = launch_gemm<MODE_FWD>(h, tA, tB, p, s);
+      if (st != CCE_OK) return st;
+    } else {
+      CUtensorMap tA, tB;
+      if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM)) return CCE_ERR_CUDA;
+      if (!make_map(&tB, W, D, V_local, ldw, pairk::PN / 2)) return CCE_ERR_CUDA;
+      if (cudaMemsetAsync(at<int>(ws, L.sched), 0, 8, s) != cudaSuccess) return CCE_ERR_CUDA;
+      pairk::PairParams pp{};
+      pp.g = p;
+      pp.mode = 0;
+      pp.n_chunks = 0;
+      pp.slots = GBUF_SLOTS;
+      if (const char* e = getenv("CCE_DEBUG_STRICT")) pp.strict = atoi(e);
+      pp.sched = at<int>(ws, L.sched);
+      pp.trace = static_cast<TraceRec*>(h->fwd_trace);
+      pp.trace_cap = (int)(h->fwd_trace_bytes / sizeof(TraceRec));
+      cce_status st = launch_pair(h, tA, tB, tA, tA, tA, tA, pp, s, 0);
+      if (st != CCE_OK) return st;
+    }
   }
 
   // a4: merge tiles -> per-rank stats; a9: allgather across vocabulary shards
@@ -448,13 +490,8 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
   float* dH32 = at<float>(ws, L.dH32);
 
   if (V_local > 0 && N > 0) {
-    CUtensorMap mHcK, mWK, mHcMN, mGMN, mWMN, mGK;
     void* Hc = at<void>(ws, L.Hc);
     void* G = at<void>(ws, L.gbuf);
-    if (!make_map(&mHcK, Hc, D, L.Npad, D, BM) || !make_map(&mWK, h->W, D, V_local, h->ldw, BN) ||
-        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, GBUF_SLOTS * L.Npad, L.C, 64) ||
-        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, GBUF_SLOTS * L.Npad, L.C, BN))
-      return CCE_ERR_CUDA;
     GemmParams p{};
     p.D = (int)D;
     p.V_local = (int)V_local;
@@ -468,6 +505,35 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     p.gbuf = at<__nv_bfloat16>(ws, L.gbuf);
     p.dW = static_cast<__nv_bfloat16*>(dW);
     p.dH32 = dH32;
+    int slots = GBUF_SLOTS, strict = 0;
+    if (const char* e = getenv("CCE_DEBUG_SLOTS")) slots = atoi(e) >= 2 && atoi(e) <= GBUF_SLOTS ? atoi(e) : GBUF_SLOTS;
+    if (const char* e = getenv("CCE_DEBUG_STRICT")) strict = atoi(e);
+    if (!(h->cfg.flags & CCE_FLAG_ONE_CTA)) {
+      // CTA-pair persistent backward: G / DW / DH tiles of every chunk from one work queue
+      CUtensorMap mHcK, mWK, mGMN, mHcMN, mGK, mWMN;
+      if (!make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM) || !make_map(&mWK, h->W, D, V_local, h->ldw, pairk::PN / 2) ||
+          !make_map(&mGMN, G, L.C, GBUF_SLOTS * L.Npad, L.C, 64) || !make_map(&mHcMN, Hc, D, L.Npad, D, 64) ||
+          !make_map(&mGK, G, L.C, GBUF_SLOTS * L.Npad, L.C, pairk::HM) ||
+          !make_map(&mWMN, h->W, D, V_local, h->ldw, 64))
+        return CCE_ERR_CUDA;
+      if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+      pairk::PairParams pp{};
+      pp.g = p;
+      pp.mode = 1;
+      pp.n_chunks = (int)L.n_chunks;
+      pp.slots = slots;
+      pp.strict = strict;
+      pp.sched = at<int>(ws, L.sched);
+      pp.trace = static_cast<TraceRec*>(h->trace);
+      pp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
+      cce_status st = launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, pp, s, 1);
+      if (st != CCE_OK) return st;
+    } else {
+    CUtensorMap mHcK, mWK, mHcMN, mGMN, mWMN, mGK;
+    if (!make_map(&mHcK, Hc, D, L.Npad, D, BM) || !make_map(&mWK, h->W, D, V_local, h->ldw, BN) ||
+        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, GBUF_SLOTS * L.Npad, L.C, 64) ||
+        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, GBUF_SLOTS * L.Npad, L.C, BN))
+      return CCE_ERR_CUDA;
     if (h->cfg.flags & CCE_FLAG_BWD_PER_CHUNK) {
       // reference schedule: three launches per vocabulary chunk
       for (int64_t c0 = 0; c0 < V_local; c0 += L.C) {
@@ -498,15 +564,14 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
       bp.sched = at<int>(ws, L.sched);
       bp.trace = static_cast<TraceRec*>(h->trace);
       bp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
-      bp.slots = GBUF_SLOTS;
-      bp.strict = 0;
-      if (const char* e = getenv("CCE_DEBUG_SLOTS")) bp.slots = atoi(e) >= 2 && atoi(e) <= GBUF_SLOTS ? atoi(e) : GBUF_SLOTS;
-      if (const char* e = getenv("CCE_DEBUG_STRICT")) bp.strict = atoi(e);
+      bp.slots = slots;
+      bp.strict = strict;
       {
         ProfScope ps(h, s, 1);
         cce_bwd_kernel<<<h->num_sms, GEMM_THREADS, BWD_SMEM_BYTES, s>>>(mHcK, mWK, mHcMN, mGMN, mWMN, mGK, bp);
       }
       if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
+    }
     }
   } else if (V_local > 0 && N == 0) {
     // no rows: dW = 0

@@ -36,6 +36,7 @@ struct Item {
 // Optional per-item trace record (cce_debug_trace): 8 x u64 per queue position.
 struct TraceRec {
   unsigned long long q_type_c, smid, t_deq, t_ready, t_epi0, t_epi1, tile, pad;
+  unsigned long long t_load0, t_load1, t_mma0, t_mma1, t_full_wait, r0, r1, r2;  // pair kernel only
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;

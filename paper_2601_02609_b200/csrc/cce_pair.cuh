@@ -1,0 +1,615 @@
+// cce_pair.cuh -- the CCE hot path on CTA PAIRS: one persistent kernel, launched in
+// clusters of 2, that runs either the forward queue (logit tiles + online-softmax
+// epilogue) or the backward queue (recompute + dlogits, dW,
+// dH, rows a5-a8) with tcgen05.mma.cta_group::2.
+//
+// Why pairs: a 1-CTA 128x256 tile loads 48 KB of operands per 64-wide k-block and
+// was measured L2->SM bandwidth bound (~100 GB/s per SM, 0.48-0.61 us per k-block
+// against a 0.27 us tensor floor).  A pair computes a 256 x N tile with M=256 MMAs:
+// each CTA loads its own 128 rows of A and N/2 rows of B (32 KB per k-block at
+// N=256), i.e. 1.5x less operand traffic for the same tensor work.
+//
+// Roles (384 threads per CTA):
+//   warp 0   TMA producer (both CTAs): item from the local ring, dependency waits,
+//            loads of this CTA's operand halves (the leader arms each full barrier
+//            with both CTAs' transaction bytes)
+//   warp 1   leader: MMA issuer (one thread, cta_group::2); peer: idle
+//   warp 2   TMEM allocator (cta_group::2, 512 columns = 2 x 256 fp32 accumulators)
+//   warp 3   leader: scheduler -- dequeues items from the global queue and publishes
+//            them into both CTAs' rings up to 4 items ahead
+//   warps 4-11  epilogue: warp w reads TMEM lane quarter w%4 and column half (w-4)/4
+// The leader dequeues an item, checks its dependencies, and broadcasts it into
+// both CTAs' 4-entry item rings (the peer's over DSMEM with release/acquire
+// cluster-scope mbarriers).  Full barriers live in the leader; each CTA's TMA
+// signals its bytes there.  MMA completion is multicast to both CTAs' empty /
+// accumulator-full barriers; both epilogues report accumulator-empty to the leader.
+//
+// Tile orientation (all types: M = 256 per pair, accumulator row = TMEM lane):
+//   FWD  S  = Hc W^T           M = rows,  N = vocab (256), K = D    A,B K-major
+//   G    S  = Hc W_c^T -> G    M = rows,  N = vocab (256), K = D    A,B K-major
+//   DW   dW = G^T Hc           M = vocab, N = hidden (<=256), K = rows   A,B MN-major
+//   DH   dH += G W_c           M = rows,  N = hidden (<=256), K = vocab  A K-, B MN-major
+// Hidden-dimension tiles are 256 wide with a 128-wide tail (D = 896 -> 256,256,256,128),
+// so no MMA work is wasted and dW / dH rows are written as contiguous vectors.
+#pragma once
+#include "cce_bwd.cuh"
+#include "cce_gemm.cuh"
+
+namespace cce {
+namespace pairk {
+
+constexpr int PM = 256;                  // tile rows per pair
+constexpr int HM = 128;                  // tile rows per CTA
+constexpr int PN = 256;                  // max tile columns
+constexpr int PSTAGES = 6;
+constexpr int PA_BYTES = HM * BK * 2;        // 16 KB
+constexpr int PB_BYTES = (PN / 2) * BK * 2;  // 16 KB
+constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES;
+constexpr int PRING = 4;
+constexpr int PEPI_WARPS = 8;
+constexpr int PEPI_THREADS = 32 * PEPI_WARPS;
+constexpr int PTHREADS = 128 + PEPI_THREADS;
+constexpr int PSMEM = PSTAGES * PSTAGE_BYTES + 1024 /*align*/ + 1024 /*barriers+rings*/ + 1024 /*xchg*/;
+
+enum PType : int { PT_FWD = 0, PT_G = 1, PT_DW = 2, PT_DH = 3, PT_END = 4 };
+
+struct PItem {
+  int type, c, m0, n0, N, num_kb, tile_id, q;
+  unsigned long long t_deq, t_ready;
+};
+static_assert(sizeof(PItem) == 48, "PItem layout");
+
+struct PairParams {
+  GemmParams g;
+  int mode;        // 0 = forward queue, 1 = backward queue
+  int n_chunks;
+  int slots;       // Gbuf ring slots
+  int strict;      // debug bit 0: serialise every item behind all earlier ones;
+                   // debug bit 1: skip operand loads (measures raw MMA throughput; garbage results)
+  int* sched;      // zeroed: [0] head [1] done | g_done[n] | w_done[n] | dh_flag[n_dt * t256]
+  TraceRec* trace;
+  int trace_cap;
+};
+
+struct PCounts {
+  int nv, t256, n_dt, n_dh, tv;
+};
+
+__device__ __forceinline__ int dtile_N(int D, int dt) {
+  const int rem = D - dt * PN;
+  return rem >= PN ? PN : ((rem + 127) / 128) * 128;
+}
+
+__device__ __forceinline__ PItem make_item(int type, int c, int m0, int n0, int N, int num_kb, int tile_id, int q) {
+  PItem it;
+  it.type = type; it.c = c; it.m0 = m0; it.n0 = n0; it.N = N; it.num_kb = num_kb; it.tile_id = tile_id; it.q = q;
+  it.t_deq = 0; it.t_ready = 0;
+  return it;
+}
+
+__device__ __forceinline__ int p_chunk_width(const GemmParams& g, int c) {
+  const int rem = g.V_local - c * g.C;
+  return rem < g.C ? rem : g.C;
+}
+__device__ __forceinline__ int p_n_g(const PCounts& k, int w) { return k.t256 * ((w + PN - 1) / PN); }
+__device__ __forceinline__ int p_n_dw(const PCounts& k, int w) { return ((w + PM - 1) / PM) * k.n_dt; }
+
+// Forward queue: vocabulary tile outer, row tile inner (all row tiles share one W tile in L2).
+// Backward queue: G0, G1, W0, G2, W1, ..., W_{n-1}   (W_c = DH(c) items, then DW(c) items).
+__device__ PItem decode(const PairParams& P, const PCounts& k, int q) {
+  const GemmParams& g = P.g;
+  if (P.mode == 0) {
+    if (q < k.t256 * k.tv) return make_item(PT_FWD, 0, (q % k.t256) * PM, (q / k.t256) * PN, PN, g.D / BK, 0, q);
+    return make_item(PT_END, 0, 0, 0, 0, 0, 0, q);
+  }
+  const int n = P.n_chunks;
+  int r = q;
+  for (int ph = 0; ph < 2 * n; ++ph) {
+    int isG, c;
+    if (ph == 0) { isG = 1; c = 0; }
+    else if (ph == 2 * n - 1) { isG = 0; c = n - 1; }
+    else if (ph & 1) { isG = 1; c = (ph + 1) / 2; }
+    else { isG = 0; c = ph / 2 - 1; }
+    const int w = p_chunk_width(g, c);
+    const int c0 = c * g.C;
+    if (isG) {
+      const int cnt = p_n_g(k, w);
+      if (r < cnt) return make_item(PT_G, c, (r % k.t256) * PM, c0 + (r / k.t256) * PN, PN, g.D / BK, 0, q);
+      r -= cnt;
+    } else {
+      if (r < k.n_dh) {
+        const int dt = r % k.n_dt;
+        return make_item(PT_DH, c, (r / k.n_dt) * PM, dt * PN, dtile_N(g.D, dt), (w + BK - 1) / BK, r, q);
+      }
+      r -= k.n_dh;
+      const int cnt = p_n_dw(k, w);
+      if (r < cnt) {
+        const int dt = r % k.n_dt;
+        return make_item(PT_DW, c, (r / k.n_dt) * PM, dt * PN, dtile_N(g.D, dt), (k.nv + BK - 1) / BK, 0, q);
+      }
+      r -= cnt;
+    }
+  }
+  return make_item(PT_END, 0, 0, 0, 0, 0, 0, q);
+}
+
+// ------------------------------------------------------------------ epilogues (per CTA)
+struct PEpi {
+  int rit;      // row in this CTA's 128-row half == TMEM lane
+  int q, half;  // lane quarter, column half
+  int rank;
+  float* xchg;
+};
+
+__device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv) {
+  const int row = it.m0 + e.rank * HM + e.rit;
+  const bool rv = row < nv;
+  const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+  const int cb = e.half * (PN / 2);
+  float m = -INFINITY, d = 0.f;
+#pragma unroll 1
+  for (int j = 0; j < PN / 2 / 32; ++j) {
+    float v[32];
+    tmem_ld32(taddr + cb + j * 32, v);
+    const int col0 = it.n0 + cb + j * 32;
+    if (col0 >= p.V_local) break;  // warp-uniform
+    if (col0 + 32 > p.V_local) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i >= p.V_local) v[i] = -INFINITY;
+    }
+    float cmax = v[0];
+#pragma unroll
+    for (int i = 1; i < 32; ++i) cmax = fmaxf(cmax, v[i]);
+    const float mn = fmaxf(m, cmax);
+    const float ms = mn * LOG2E;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      s0 += ex2(fmaf(v[i], LOG2E, -ms));
+      s1 += ex2(fmaf(v[i + 1], LOG2E, -ms));
+    }
+    d = d * ex2((m - mn) * LOG2E) + (s0 + s1);
+    m = mn;
+    const unsigned off = (unsigned)(y - col0);
+    if (off < 32u) {
+      float zy = 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (off == (unsigned)i) zy = v[i];
+      p.zy_c[row] = zy;
+    }
+  }
+  float2* x = reinterpret_cast<float2*>(e.xchg);
+  if (e.half == 1) x[e.rit] = make_float2(m, d);
+  named_bar_sync(3 + e.q, 64);
+  if (e.half == 0) {
+    const float2 o = x[e.rit];
+    const float mn = fmaxf(m, o.x);
+    const float dd = (d > 0.f ? d * ex2((m - mn) * LOG2E) : 0.f) + (o.y > 0.f ? o.y * ex2((o.x - mn) * LOG2E) : 0.f);
+    if (rv) p.part[(size_t)(it.n0 / PN) * p.Npad + row] = make_float2(mn, dd);
+  }
+  named_bar_sync(3 + e.q, 64);
+}
+
+__device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv,
+                                      float scale, __nv_bfloat16* gslot) {
+  const int row = it.m0 + e.rank * HM + e.rit;
+  const bool rv = row < nv;
+  const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+  const float off2 = rv ? (p.lse_c[row] * LOG2E - __log2f(fabsf(scale))) : INFINITY;
+  const int c0 = it.c * p.C;
+  const int width = min(p.C, p.V_local - c0);
+  const int cb = e.half * (PN / 2);
+  __nv_bfloat16* out = gslot + (size_t)row * p.C + (it.n0 - c0) + cb;
+#pragma unroll 1
+  for (int j = 0; j < PN / 2 / 32; ++j) {
+    float v[32];
+    tmem_ld32(taddr + cb + j * 32, v);
+    const int lcol0 = (it.n0 - c0) + cb + j * 32;  // column within the chunk
+    const int col0 = c0 + lcol0;                   // local vocabulary row
+    float gg[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) gg[i] = ex2(fmaf(v[i], LOG2E, -off2));
+    if (scale < 0.f) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) gg[i] = -gg[i];
+    }
+    const unsigned toff = (unsigned)(y - col0);
+    if (toff < 32u) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (toff == (unsigned)i) gg[i] -= scale;
+    }
+    if (lcol0 + 32 > width) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (lcol0 + i >= width) gg[i] = 0.f;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + j * 32);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4)
+      dst[q4] = make_uint4(pack_bf16(gg[8 * q4], gg[8 * q4 + 1]), pack_bf16(gg[8 * q4 + 2], gg[8 * q4 + 3]),
+                           pack_bf16(gg[8 * q4 + 4], gg[8 * q4 + 5]), pack_bf16(gg[8 * q4 + 6], gg[8 * q4 + 7]));
+  }
+}
+
+__device__ __forceinline__ void epi_dw(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it,
+                                       bool have_acc) {
+  const int c0 = it.c * p.C;
+  const int width = min(p.C, p.V_local - c0);
+  const int vrow = it.m0 + e.rank * HM + e.rit;  // vocabulary row within the chunk
+  const int hw = it.N / 2;
+  const int cb = e.half * hw;
+#pragma unroll 1
+  for (int j = 0; j < hw / 32; ++j) {
+    float v[32];
+    if (have_acc) {
+      tmem_ld32(taddr + cb + j * 32, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    }
+    const int d0 = it.n0 + cb + j * 32;
+    if (vrow < width && d0 < p.D) {
+      uint4* dst = reinterpret_cast<uint4*>(p.dW + (size_t)(c0 + vrow) * p.D + d0);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        dst[q4] = make_uint4(pack_bf16(v[8 * q4], v[8 * q4 + 1]), pack_bf16(v[8 * q4 + 2], v[8 * q4 + 3]),
+                             pack_bf16(v[8 * q4 + 4], v[8 * q4 + 5]), pack_bf16(v[8 * q4 + 6], v[8 * q4 + 7]));
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_dh(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv) {
+  const int t = it.m0 + e.rank * HM + e.rit;  // compact row
+  const int hw = it.N / 2;
+  const int cb = e.half * hw;
+  const bool acc = it.c > 0;
+#pragma unroll 1
+  for (int j = 0; j < hw / 32; ++j) {
+    float v[32];
+    tmem_ld32(taddr + cb + j * 32, v);
+    const int d0 = it.n0 + cb + j * 32;
+    if (t < nv && d0 < p.D) {
+      float4* dst = reinterpret_cast<float4*>(p.dH32 + (size_t)t * p.D + d0);
+      if (acc) {
+        float4 o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = __ldcg(dst + i);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[4 * i] += o[i].x; v[4 * i + 1] += o[i].y; v[4 * i + 2] += o[i].z; v[4 * i + 3] += o[i].w;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) __stcg(dst + i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ MMA issue (leader warp)
+// All 32 lanes wait on the full barrier; one elected lane issues the 4 K=16 pair MMAs
+// of a 64-wide k-block and commits the stage back to both CTAs' empty barriers.  The
+// descriptors are built once per k-block; the per-K step is a constant added to the
+// start-address field (+32 B K-major, +2 KB MN-major, in 16-byte units).
+template <bool A_MN, bool B_MN>
+__device__ __forceinline__ void mma_item(const PItem& it, uint64_t* full_bar, uint64_t* empty_bar, uint32_t a_base,
+                                         uint32_t b_base, uint32_t tmem_d, uint32_t& stage, uint32_t& phase,
+                                         unsigned long long* wait_ns) {
+  const uint32_t idesc = idesc_bf16_f32(PM, it.N, A_MN ? 1 : 0, B_MN ? 1 : 0);
+  for (int kb = 0; kb < it.num_kb; ++kb) {
+    if (wait_ns) {
+      const unsigned long long w0 = gtimer();
+      mbar_wait(&full_bar[stage], phase);
+      *wait_ns += gtimer() - w0;
+    }
+    mbar_wait(&full_bar[stage], phase);
+    tc_fence_after();
+    const uint64_t ad = sdesc_sw128(a_base + stage * PA_BYTES, A_MN ? 8192 : 16, 1024);
+    const uint64_t bd = sdesc_sw128(b_base + stage * PB_BYTES, B_MN ? 8192 : 16, 1024);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk)
+        umma_bf16_pair(tmem_d, ad + (uint64_t)(A_MN ? 128 * kk : 2 * kk), bd + (uint64_t)(B_MN ? 128 * kk : 2 * kk),
+                       idesc, (kb | kk) ? 1u : 0u);
+      umma_commit_pair(&empty_bar[stage]);
+    }
+    __syncwarp();
+    if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
+    cce_pair_kernel(const __grid_constant__ CUtensorMap tmHcK, const __grid_constant__ CUtensorMap tmWK,
+                    const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
+                    const __grid_constant__ CUtensorMap tmGK, const __grid_constant__ CUtensorMap tmWMN,
+                    const PairParams P) {
+  const GemmParams& g = P.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + PSTAGES * PA_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + PSTAGES * PSTAGE_BYTES);
+  uint64_t* empty_bar = full_bar + PSTAGES;
+  uint64_t* tfull_bar = empty_bar + PSTAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* rfull_bar = tempty_bar + 2;
+  uint64_t* rempty_l = rfull_bar + PRING;   // leader: local consumers (MMA + epilogue warps)
+  uint64_t* rempty_p = rempty_l + PRING;    // leader: peer consumers (producer + epilogue warps)
+  PItem* ring = reinterpret_cast<PItem*>(rempty_p + PRING);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + PRING);
+  float* xchg = reinterpret_cast<float*>(smem + PSTAGES * PSTAGE_BYTES + 1024);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  int* head = P.sched;
+  int* done_total = P.sched + 1;
+  int* g_done = P.sched + 2;
+  int* w_done = P.sched + 2 + P.n_chunks;
+  int* dh_flag = P.sched + 2 + 2 * P.n_chunks;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmHcK); tma_prefetch_desc(&tmWK);
+    if (P.mode == 1) {
+      tma_prefetch_desc(&tmGMN); tma_prefetch_desc(&tmHcMN); tma_prefetch_desc(&tmGK); tma_prefetch_desc(&tmWMN);
+    }
+    for (int s = 0; s < PSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 2 * PEPI_WARPS); }
+    for (int r = 0; r < PRING; ++r) {
+      mbar_init(&rfull_bar[r], 1);
+      mbar_init(&rempty_l[r], 2 + PEPI_WARPS);  // leader producer + MMA + epilogue warps
+      mbar_init(&rempty_p[r], 1 + PEPI_WARPS);  // peer producer + epilogue warps
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  PCounts k;
+  k.nv = *g.n_valid;
+  k.t256 = (k.nv + PM - 1) / PM;
+  k.n_dt = (g.D + PN - 1) / PN;
+  k.n_dh = k.t256 * k.n_dt;
+  k.tv = (g.V_local + PN - 1) / PN;
+  const int slot_rows = g.Npad;
+
+  if (warp == 3) {
+    if (lane == 0 && rank == 0) {
+      // ===== scheduler (leader): dequeue items and publish them into both CTAs' rings,
+      // up to PRING items ahead of the consumers (hides the atomic and DSMEM latency).
+      uint32_t rs = 0, rph = 0;
+      while (true) {
+        const int q = atomicAdd(head, 1);
+        PItem it = decode(P, k, q);
+        if (P.trace) it.t_deq = gtimer();
+        mbar_wait(&rempty_l[rs], rph ^ 1);
+        mbar_wait(&rempty_p[rs], rph ^ 1);
+        ring[rs] = it;
+        const uint32_t remote = mapa_shared(smem_u32(&ring[rs]), 1);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&it);
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(PItem) / 4); ++i) st_cluster_u32(remote + 4 * i, w[i]);
+        mbar_arrive(&rfull_bar[rs]);
+        mbar_arrive_cluster(mapa_shared(smem_u32(&rfull_bar[rs]), 1));
+        if (++rs == PRING) { rs = 0; rph ^= 1; }
+        if (it.type == PT_END) break;
+      }
+    }
+  } else if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs): next item from the local ring, dependencies, loads
+      uint32_t stage = 0, phase = 0, rs = 0, rph = 0;
+      const uint32_t full_leader0 = mapa_shared(smem_u32(&full_bar[0]), 0);
+      while (true) {
+        if (rank == 0) mbar_wait(&rfull_bar[rs], rph);
+        else mbar_wait_cluster(&rfull_bar[rs], rph);
+        const PItem it = ring[rs];
+        if (rank == 0) mbar_arrive(&rempty_l[rs]);
+        else mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&rempty_p[rs]), 0));
+        if (++rs == PRING) { rs = 0; rph ^= 1; }
+        if (it.type == PT_END) break;
+        if (P.mode == 1) {
+          // dependencies: only on items earlier in the queue (deadlock-free)
+          if (P.strict & 1) wait_ge(done_total, 2 * it.q);
+          if (it.type == PT_G) {
+            if (it.c >= P.slots) {
+              const int wc = it.c - P.slots;
+              wait_ge(&w_done[wc], 2 * (k.n_dh + p_n_dw(k, p_chunk_width(g, wc))));
+            }
+          } else {
+            wait_ge(&g_done[it.c], 2 * p_n_g(k, p_chunk_width(g, it.c)));
+            if (it.type == PT_DH) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
+          }
+          fence_proxy_async_global();
+        }
+        if (P.trace && rank == 0 && it.q < P.trace_cap) P.trace[it.q].t_ready = gtimer();
+        // operand loads for this CTA's halves
+        const int hr = rank * HM;             // this CTA's first tile row
+        const int hn = rank * (it.N / 2);     // this CTA's first B row / column
+        const int b_bytes = (it.N / 2) * BK * 2;
+        const int slot_row0 = (it.c % P.slots) * slot_rows;
+        const int c0 = it.c * g.C;
+        unsigned long long tl0 = 0;
+        for (int kb = 0; kb < it.num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (P.trace && kb == 0) tl0 = gtimer();
+          uint8_t* a = sA + stage * PA_BYTES;
+          uint8_t* b = sB + stage * PB_BYTES;
+          const uint32_t fb = full_leader0 + stage * 8;
+          // the leader arms its full barrier with BOTH CTAs' bytes; the peer's TMA only
+          // signals completion bytes there (no per-stage remote arrive / release fence)
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
+          if (it.type == PT_FWD || it.type == PT_G) {
+            tma_load_2d_pair(&tmHcK, fb, a, kb * BK, it.m0 + hr);
+            tma_load_2d_pair(&tmWK, fb, b, kb * BK, it.n0 + hn);
+          } else if (it.type == PT_DW) {
+#pragma unroll
+            for (int j = 0; j < HM / 64; ++j)
+              tma_load_2d_pair(&tmGMN, fb, a + j * 8192, it.m0 + hr + j * 64, slot_row0 + kb * BK);
+            for (int j = 0; j < it.N / 2 / 64; ++j)
+              tma_load_2d_pair(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK);
+          } else {  // PT_DH
+            tma_load_2d_pair(&tmGK, fb, a, kb * BK, slot_row0 + it.m0 + hr);
+            for (int j = 0; j < it.N / 2 / 64; ++j)
+              tma_load_2d_pair(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK);
+          }
+          if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
+        }
+        if (P.trace && rank == 0 && it.q < P.trace_cap) {
+          P.trace[it.q].t_load0 = tl0;
+          P.trace[it.q].t_load1 = gtimer();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // ===== MMA issuer (leader): the whole warp runs the loop so every operand is
+      // warp-uniform; one elected lane issues the MMAs and commits.
+      uint32_t stage = 0, phase = 0, rs = 0, rph = 0;
+      int acc_it = 0;
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      while (true) {
+        mbar_wait(&rfull_bar[rs], rph);
+        const PItem it = ring[rs];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty_l[rs]);
+        if (++rs == PRING) { rs = 0; rph ^= 1; }
+        if (it.type == PT_END) break;
+        if (it.num_kb == 0) continue;
+        const uint32_t acc = acc_it & 1, acc_phase = (acc_it >> 1) & 1;
+        ++acc_it;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * PN;
+        const unsigned long long tm0 = P.trace ? gtimer() : 0ull;
+        const unsigned long long cm0 = P.trace ? clock64() : 0ull;
+        unsigned long long fw = 0;
+        unsigned long long* fwp = P.trace ? &fw : nullptr;
+        if (it.type == PT_DW)
+          mma_item<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+        else if (it.type == PT_DH)
+          mma_item<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+        else
+          mma_item<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+        if (elect_one()) umma_commit_pair(&tfull_bar[acc]);
+        __syncwarp();
+        if (P.trace && lane == 0 && it.q < P.trace_cap) {
+          P.trace[it.q].t_mma0 = tm0;
+          P.trace[it.q].t_mma1 = gtimer();
+          P.trace[it.q].t_full_wait = fw;
+          P.trace[it.q].r0 = clock64() - cm0;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue (both CTAs) =====
+    PEpi e;
+    e.q = warp & 3;
+    e.half = (warp - 4) >> 2;
+    e.rit = e.q * 32 + lane;
+    e.rank = rank;
+    e.xchg = xchg;
+    const bool leader = (threadIdx.x == 128);
+    const float scale = (P.mode == 1 && k.nv > 0) ? (*g.dloss) / (float)k.nv : 0.f;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    uint32_t rs = 0, rph = 0;
+    int acc_it = 0;
+    while (true) {
+      if (rank == 0) mbar_wait(&rfull_bar[rs], rph);
+      else mbar_wait_cluster(&rfull_bar[rs], rph);
+      const PItem it = ring[rs];
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) mbar_arrive(&rempty_l[rs]);
+        else mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&rempty_p[rs]), 0));
+      }
+      if (++rs == PRING) { rs = 0; rph ^= 1; }
+      if (it.type == PT_END) break;
+      const bool have_acc = it.num_kb > 0;
+      uint32_t acc = 0;
+      if (have_acc) {
+        acc = acc_it & 1;
+        const uint32_t acc_phase = (acc_it >> 1) & 1;
+        ++acc_it;
+        if (P.strict & 16) {
+          const uint32_t ba = smem_u32(&tfull_bar[acc]);
+          while (!mbar_try_wait(ba, acc_phase)) __nanosleep(256);
+        } else {
+          mbar_wait(&tfull_bar[acc], acc_phase);
+        }
+        tc_fence_after();
+      }
+      const uint32_t taddr = tmem_base + acc * PN + ((uint32_t)(e.q * 32) << 16);
+      const unsigned long long t_epi0 = P.trace ? gtimer() : 0ull;
+      if (P.strict & 4) {
+        // debug: skip the epilogue entirely (no TMEM reads, no stores)
+      } else if (it.type == PT_FWD) {
+        epi_fwd(g, taddr, e, it, k.nv);
+      } else if (it.type == PT_G) {
+        epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
+      } else if (it.type == PT_DW) {
+        epi_dw(g, taddr, e, it, have_acc);
+      } else {
+        // DH(c-1, tile) halves published; re-acquire so the .cg loads below see them
+        if (leader) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
+        named_bar_sync(2, PEPI_THREADS);
+        epi_dh(g, taddr, e, it, k.nv);
+      }
+      if (have_acc) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(&tempty_bar[acc]);
+          else mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);  // TMEM reads retired (wait::ld)
+        }
+      }
+      if (P.mode == 0 && P.trace && leader && rank == 0 && it.q < P.trace_cap) {
+        P.trace[it.q].q_type_c = ((unsigned long long)it.q << 32) | ((unsigned long long)it.type << 16) | (unsigned)it.c;
+        P.trace[it.q].smid = smid();
+        P.trace[it.q].t_deq = it.t_deq;
+        P.trace[it.q].t_epi0 = t_epi0;
+        P.trace[it.q].t_epi1 = gtimer();
+        P.trace[it.q].pad = it.num_kb;
+      }
+      if (P.mode == 1) {
+        // publish this CTA's half of the item: all stores, then one release per CTA
+        fence_proxy_async_global();
+        __threadfence();
+        named_bar_sync(1, PEPI_THREADS);
+        if (leader) {
+          if (P.trace && rank == 0 && it.q < P.trace_cap) {
+            TraceRec& r = P.trace[it.q];
+            r.q_type_c = ((unsigned long long)it.q << 32) | ((unsigned long long)it.type << 16) | (unsigned)it.c;
+            r.smid = smid();
+            r.t_deq = it.t_deq;
+            r.t_epi0 = t_epi0;
+            r.t_epi1 = gtimer();
+            r.tile = ((unsigned long long)it.m0 << 32) | (unsigned)it.n0;
+            r.pad = it.num_kb;
+          }
+          if (it.type == PT_G) atomicAdd(&g_done[it.c], 1);
+          else {
+            if (it.type == PT_DH) atomicAdd(&dh_flag[it.tile_id], 1);
+            atomicAdd(&w_done[it.c], 1);
+          }
+          atomicAdd(done_total, 1);
+        }
+      }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair(tmem_base, TMEM_COLS);
+}
+
+}  // namespace pairk
+}  // namespace cce

@@ -1,0 +1,61 @@
+"""Per-item timeline of the pair kernels (forward + backward) via cce_debug_trace."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2601_02609_b200 as cce  # noqa: E402
+import workload  # noqa: E402
+from cce_testutil import to_dev  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "qwen05b"
+out = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "trace_pair.npz")
+dev = torch.device("cuda:0")
+c = workload.CONFIGS[cfg]
+p = workload.make_config(cfg, seed=42)
+H, W, y = to_dev(p, dev)
+h = cce.CCEHandle(vocab_total=c.V)
+dH = torch.empty(H.shape, dtype=torch.bfloat16, device=dev)
+dW = torch.empty(W.shape, dtype=torch.bfloat16, device=dev)
+one = torch.ones((), dtype=torch.float32, device=dev)
+for _ in range(3):
+    h.forward(H, W, y)
+    h.backward(one, dH, dW)
+CAP = 60000
+buf = torch.zeros(2 * CAP * 128, dtype=torch.uint8, device=dev)
+cce.cce_debug_trace(h.h, buf)
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+ev[0].record()
+h.forward(H, W, y)
+ev[1].record()
+h.backward(one, dH, dW)
+ev[2].record()
+torch.cuda.synchronize()
+cce.cce_debug_trace(h.h, None)
+allrec = buf.view(torch.int64).view(2, CAP, 16).cpu().numpy().astype(np.uint64)
+np.savez(out, bwd=allrec[0], fwd=allrec[1])
+print(f"{cfg}: fwd {ev[0].elapsed_time(ev[1]):.3f} ms, bwd {ev[1].elapsed_time(ev[2]):.3f} ms")
+NAMES = {0: "FWD", 1: "G", 2: "DW", 3: "DH"}
+for name, rec in (("forward", allrec[1]), ("backward", allrec[0])):
+    rec = rec[rec[:, 5] > 0]
+    if len(rec) == 0:
+        continue
+    typ = ((rec[:, 0] >> 16) & 0xFFFF).astype(np.int64)
+    t0 = rec[:, 2].min()
+    f = lambda i: (rec[:, i].astype(np.float64) - float(t0)) / 1e3  # noqa: E731
+    deq, rdy, ep0, ep1, l0, l1, m0, m1 = [f(i) for i in (2, 3, 4, 5, 8, 9, 10, 11)]
+    fw = rec[:, 12].astype(np.float64) / 1e3
+    kb = rec[:, 7].astype(np.float64)
+    cyc = rec[:, 13].astype(np.float64)
+    print(f" {name}: items {len(rec)} span {ep1.max():.1f} us")
+    for t in sorted(set(typ.tolist())):
+        m = typ == t
+        print(f"   {NAMES[t]:3s} n={m.sum():6d} kb={kb[m].mean():5.1f} | mma window {np.mean(m1[m]-m0[m]):7.2f} us "
+              f"(full-wait {np.mean(fw[m]):6.2f}) | load window {np.mean(l1[m]-l0[m]):7.2f} | "
+              f"mma_end->epi0 {np.mean(ep0[m]-m1[m]):6.2f} | epi {np.mean(ep1[m]-ep0[m]):6.2f} | "
+              f"per-kb {np.mean((m1[m]-m0[m])/np.maximum(kb[m],1)):.3f} us, {np.mean(cyc[m]/np.maximum(kb[m],1)):.0f} cyc"
+              f" (clock {np.sum(cyc[m])/np.sum((m1[m]-m0[m])*1e3):.2f} GHz)")
