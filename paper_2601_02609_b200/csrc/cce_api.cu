@@ -113,6 +113,21 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t r
   return r == CUDA_SUCCESS;
 }
 
+// 3-D bf16 tensor map over the column-blocked dlogits ring [blocks][rows][64]:
+// dims {64, rows, blocks}, box {64, box_rows, 1}, 128-byte swizzle.
+static bool make_map_blocked(CUtensorMap* m, const void* base, uint64_t rows, uint64_t blocks, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {64, rows, blocks};
+  cuuint64_t strides[2] = {128, rows * 128};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // ------------------------------------------------------------------ NCCL (dlopen)
 namespace {
 struct NcclId {
@@ -512,8 +527,9 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
       // CTA-pair persistent backward: G / DW / DH tiles of every chunk from one work queue
       CUtensorMap mHcK, mWK, mGMN, mHcMN, mGK, mWMN;
       if (!make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM) || !make_map(&mWK, h->W, D, V_local, h->ldw, pairk::PN / 2) ||
-          !make_map(&mGMN, G, L.C, GBUF_SLOTS * L.Npad, L.C, 64) || !make_map(&mHcMN, Hc, D, L.Npad, D, 64) ||
-          !make_map(&mGK, G, L.C, GBUF_SLOTS * L.Npad, L.C, pairk::HM) ||
+          !make_map_blocked(&mGMN, G, L.Npad, GBUF_SLOTS * (L.C / 64), 64) ||
+          !make_map(&mHcMN, Hc, D, L.Npad, D, 64) ||
+          !make_map_blocked(&mGK, G, L.Npad, GBUF_SLOTS * (L.C / 64), pairk::HM) ||
           !make_map(&mWMN, h->W, D, V_local, h->ldw, 64))
         return CCE_ERR_CUDA;
       if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;

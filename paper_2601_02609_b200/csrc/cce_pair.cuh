@@ -29,6 +29,8 @@
 //   G    S  = Hc W_c^T -> G    M = rows,  N = vocab (256), K = D    A,B K-major
 //   DW   dW = G^T Hc           M = vocab, N = hidden (<=256), K = rows   A,B MN-major
 //   DH   dH += G W_c           M = rows,  N = hidden (<=256), K = vocab  A K-, B MN-major
+// The chunk dlogits G live in a column-blocked ring [slot][C/64][Npad][64] (bf16), so
+// every TMA box of G and every epilogue store is one contiguous run in HBM.
 // Hidden-dimension tiles are 256 wide with a 128-wide tail (D = 896 -> 256,256,256,128),
 // so no MMA work is wasted and dW / dH rows are written as contiguous vectors.
 #pragma once
@@ -49,7 +51,9 @@ constexpr int PRING = 4;
 constexpr int PEPI_WARPS = 8;
 constexpr int PEPI_THREADS = 32 * PEPI_WARPS;
 constexpr int PTHREADS = 128 + PEPI_THREADS;
-constexpr int PSMEM = PSTAGES * PSTAGE_BYTES + 1024 /*align*/ + 1024 /*barriers+rings*/ + 1024 /*xchg*/;
+constexpr int PSMEM = PSTAGES * PSTAGE_BYTES + 1024 /*align*/ + 1024 /*barriers+rings*/ + 1024 /*xchg*/ +
+                      PEPI_WARPS * 4096 /*epilogue store staging*/;
+static_assert(PSMEM <= 232448, "pair kernel shared memory");
 
 enum PType : int { PT_FWD = 0, PT_G = 1, PT_DW = 2, PT_DH = 3, PT_END = 4 };
 
@@ -139,6 +143,7 @@ struct PEpi {
   int q, half;  // lane quarter, column half
   int rank;
   float* xchg;
+  uint8_t* stage;  // this warp's 4 KB store-staging tile
 };
 
 __device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv) {
@@ -194,6 +199,10 @@ __device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, con
 
 __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv,
                                       float scale, __nv_bfloat16* gslot) {
+  // G = s (exp(S - lse) - 1[v = y]) with s folded into the exponent.
+  // Each warp converts 64 columns of its 32 rows at a time into a 4 KB SMEM tile
+  // (16-byte chunks XOR-swizzled by row: conflict-free), then writes it out as
+  // fully coalesced 512-byte runs of the column-blocked G ring.
   const int row = it.m0 + e.rank * HM + e.rit;
   const bool rv = row < nv;
   const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
@@ -201,36 +210,53 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
   const int c0 = it.c * p.C;
   const int width = min(p.C, p.V_local - c0);
   const int cb = e.half * (PN / 2);
-  __nv_bfloat16* out = gslot + (size_t)row * p.C + (it.n0 - c0) + cb;
+  const int lane = e.rit & 31;
+  uint4* stg = reinterpret_cast<uint4*>(e.stage);  // [32 rows][8 x 16 B]
+  const int row0 = it.m0 + e.rank * HM + (e.rit & ~31);  // first row of this warp
 #pragma unroll 1
-  for (int j = 0; j < PN / 2 / 32; ++j) {
-    float v[32];
-    tmem_ld32(taddr + cb + j * 32, v);
-    const int lcol0 = (it.n0 - c0) + cb + j * 32;  // column within the chunk
-    const int col0 = c0 + lcol0;                   // local vocabulary row
-    float gg[32];
+  for (int j2 = 0; j2 < PN / 2 / 64; ++j2) {
+    const int lcol64 = (it.n0 - c0) + cb + j2 * 64;  // 64-column block within the chunk
 #pragma unroll
-    for (int i = 0; i < 32; ++i) gg[i] = ex2(fmaf(v[i], LOG2E, -off2));
-    if (scale < 0.f) {
+    for (int h = 0; h < 2; ++h) {
+      float v[32];
+      tmem_ld32(taddr + cb + j2 * 64 + h * 32, v);
+      const int lcol0 = lcol64 + h * 32;
+      const int col0 = c0 + lcol0;
+      float gg[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) gg[i] = -gg[i];
+      for (int i = 0; i < 32; ++i) gg[i] = ex2(fmaf(v[i], LOG2E, -off2));
+      if (scale < 0.f) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) gg[i] = -gg[i];
+      }
+      const unsigned toff = (unsigned)(y - col0);
+      if (toff < 32u) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (toff == (unsigned)i) gg[i] -= scale;
+      }
+      if (lcol0 + 32 > width) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (lcol0 + i >= width) gg[i] = 0.f;
+      }
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int chunk = h * 4 + q4;
+        stg[lane * 8 + (chunk ^ (lane & 7))] =
+            make_uint4(pack_bf16(gg[8 * q4], gg[8 * q4 + 1]), pack_bf16(gg[8 * q4 + 2], gg[8 * q4 + 3]),
+                       pack_bf16(gg[8 * q4 + 4], gg[8 * q4 + 5]), pack_bf16(gg[8 * q4 + 6], gg[8 * q4 + 7]));
+      }
     }
-    const unsigned toff = (unsigned)(y - col0);
-    if (toff < 32u) {
+    __syncwarp();
+    // 32 rows x 128 B of block (lcol64 / 64) are contiguous in the blocked layout
+    uint4* dst = reinterpret_cast<uint4*>(gslot + ((size_t)(lcol64 >> 6) * p.Npad + row0) * 64);
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (toff == (unsigned)i) gg[i] -= scale;
+    for (int i = 0; i < 8; ++i) {
+      const int r = i * 4 + (lane >> 3), c = lane & 7;
+      dst[r * 8 + c] = stg[r * 8 + (c ^ (r & 7))];
     }
-    if (lcol0 + 32 > width) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (lcol0 + i >= width) gg[i] = 0.f;
-    }
-    uint4* dst = reinterpret_cast<uint4*>(out + j * 32);
-#pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4)
-      dst[q4] = make_uint4(pack_bf16(gg[8 * q4], gg[8 * q4 + 1]), pack_bf16(gg[8 * q4 + 2], gg[8 * q4 + 3]),
-                           pack_bf16(gg[8 * q4 + 4], gg[8 * q4 + 5]), pack_bf16(gg[8 * q4 + 6], gg[8 * q4 + 7]));
+    __syncwarp();
   }
 }
 
@@ -341,6 +367,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   PItem* ring = reinterpret_cast<PItem*>(rempty_p + PRING);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + PRING);
   float* xchg = reinterpret_cast<float*>(smem + PSTAGES * PSTAGE_BYTES + 1024);
+  uint8_t* stage_base = smem + PSTAGES * PSTAGE_BYTES + 2048;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -433,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         const int hr = rank * HM;             // this CTA's first tile row
         const int hn = rank * (it.N / 2);     // this CTA's first B row / column
         const int b_bytes = (it.N / 2) * BK * 2;
-        const int slot_row0 = (it.c % P.slots) * slot_rows;
+        const int slot_blk0 = (it.c % P.slots) * (g.C / 64);  // first 64-column block of the slot
         const int c0 = it.c * g.C;
         unsigned long long tl0 = 0;
         for (int kb = 0; kb < it.num_kb; ++kb) {
@@ -451,11 +478,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           } else if (it.type == PT_DW) {
 #pragma unroll
             for (int j = 0; j < HM / 64; ++j)
-              tma_load_2d_pair(&tmGMN, fb, a + j * 8192, it.m0 + hr + j * 64, slot_row0 + kb * BK);
+              tma_load_3d_pair(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j);
             for (int j = 0; j < it.N / 2 / 64; ++j)
               tma_load_2d_pair(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK);
           } else {  // PT_DH
-            tma_load_2d_pair(&tmGK, fb, a, kb * BK, slot_row0 + it.m0 + hr);
+            tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb);
             for (int j = 0; j < it.N / 2 / 64; ++j)
               tma_load_2d_pair(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK);
           }
@@ -515,6 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     e.rit = e.q * 32 + lane;
     e.rank = rank;
     e.xchg = xchg;
+    e.stage = stage_base + (warp - 4) * 4096;
     const bool leader = (threadIdx.x == 128);
     const float scale = (P.mode == 1 && k.nv > 0) ? (*g.dloss) / (float)k.nv : 0.f;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
@@ -552,14 +580,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       } else if (it.type == PT_FWD) {
         epi_fwd(g, taddr, e, it, k.nv);
       } else if (it.type == PT_G) {
-        epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
+        if (!(P.strict & 32)) epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
       } else if (it.type == PT_DW) {
         epi_dw(g, taddr, e, it, have_acc);
       } else {
         // DH(c-1, tile) halves published; re-acquire so the .cg loads below see them
         if (leader) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
         named_bar_sync(2, PEPI_THREADS);
-        epi_dh(g, taddr, e, it, k.nv);
+        if (!(P.strict & 64)) epi_dh(g, taddr, e, it, k.nv);
       }
       if (have_acc) {
         tc_fence_before();

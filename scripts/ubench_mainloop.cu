@@ -24,7 +24,7 @@ constexpr int KB = 14, ST = 6;
 
 // PAIR=0: 128x256 tile per CTA (A 16 KB + B 32 KB per stage). PAIR=1: 256x256 per pair
 // (each CTA: A 16 KB + B 16 KB per stage).
-template <int PAIR>
+template <int PAIR, int SPLIT = 0>
 __global__ void __launch_bounds__(128, 1) kml(const __grid_constant__ CUtensorMap ta,
                                               const __grid_constant__ CUtensorMap tb, int tiles_m, int tiles_total,
                                               unsigned long long* out) {
@@ -58,8 +58,15 @@ __global__ void __launch_bounds__(128, 1) kml(const __grid_constant__ CUtensorMa
         mbar_wait(&empty[st], ph ^ 1);
         if (PAIR) {
           if (rank == 0) mbar_arrive_expect_tx(&full[st], 2 * (A_B + B_B));
-          tma_load_2d_pair(&ta, fb0 + st * 8, sA + st * A_B, kb * 64, mt * 256 + rank * 128);
-          tma_load_2d_pair(&tb, fb0 + st * 8, sB + st * B_B, kb * 64, nt * 256 + rank * 128);
+          if (SPLIT) {  // same bytes as 4 boxes of 64 rows (the MN-major pattern's box count)
+            for (int j = 0; j < 2; ++j) {
+              tma_load_2d_pair(&ta, fb0 + st * 8, sA + st * A_B + j * 8192, kb * 64, mt * 256 + rank * 128 + j * 64);
+              tma_load_2d_pair(&tb, fb0 + st * 8, sB + st * B_B + j * 8192, kb * 64, nt * 256 + rank * 128 + j * 64);
+            }
+          } else {
+            tma_load_2d_pair(&ta, fb0 + st * 8, sA + st * A_B, kb * 64, mt * 256 + rank * 128);
+            tma_load_2d_pair(&tb, fb0 + st * 8, sB + st * B_B, kb * 64, nt * 256 + rank * 128);
+          }
         } else {
           mbar_arrive_expect_tx(&full[st], A_B + B_B);
           tma_load_2d(&ta, &full[st], sA + st * A_B, kb * 64, mt * 128);
@@ -108,14 +115,14 @@ __global__ void fill_random(uint16_t* p, size_t n, uint32_t seed) {
   }
 }
 
-template <int PAIR>
+template <int PAIR, int SPLIT = 0>
 void run(void* A, void* B, int rows, int cols) {
   CUtensorMap ta, tb;
-  mk(&ta, A, 896, rows, PAIR ? 128 : 128);
-  mk(&tb, B, 896, cols, PAIR ? 128 : 256);
+  mk(&ta, A, 896, rows, SPLIT ? 64 : 128);
+  mk(&tb, B, 896, cols, SPLIT ? 64 : (PAIR ? 128 : 256));
   const int tiles_m = PAIR ? rows / 256 : rows / 128, tiles_n = cols / 256;
   const int smem = ST * (16384 + (PAIR ? 16384 : 32768)) + 1024;
-  auto k = kml<PAIR>;
+  auto k = kml<PAIR, SPLIT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   unsigned long long* d;
   cudaMalloc(&d, 148 * 8);
@@ -170,5 +177,8 @@ int main() {
   printf("random data:\n");
   run<1>(A, B, rows, cols);
   run<1>(A, B, rows, cols);
+  printf("random data, 64-row boxes (4 TMA per CTA per k-block):\n");
+  run<1, 1>(A, B, rows, cols);
+  run<1, 1>(A, B, rows, cols);
   return 0;
 }
