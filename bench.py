@@ -207,8 +207,7 @@ def main():
     cce.lib()
 
     c = workload.CONFIGS[args.config]
-    lo = rank * c.V // world
-    hi = (rank + 1) * c.V // world
+    lo, hi = cce.shard_range(c.V, rank, world)
     p = workload.make_config(args.config, seed=args.seed, w_rows=(lo, hi))
     n_valid = int((p["labels"] != -100).sum())
     H = torch.from_numpy(p["H"].view(np.int16)).view(torch.bfloat16).to(dev)

@@ -210,6 +210,14 @@ def cce_nccl_comm_destroy(comm):
 
 
 # ----------------------------------------------------------------- convenience
+def shard_range(V: int, rank: int, world: int):
+    """Contiguous vocabulary shard [lo, hi) owned by `rank` (sizes differ by at most 1;
+    any size is allowed, including empty shards when world > V)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    return rank * V // world, (rank + 1) * V // world
+
+
 class CCEHandle:
     """A library handle plus a cached device workspace (torch-allocated)."""
 

@@ -9,7 +9,7 @@
 #include "../paper_2601_02609_b200/csrc/sm100.cuh"
 using namespace cce;
 
-template <int PAIR>
+template <int PAIR, int AMN = 0, int BMN = 0>
 __global__ void __launch_bounds__(128, 1) kmma(int iters, unsigned long long* out, int n_k_major) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(128, 1) kmma(int iters, unsigned long long* ou
   const uint32_t tmem = slot;
   unsigned long long t0 = 0, t1 = 0;
   if (warp == 0 && lane == 0 && rank == 0) {
-    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 16384);
-    const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, 256, 0, 0);
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+    const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, 256, AMN, BMN);
     uint32_t ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -41,8 +41,8 @@ __global__ void __launch_bounds__(128, 1) kmma(int iters, unsigned long long* ou
       tc_fence_after();
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint64_t ad = sdesc_sw128(a + k * 32, 16, 1024);
-        const uint64_t bd = sdesc_sw128(b + k * 32, 16, 1024);
+        const uint64_t ad = AMN ? sdesc_sw128(a + k * 2048, 8192, 1024) : sdesc_sw128(a + k * 32, 16, 1024);
+        const uint64_t bd = BMN ? sdesc_sw128(b + k * 2048, 8192, 1024) : sdesc_sw128(b + k * 32, 16, 1024);
         if (PAIR) umma_bf16_pair(tmem + (it & 1) * 256, ad, bd, idesc, k > 0 ? 1u : 0u);
         else umma_bf16(tmem + (it & 1) * 256, ad, bd, idesc, k > 0 ? 1u : 0u);
       }
@@ -61,17 +61,17 @@ __global__ void __launch_bounds__(128, 1) kmma(int iters, unsigned long long* ou
   }
 }
 
-template <int PAIR>
+template <int PAIR, int AMN = 0, int BMN = 0>
 void run(int grid, int iters) {
   unsigned long long* d;
   cudaMalloc(&d, grid * 8);
   cudaMemset(d, 0, grid * 8);
-  auto k = kmma<PAIR>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  auto k = kmma<PAIR, AMN, BMN>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = 64 * 1024;
+  cfg.dynamicSmemBytes = 80 * 1024;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = PAIR ? 2 : 1;
@@ -94,16 +94,16 @@ void run(int grid, int iters) {
   unsigned long long mx = 0;
   for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
   const double flops = (double)grid * iters * 4 * 128.0 * 256 * 16 * 2;  // per CTA share
-  printf("%s grid=%d iters=%d err=%s: %.3f ms, %.1f TFLOP/s, max cycles/kblock %.1f (ideal 512)\n",
-         PAIR ? "pair M=256" : "1cta M=128", grid, iters, cudaGetErrorString(err), ms, flops / ms / 1e9,
+  printf("amn=%d bmn=%d %s grid=%d iters=%d err=%s: %.3f ms, %.1f TFLOP/s, max cycles/kblock %.1f (ideal 512)\n",
+         AMN, BMN, PAIR ? "pair M=256" : "1cta M=128", grid, iters, cudaGetErrorString(err), ms, flops / ms / 1e9,
          (double)mx / iters);
   cudaFree(d);
 }
 
 int main() {
-  run<0>(148, 20000);
   run<1>(148, 20000);
-  run<0>(2, 20000);
-  run<1>(2, 20000);
+  run<1, 0, 1>(148, 20000);
+  run<1, 1, 1>(148, 20000);
+  run<1, 1, 0>(148, 20000);
   return 0;
 }
