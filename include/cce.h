@@ -78,6 +78,9 @@ typedef enum {
 /* Kernels: 0 (default) = CTA-pair kernels (tcgen05.mma.cta_group::2, 256-row
  * tiles); CCE_FLAG_ONE_CTA = single-CTA 128x256-tile kernels (kept for A/B). */
 #define CCE_FLAG_ONE_CTA 4u
+/* CTA-pair kernels without cross-pair TMA multicast (default: 4-CTA clusters = two
+ * pairs sharing one operand by multicast). */
+#define CCE_FLAG_PAIR 8u
 
 typedef struct {
   int32_t ignore_index;   /* label value that marks a skipped row; -100 in the paper */

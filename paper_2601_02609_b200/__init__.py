@@ -33,6 +33,8 @@ PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 # "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
 # FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
 FLAG_BWD_PER_CHUNK = 2
+FLAG_ONE_CTA = 4
+FLAG_PAIR = 8
 
 
 class CCEError(RuntimeError):

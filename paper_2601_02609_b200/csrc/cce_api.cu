@@ -16,6 +16,7 @@
 #include "cce_bwd.cuh"
 #include "cce_gemm.cuh"
 #include "cce_pair.cuh"
+#include "cce_quad.cuh"
 
 using namespace cce;
 
@@ -260,6 +261,23 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
+cce_status launch_quad(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
+                       const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5,
+                       const pairk::PairParams& pp, cudaStream_t s, int prof_class) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(quadk::cce_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, quadk::QSMEM) !=
+        cudaSuccess)
+      return CCE_ERR_CUDA;
+    attr = true;
+  }
+  const int grid = (h->num_sms / 4) * 4;  // whole 4-CTA clusters
+  {
+    ProfScope ps(h, s, prof_class);
+    quadk::cce_quad_kernel<<<grid, quadk::QTHREADS, quadk::QSMEM, s>>>(m0, m1, m2, m3, m4, m5, pp);
+  }
+  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+}
 }  // namespace
 
 // ------------------------------------------------------------------ API
@@ -435,20 +453,24 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
       cce_status st = launch_gemm<MODE_FWD>(h, tA, tB, p, s);
       if (st != CCE_OK) return st;
     } else {
+      const bool quad = !(h->cfg.flags & CCE_FLAG_PAIR);
       CUtensorMap tA, tB;
       if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM)) return CCE_ERR_CUDA;
-      if (!make_map(&tB, W, D, V_local, ldw, pairk::PN / 2)) return CCE_ERR_CUDA;
+      if (!make_map(&tB, W, D, V_local, ldw, quad ? 64 : pairk::PN / 2)) return CCE_ERR_CUDA;
       if (cudaMemsetAsync(at<int>(ws, L.sched), 0, 8, s) != cudaSuccess) return CCE_ERR_CUDA;
       pairk::PairParams pp{};
       pp.g = p;
       pp.mode = 0;
       pp.n_chunks = 0;
       pp.slots = GBUF_SLOTS;
+      pp.prefetch = 0;
+      if (const char* e = getenv("CCE_PREFETCH_FWD")) pp.prefetch = atoi(e);
       if (const char* e = getenv("CCE_DEBUG_STRICT")) pp.strict = atoi(e);
       pp.sched = at<int>(ws, L.sched);
       pp.trace = static_cast<TraceRec*>(h->fwd_trace);
       pp.trace_cap = (int)(h->fwd_trace_bytes / sizeof(TraceRec));
-      cce_status st = launch_pair(h, tA, tB, tA, tA, tA, tA, pp, s, 0);
+      cce_status st = quad ? launch_quad(h, tA, tB, tA, tA, tA, tA, pp, s, 0)
+                           : launch_pair(h, tA, tB, tA, tA, tA, tA, pp, s, 0);
       if (st != CCE_OK) return st;
     }
   }
@@ -524,12 +546,15 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     if (const char* e = getenv("CCE_DEBUG_SLOTS")) slots = atoi(e) >= 2 && atoi(e) <= GBUF_SLOTS ? atoi(e) : GBUF_SLOTS;
     if (const char* e = getenv("CCE_DEBUG_STRICT")) strict = atoi(e);
     if (!(h->cfg.flags & CCE_FLAG_ONE_CTA)) {
-      // CTA-pair persistent backward: G / DW / DH tiles of every chunk from one work queue
+      // CTA-pair (or quad: two pairs sharing an operand by TMA multicast) persistent
+      // backward: G / DW / DH tiles of every chunk from one work queue
+      const bool quad = !(h->cfg.flags & CCE_FLAG_PAIR);
       CUtensorMap mHcK, mWK, mGMN, mHcMN, mGK, mWMN;
-      if (!make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM) || !make_map(&mWK, h->W, D, V_local, h->ldw, pairk::PN / 2) ||
+      if (!make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM) ||
+          !make_map(&mWK, h->W, D, V_local, h->ldw, quad ? 64 : pairk::PN / 2) ||
           !make_map_blocked(&mGMN, G, L.Npad, GBUF_SLOTS * (L.C / 64), 64) ||
           !make_map(&mHcMN, Hc, D, L.Npad, D, 64) ||
-          !make_map_blocked(&mGK, G, L.Npad, GBUF_SLOTS * (L.C / 64), pairk::HM) ||
+          !make_map_blocked(&mGK, G, L.Npad, GBUF_SLOTS * (L.C / 64), quad ? 64 : pairk::HM) ||
           !make_map(&mWMN, h->W, D, V_local, h->ldw, 64))
         return CCE_ERR_CUDA;
       if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
@@ -539,10 +564,13 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
       pp.n_chunks = (int)L.n_chunks;
       pp.slots = slots;
       pp.strict = strict;
+      pp.prefetch = 0;  // L2 prefetch measured harmful (adds L2 requests); env CCE_PREFETCH to experiment
+      if (const char* e = getenv("CCE_PREFETCH")) pp.prefetch = atoi(e);
       pp.sched = at<int>(ws, L.sched);
       pp.trace = static_cast<TraceRec*>(h->trace);
       pp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
-      cce_status st = launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, pp, s, 1);
+      cce_status st = quad ? launch_quad(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, pp, s, 1)
+                           : launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, pp, s, 1);
       if (st != CCE_OK) return st;
     } else {
     CUtensorMap mHcK, mWK, mHcMN, mGMN, mWMN, mGK;

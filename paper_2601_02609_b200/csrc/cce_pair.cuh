@@ -68,6 +68,7 @@ struct PairParams {
   int mode;        // 0 = forward queue, 1 = backward queue
   int n_chunks;
   int slots;       // Gbuf ring slots
+  int prefetch;    // k-blocks of L2 prefetch (TMA prefetch.tensor) beyond the SMEM ring
   int strict;      // debug bit 0: serialise every item behind all earlier ones;
                    // debug bit 1: skip operand loads (measures raw MMA throughput; garbage results)
   int* sched;      // zeroed: [0] head [1] done | g_done[n] | w_done[n] | dh_flag[n_dt * t256]
@@ -472,6 +473,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           // the leader arms its full barrier with BOTH CTAs' bytes; the peer's TMA only
           // signals completion bytes there (no per-stage remote arrive / release fence)
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
+          // L2 prefetch `prefetch` k-blocks ahead of this load (hides HBM latency beyond
+          // the 6-stage SMEM ring; no SMEM or barrier involved)
+          const int pk = kb + P.prefetch;
+          if (P.prefetch > 0 && pk < it.num_kb) {
+            if (it.type == PT_FWD || it.type == PT_G) {
+              tma_prefetch_2d(&tmHcK, pk * BK, it.m0 + hr);
+              tma_prefetch_2d(&tmWK, pk * BK, it.n0 + hn);
+            } else if (it.type == PT_DW) {
+#pragma unroll
+              for (int j = 0; j < HM / 64; ++j) tma_prefetch_3d(&tmGMN, 0, pk * BK, slot_blk0 + (it.m0 + hr) / 64 + j);
+              for (int j = 0; j < it.N / 2 / 64; ++j) tma_prefetch_2d(&tmHcMN, it.n0 + hn + j * 64, pk * BK);
+            } else {
+              tma_prefetch_3d(&tmGK, 0, it.m0 + hr, slot_blk0 + pk);
+              for (int j = 0; j < it.N / 2 / 64; ++j) tma_prefetch_2d(&tmWMN, it.n0 + hn + j * 64, c0 + pk * BK);
+            }
+          }
           if (it.type == PT_FWD || it.type == PT_G) {
             tma_load_2d_pair(&tmHcK, fb, a, kb * BK, it.m0 + hr);
             tma_load_2d_pair(&tmWK, fb, b, kb * BK, it.n0 + hn);
@@ -606,11 +623,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         P.trace[it.q].pad = it.num_kb;
       }
       if (P.mode == 1) {
-        // publish this CTA's half of the item: all stores, then one release per CTA
+        // publish this CTA's half of the item: every thread's stores are ordered before
+        // the named barrier; the publishing thread's gpu-scope fence is cumulative
         fence_proxy_async_global();
-        __threadfence();
         named_bar_sync(1, PEPI_THREADS);
         if (leader) {
+          __threadfence();
           if (P.trace && rank == 0 && it.q < P.trace_cap) {
             TraceRec& r = P.trace[it.q];
             r.q_type_c = ((unsigned long long)it.q << 32) | ((unsigned long long)it.type << 16) | (unsigned)it.c;

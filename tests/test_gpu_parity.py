@@ -33,7 +33,7 @@ def test_tiny_config(dev, seed):
     _check(workload.make_config("tiny", seed=seed), dev)
 
 
-@pytest.mark.parametrize("flags", [0, 4, 6], ids=["pair", "cta1_queue", "cta1_per_chunk"])
+@pytest.mark.parametrize("flags", [0, 8, 4, 6], ids=["quad", "pair", "cta1_queue", "cta1_per_chunk"])
 @pytest.mark.parametrize("N,D,V,ign", [
     (700, 128, 3000, "bern40"),        # ragged rows (5.5 tiles), ragged vocab (11.7 tiles)
     (257, 64, 256, "none"),             # exactly one vocab tile, one ragged row
