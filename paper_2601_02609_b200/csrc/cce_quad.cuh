@@ -150,9 +150,14 @@ __device__ __forceinline__ pairk::PItem sub_item(const QItem& it, int p) {
 template <bool A_MN, bool B_MN>
 __device__ __forceinline__ void q_mma_item(int N, int num_kb, uint64_t* full_bar, uint64_t* empty_bar,
                                            uint32_t a_base, uint32_t b_base, uint32_t tmem_d, uint32_t& stage,
-                                           uint32_t& phase) {
+                                           uint32_t& phase, unsigned long long* wait_ns) {
   const uint32_t idesc = idesc_bf16_f32(PM, N, A_MN ? 1 : 0, B_MN ? 1 : 0);
   for (int kb = 0; kb < num_kb; ++kb) {
+    if (wait_ns) {
+      const unsigned long long w0 = gtimer();
+      mbar_wait(&full_bar[stage], phase);
+      *wait_ns += gtimer() - w0;
+    }
     mbar_wait(&full_bar[stage], phase);
     tc_fence_after();
     const uint64_t ad = sdesc_sw128(a_base + stage * PA_BYTES, A_MN ? 8192 : 16, 1024);
@@ -293,13 +298,22 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
         const int slot_blk0 = (it.c % P.slots) * (g.C / 64);
         const int c0 = it.c * g.C;
         const int m0 = it.m0[pp], n0 = it.n0[pp];
+        unsigned long long tl0 = 0;
         for (int kb = 0; kb < it.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (P.trace && kb == 0) tl0 = gtimer();
           uint8_t* a = sA + stage * PA_BYTES;
           uint8_t* b = sB + stage * PB_BYTES;
           const uint32_t fb = full_leader0 + stage * 8;
           const uint32_t fl = full_local0 + stage * 8;
           if (pr == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
+          // L2 prefetch of the HBM-resident dlogits operand only (the other operand of
+          // DW / DH items is L2-resident and a prefetch would only add L2 requests)
+          const int pk = kb + P.prefetch;
+          if (P.prefetch > 0 && pk < it.num_kb) {
+            if (it.type == PT_DW) tma_prefetch_3d(&tmGMN, 0, pk * BK, slot_blk0 + (m0 + hr) / 64 + pp);
+            else if (it.type == PT_DH) tma_prefetch_3d(&tmGK64, 0, m0 + hr + pp * 64, slot_blk0 + pk);
+          }
           if (it.type == PT_FWD || it.type == PT_G) {
             // A (rows) private to the pair; B (vocabulary rows) shared: this CTA loads the
             // 64-row half `pp` of its 128-row share and multicasts it to its counterpart
@@ -316,6 +330,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
               tma_load_2d_pair(&tmWMN, fb, b + j * 8192, n0 + hn + j * 64, c0 + kb * BK);
           }
           if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
+        }
+        if (P.trace && rank == 0 && it.q < P.trace_cap) {
+          P.trace[it.q].t_load0 = tl0;
+          P.trace[it.q].t_load1 = gtimer();
         }
       }
     }
@@ -340,14 +358,24 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * PN;
         const int N = it.N[pp];
+        const bool tr = P.trace && rank == 0 && it.q < P.trace_cap;
+        unsigned long long fw = 0;
+        const unsigned long long tm0 = tr ? gtimer() : 0ull;
+        const unsigned long long cm0 = tr ? clock64() : 0ull;
         if (it.type == PT_DW)
-          q_mma_item<true, true>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
+          q_mma_item<true, true>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, tr ? &fw : nullptr);
         else if (it.type == PT_DH)
-          q_mma_item<false, true>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
+          q_mma_item<false, true>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, tr ? &fw : nullptr);
         else
-          q_mma_item<false, false>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
+          q_mma_item<false, false>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, tr ? &fw : nullptr);
         if (elect_one()) umma_commit_mask(&tfull_bar[acc], pair_mask);
         __syncwarp();
+        if (tr && lane == 0) {
+          P.trace[it.q].t_mma0 = tm0;
+          P.trace[it.q].t_mma1 = gtimer();
+          P.trace[it.q].t_full_wait = fw;
+          P.trace[it.q].r0 = clock64() - cm0;
+        }
       }
     }
   } else if (warp >= 4) {
@@ -383,6 +411,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
       const pairk::PItem it = sub_item(qit, pp);
       const bool active = qit.active[pp] != 0;
       const uint32_t taddr = tmem_base + acc * PN + ((uint32_t)(e.q * 32) << 16);
+      const unsigned long long t_epi0 = P.trace ? gtimer() : 0ull;
       if (!active) {
         // out-of-range sub-tile (odd tile counts): MMAs ran on zero-filled operands, no output
       } else if (it.type == PT_FWD) {
@@ -403,6 +432,16 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
           if (pr == 0) mbar_arrive(&tempty_bar[acc]);
           else mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);
         }
+      }
+      if (P.trace && leader && rank == 0 && qit.q < P.trace_cap) {
+        TraceRec& r = P.trace[qit.q];
+        r.q_type_c = ((unsigned long long)qit.q << 32) | ((unsigned long long)qit.type << 16) | (unsigned)qit.c;
+        r.smid = smid();
+        r.t_deq = qit.t_deq;
+        r.t_epi0 = t_epi0;
+        r.t_epi1 = gtimer();
+        r.tile = ((unsigned long long)qit.m0[0] << 32) | (unsigned)qit.n0[0];
+        r.pad = qit.num_kb;
       }
       if (P.mode == 1) {
         fence_proxy_async_global();
