@@ -78,9 +78,15 @@ typedef enum {
 /* Kernels: 0 (default) = CTA-pair kernels (tcgen05.mma.cta_group::2, 256-row
  * tiles); CCE_FLAG_ONE_CTA = single-CTA 128x256-tile kernels (kept for A/B). */
 #define CCE_FLAG_ONE_CTA 4u
-/* CTA-pair kernels without cross-pair TMA multicast (default: 4-CTA clusters = two
- * pairs sharing one operand by multicast). */
+/* Kernels (default): persistent CTA-pair kernels (clusters of 2, tcgen05.mma.cta_group::2,
+ * 256 x 256 tiles).  CCE_FLAG_PAIR names the default explicitly.  CCE_FLAG_QUAD = 4-CTA
+ * clusters (two pairs sharing one operand by TMA multicast), plus single pairs running
+ * the same work queue on the SMs 4-CTA clusters cannot use (measured slower on B200:
+ * the multicast couples the two pairs' pipelines; kept for A/B). */
 #define CCE_FLAG_PAIR 8u
+#define CCE_FLAG_QUAD 32u
+/* With CCE_FLAG_QUAD (or alone): quad kernels on the co-resident 4-CTA clusters only. */
+#define CCE_FLAG_QUAD_ONLY 16u
 
 typedef struct {
   int32_t ignore_index;   /* label value that marks a skipped row; -100 in the paper */

@@ -35,6 +35,8 @@ PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 FLAG_BWD_PER_CHUNK = 2
 FLAG_ONE_CTA = 4
 FLAG_PAIR = 8
+FLAG_QUAD_ONLY = 16
+FLAG_QUAD = 32
 
 
 class CCEError(RuntimeError):

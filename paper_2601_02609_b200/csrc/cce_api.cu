@@ -30,6 +30,7 @@ struct cce_handle {
   int device = 0;
   int num_sms = 148;
   int64_t chunk = CCE_CHUNK;  // backward vocabulary chunk (env CCE_CHUNK overrides; multiple of 256)
+  int slots = GBUF_SLOTS;     // dlogits ring slots (env CCE_SLOTS overrides, 2..8)
   // state saved by the forward for the backward (like autograd-saved tensors)
   bool have_fwd = false;
   const void* W = nullptr;
@@ -37,6 +38,9 @@ struct cce_handle {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   int64_t launches = 0;
+  int quad_clusters = -1;           // co-resident 4-CTA clusters (queried once)
+  cudaStream_t side = nullptr;      // forked stream for the NP = 1 co-launch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* trace = nullptr;  // cce_debug_trace: per-item records of the backward
   size_t trace_bytes = 0;
   void* fwd_trace = nullptr;  // ... and of the forward (second half of the buffer)
@@ -114,6 +118,23 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t r
   return r == CUDA_SUCCESS;
 }
 
+// 2-D fp32 tensor map over a row-major matrix [rows][cols] (row stride `ld` elements),
+// box {box_cols, box_rows}, 128-byte swizzle (box_cols * 4 == 128): the dH32 target of
+// the TMA store / reduce-add epilogue.
+static bool make_map_f32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                         uint32_t box_cols, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 3-D bf16 tensor map over the column-blocked dlogits ring [blocks][rows][64]:
 // dims {64, rows, blocks}, box {64, box_rows, 1}, 128-byte swizzle.
 static bool make_map_blocked(CUtensorMap* m, const void* base, uint64_t rows, uint64_t blocks, uint32_t box_rows) {
@@ -178,7 +199,7 @@ struct Layout {
   size_t scal, pos, idx, labels_c, Hc, part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32, sched, total;
 };
 
-Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk) {
+Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots) {
   Layout L;
   L.Npad = align_up((size_t)(N > 0 ? N : 1), 256);  // pair tiles are 256 rows
   L.Tv = (V_local + BN - 1) / BN;
@@ -204,7 +225,7 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk) {
   L.stats_all = take((size_t)world * L.Npad * 16);
   L.lse_c = take((size_t)L.Npad * 4);
   L.loss_rows = take((size_t)L.Npad * 4);
-  L.gbuf = take((size_t)GBUF_SLOTS * L.Npad * L.C * 2);  // ring of N x chunk dlogits (never N x V)
+  L.gbuf = take((size_t)slots * L.Npad * L.C * 2);  // ring of N x chunk dlogits (never N x V)
   L.dH32 = take((size_t)L.Npad * D * 4);
   L.n_chunks = (V_local + L.C - 1) / L.C;
   // backward work queue: head | g_done[n] | w_done[n] | dh_flag[tiles_d * ceil(Npad/BN)]
@@ -245,7 +266,7 @@ cce_status launch_gemm(cce_handle* h, const CUtensorMap& a, const CUtensorMap& b
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
 cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
-                       const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5,
+                       const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5, const CUtensorMap& m6,
                        const pairk::PairParams& pp, cudaStream_t s, int prof_class) {
   static bool attr = false;
   if (!attr) {
@@ -257,24 +278,95 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
   const int grid = (h->num_sms / 2) * 2;  // whole CTA pairs
   {
     ProfScope ps(h, s, prof_class);
-    pairk::cce_pair_kernel<<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, pp);
+    pairk::cce_pair_kernel<<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
+template <int NP>
+cudaError_t launch_quad_np(int grid, cudaStream_t s, const CUtensorMap& m0, const CUtensorMap& m1,
+                           const CUtensorMap& m2, const CUtensorMap& m3, const CUtensorMap& m4,
+                           const CUtensorMap& m5, const CUtensorMap& m6, const pairk::PairParams& pp) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(quadk::QTHREADS, 1, 1);
+  cfg.dynamicSmemBytes = quadk::QSMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * NP;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, quadk::cce_quad_kernel<NP>, m0, m1, m2, m3, m4, m5, m6, pp);
+}
+
+// How many 4-CTA clusters of the quad kernel can be co-resident (GPC packing leaves
+// SMs stranded), computed once per device.
+int quad_clusters(cce_handle* h) {
+  if (h->quad_clusters >= 0) return h->quad_clusters;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->num_sms / 4 * 4, 1, 1);
+  cfg.blockDim = dim3(quadk::QTHREADS, 1, 1);
+  cfg.dynamicSmemBytes = quadk::QSMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, quadk::cce_quad_kernel<2>, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = h->num_sms / 4;
+  }
+  if (n > h->num_sms / 4) n = h->num_sms / 4;
+  if (const char* e = getenv("CCE_QUAD_CLUSTERS")) {  // debug / A-B: cap the 4-CTA clusters
+    const int c = atoi(e);
+    if (c >= 0 && c < n) n = c;
+  }
+  h->quad_clusters = n;
+  return n;
+}
+
+// The quad kernel on every co-resident 4-CTA cluster plus, on a forked stream, the
+// NP = 1 variant on the SMs the 4-CTA clusters strand; both drain the same queue.
 cce_status launch_quad(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
-                       const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5,
+                       const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5, const CUtensorMap& m6,
                        const pairk::PairParams& pp, cudaStream_t s, int prof_class) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(quadk::cce_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, quadk::QSMEM) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(quadk::cce_quad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, quadk::QSMEM) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(quadk::cce_quad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, quadk::QSMEM) !=
+            cudaSuccess)
       return CCE_ERR_CUDA;
     attr = true;
   }
-  const int grid = (h->num_sms / 4) * 4;  // whole 4-CTA clusters
-  {
-    ProfScope ps(h, s, prof_class);
-    quadk::cce_quad_kernel<<<grid, quadk::QTHREADS, quadk::QSMEM, s>>>(m0, m1, m2, m3, m4, m5, pp);
+  const int nq = quad_clusters(h);
+  const int rest_pairs = (h->cfg.flags & CCE_FLAG_QUAD_ONLY) && nq > 0 ? 0 : (h->num_sms - 4 * nq) / 2;
+  ProfScope ps(h, s, prof_class);
+  if (nq == 0) {
+    if (launch_quad_np<1>(2 * rest_pairs, s, m0, m1, m2, m3, m4, m5, m6, pp) != cudaSuccess) return CCE_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+  }
+  if (rest_pairs > 0) {
+    if (!h->side) {
+      if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return CCE_ERR_CUDA;
+    }
+    if (cudaEventRecord(h->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(h->side, h->ev_fork, 0) != cudaSuccess)
+      return CCE_ERR_CUDA;
+  }
+  if (launch_quad_np<2>(4 * nq, s, m0, m1, m2, m3, m4, m5, m6, pp) != cudaSuccess) return CCE_ERR_CUDA;
+  if (rest_pairs > 0) {
+    h->launches++;
+    if (launch_quad_np<1>(2 * rest_pairs, h->side, m0, m1, m2, m3, m4, m5, m6, pp) != cudaSuccess) return CCE_ERR_CUDA;
+    if (cudaEventRecord(h->ev_join, h->side) != cudaSuccess || cudaStreamWaitEvent(s, h->ev_join, 0) != cudaSuccess)
+      return CCE_ERR_CUDA;
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
@@ -335,6 +427,10 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
     const long long c = atoll(e);
     if (c >= 256 && c % 256 == 0) h->chunk = c;
   }
+  if (const char* e = getenv("CCE_SLOTS")) {
+    const int v = atoi(e);
+    if (v >= 2 && v <= 8) h->slots = v;
+  }
   *out = h;
   return CCE_OK;
 }
@@ -346,13 +442,16 @@ cce_status cce_destroy(cce_handle* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : h->pool) cudaEventDestroy(e);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
   return CCE_OK;
 }
 
 size_t cce_workspace_bytes(const cce_handle* h, int64_t N, int64_t D, int64_t V_local) {
   if (!h || N < 0 || D <= 0 || V_local < 0) return 0;
-  return layout(N, D, V_local, h->cfg.world, h->chunk).total;
+  return layout(N, D, V_local, h->cfg.world, h->chunk, h->slots).total;
 }
 
 int64_t cce_kernel_launches(const cce_handle* h) { return h ? h->launches : 0; }
@@ -410,7 +509,7 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
   if (D % 64 != 0 || N > (1LL << 30) || V_local > (1LL << 30)) return CCE_ERR_UNSUPPORTED;
   if ((N > 0 && !aligned16(H)) || (V_local > 0 && !aligned16(W)) || (ldh * 2) % 16 || (ldw * 2) % 16)
     return CCE_ERR_UNSUPPORTED;
-  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots);
   if (!workspace || workspace_bytes < L.total || !aligned16(workspace)) return CCE_ERR_WORKSPACE;
   if (!get_encode()) return CCE_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -453,7 +552,7 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
       cce_status st = launch_gemm<MODE_FWD>(h, tA, tB, p, s);
       if (st != CCE_OK) return st;
     } else {
-      const bool quad = !(h->cfg.flags & CCE_FLAG_PAIR);
+      const bool quad = (h->cfg.flags & (CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY)) != 0;
       CUtensorMap tA, tB;
       if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM)) return CCE_ERR_CUDA;
       if (!make_map(&tB, W, D, V_local, ldw, quad ? 64 : pairk::PN / 2)) return CCE_ERR_CUDA;
@@ -462,15 +561,15 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
       pp.g = p;
       pp.mode = 0;
       pp.n_chunks = 0;
-      pp.slots = GBUF_SLOTS;
+      pp.slots = h->slots;
       pp.prefetch = 0;
       if (const char* e = getenv("CCE_PREFETCH_FWD")) pp.prefetch = atoi(e);
       if (const char* e = getenv("CCE_DEBUG_STRICT")) pp.strict = atoi(e);
       pp.sched = at<int>(ws, L.sched);
       pp.trace = static_cast<TraceRec*>(h->fwd_trace);
       pp.trace_cap = (int)(h->fwd_trace_bytes / sizeof(TraceRec));
-      cce_status st = quad ? launch_quad(h, tA, tB, tA, tA, tA, tA, pp, s, 0)
-                           : launch_pair(h, tA, tB, tA, tA, tA, tA, pp, s, 0);
+      cce_status st = quad ? launch_quad(h, tA, tB, tA, tA, tA, tA, tA, pp, s, 0)
+                           : launch_pair(h, tA, tB, tA, tA, tA, tA, tA, pp, s, 0);
       if (st != CCE_OK) return st;
     }
   }
@@ -521,7 +620,7 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
   if ((dH && !aligned16(dH)) || (dW && !aligned16(dW))) return CCE_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t N = h->N, D = h->D, V_local = h->V_local;
-  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots);
   void* ws = h->ws;
   int* nvp = at<int>(ws, L.scal);
   float* dH32 = at<float>(ws, L.dH32);
@@ -542,19 +641,19 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     p.gbuf = at<__nv_bfloat16>(ws, L.gbuf);
     p.dW = static_cast<__nv_bfloat16*>(dW);
     p.dH32 = dH32;
-    int slots = GBUF_SLOTS, strict = 0;
-    if (const char* e = getenv("CCE_DEBUG_SLOTS")) slots = atoi(e) >= 2 && atoi(e) <= GBUF_SLOTS ? atoi(e) : GBUF_SLOTS;
+    int slots = h->slots, strict = 0;
+    if (const char* e = getenv("CCE_DEBUG_SLOTS")) slots = atoi(e) >= 2 && atoi(e) <= h->slots ? atoi(e) : h->slots;
     if (const char* e = getenv("CCE_DEBUG_STRICT")) strict = atoi(e);
     if (!(h->cfg.flags & CCE_FLAG_ONE_CTA)) {
       // CTA-pair (or quad: two pairs sharing an operand by TMA multicast) persistent
       // backward: G / DW / DH tiles of every chunk from one work queue
-      const bool quad = !(h->cfg.flags & CCE_FLAG_PAIR);
+      const bool quad = (h->cfg.flags & (CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY)) != 0;
       CUtensorMap mHcK, mWK, mGMN, mHcMN, mGK, mWMN;
       if (!make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM) ||
           !make_map(&mWK, h->W, D, V_local, h->ldw, quad ? 64 : pairk::PN / 2) ||
-          !make_map_blocked(&mGMN, G, L.Npad, GBUF_SLOTS * (L.C / 64), 64) ||
+          !make_map_blocked(&mGMN, G, L.Npad, h->slots * (L.C / 64), 64) ||
           !make_map(&mHcMN, Hc, D, L.Npad, D, 64) ||
-          !make_map_blocked(&mGK, G, L.Npad, GBUF_SLOTS * (L.C / 64), quad ? 64 : pairk::HM) ||
+          !make_map_blocked(&mGK, G, L.Npad, h->slots * (L.C / 64), quad ? 64 : pairk::HM) ||
           !make_map(&mWMN, h->W, D, V_local, h->ldw, 64))
         return CCE_ERR_CUDA;
       if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
@@ -564,19 +663,31 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
       pp.n_chunks = (int)L.n_chunks;
       pp.slots = slots;
       pp.strict = strict;
+      // queue order (pair kernel): blocks of `qblock` chunks; G of block b + lookahead is
+      // queued before W of block b; deadlock-free iff (lookahead + 1) * qblock <= slots
+      pp.qblock = 1;
+      pp.lookahead = 1;
+      if (const char* e = getenv("CCE_QBLOCK")) pp.qblock = atoi(e);
+      if (const char* e = getenv("CCE_LOOKAHEAD")) pp.lookahead = atoi(e);
+      if (pp.qblock < 1) pp.qblock = 1;
+      if (pp.qblock > slots) pp.qblock = slots;
+      if (pp.lookahead < 0) pp.lookahead = 0;
+      while (pp.lookahead > 0 && (pp.lookahead + 1) * pp.qblock > slots) --pp.lookahead;
       pp.prefetch = 0;  // L2 prefetch measured harmful (adds L2 requests); env CCE_PREFETCH to experiment
       if (const char* e = getenv("CCE_PREFETCH")) pp.prefetch = atoi(e);
       pp.sched = at<int>(ws, L.sched);
       pp.trace = static_cast<TraceRec*>(h->trace);
       pp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
-      cce_status st = quad ? launch_quad(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, pp, s, 1)
-                           : launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, pp, s, 1);
+      CUtensorMap mDH;
+      if (!make_map_f32(&mDH, dH32, D, L.Npad, D, 32, 32)) return CCE_ERR_CUDA;
+      cce_status st = quad ? launch_quad(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1)
+                           : launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1);
       if (st != CCE_OK) return st;
     } else {
     CUtensorMap mHcK, mWK, mHcMN, mGMN, mWMN, mGK;
     if (!make_map(&mHcK, Hc, D, L.Npad, D, BM) || !make_map(&mWK, h->W, D, V_local, h->ldw, BN) ||
-        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, GBUF_SLOTS * L.Npad, L.C, 64) ||
-        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, GBUF_SLOTS * L.Npad, L.C, BN))
+        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, h->slots * L.Npad, L.C, 64) ||
+        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, h->slots * L.Npad, L.C, BN))
       return CCE_ERR_CUDA;
     if (h->cfg.flags & CCE_FLAG_BWD_PER_CHUNK) {
       // reference schedule: three launches per vocabulary chunk
@@ -643,7 +754,7 @@ cce_status cce_get_error(cce_handle* h, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!h->ws) return CCE_OK;
-  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots);
   int* errp = at<int>(h->ws, L.scal) + 1;
   int err = 0;
   if (cudaMemcpyAsync(&err, errp, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CCE_ERR_CUDA;

@@ -68,6 +68,8 @@ struct PairParams {
   int mode;        // 0 = forward queue, 1 = backward queue
   int n_chunks;
   int slots;       // Gbuf ring slots
+  int lookahead;   // backward queue: G of chunk block b + lookahead is queued before W of block b
+  int qblock;      // chunks per block of the backward queue ((lookahead + 1) * qblock <= slots)
   int prefetch;    // k-blocks of L2 prefetch (TMA prefetch.tensor) beyond the SMEM ring
   int strict;      // debug bit 0: serialise every item behind all earlier ones;
                    // debug bit 1: skip operand loads (measures raw MMA throughput; garbage results)
@@ -107,14 +109,22 @@ __device__ PItem decode(const PairParams& P, const PCounts& k, int q) {
     if (q < k.t256 * k.tv) return make_item(PT_FWD, 0, (q % k.t256) * PM, (q / k.t256) * PN, PN, g.D / BK, 0, q);
     return make_item(PT_END, 0, 0, 0, 0, 0, 0, q);
   }
+  // chunk blocks of B = P.qblock chunks: G(blocks 0 .. L-1), then for each block b:
+  // G(block b + L), W(block b)   (L = P.lookahead; (L + 1) B <= slots)
   const int n = P.n_chunks;
+  const int L = P.lookahead, B = P.qblock;
+  const int nb = (n + B - 1) / B;
   int r = q;
-  for (int ph = 0; ph < 2 * n; ++ph) {
+  for (int ph = 0; ph < (L + 2 * nb) * B; ++ph) {
+    const int blk_ph = ph / B, j = ph % B;
     int isG, c;
-    if (ph == 0) { isG = 1; c = 0; }
-    else if (ph == 2 * n - 1) { isG = 0; c = n - 1; }
-    else if (ph & 1) { isG = 1; c = (ph + 1) / 2; }
-    else { isG = 0; c = ph / 2 - 1; }
+    if (blk_ph < L) { isG = 1; c = blk_ph * B + j; }
+    else {
+      const int t = blk_ph - L;
+      isG = (t & 1) == 0;
+      c = ((t >> 1) + (isG ? L : 0)) * B + j;
+    }
+    if (c >= n) continue;
     const int w = p_chunk_width(g, c);
     const int c0 = c * g.C;
     if (isG) {
@@ -282,8 +292,8 @@ __device__ __forceinline__ void epi_dw(const GemmParams& p, uint32_t taddr, cons
       uint4* dst = reinterpret_cast<uint4*>(p.dW + (size_t)(c0 + vrow) * p.D + d0);
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4)
-        dst[q4] = make_uint4(pack_bf16(v[8 * q4], v[8 * q4 + 1]), pack_bf16(v[8 * q4 + 2], v[8 * q4 + 3]),
-                             pack_bf16(v[8 * q4 + 4], v[8 * q4 + 5]), pack_bf16(v[8 * q4 + 6], v[8 * q4 + 7]));
+        __stcs(dst + q4, make_uint4(pack_bf16(v[8 * q4], v[8 * q4 + 1]), pack_bf16(v[8 * q4 + 2], v[8 * q4 + 3]),
+                             pack_bf16(v[8 * q4 + 4], v[8 * q4 + 5]), pack_bf16(v[8 * q4 + 6], v[8 * q4 + 7])));
     }
   }
 }
@@ -315,6 +325,45 @@ __device__ __forceinline__ void epi_dh(const GemmParams& p, uint32_t taddr, cons
   }
 }
 
+// dH epilogue through the TMA: each warp moves its 32 rows x 32 columns of the fp32
+// accumulator into its 4 KB staging tile (128-byte swizzle: conflict-free) and issues one
+// bulk tensor store (first chunk) or bulk reduce-add (later chunks) into dH32; the L2
+// performs the adds, so the epilogue never waits on a load.  The caller orders chunk c's
+// reduce after chunk c-1's (dh_flag), so every element is summed in chunk order: the
+// result is bit-identical to a load-add-store in that order.
+__device__ __forceinline__ void epi_dh_tma(const CUtensorMap* tmDH, uint32_t taddr, const PEpi& e,
+                                           const PItem& it) {
+  const int row0 = it.m0 + e.rank * HM + e.q * 32;
+  const int hw = it.N / 2;
+  const int cb = e.half * hw;
+  const int lane = e.rit & 31;
+  uint4* stg = reinterpret_cast<uint4*>(e.stage);  // [32 rows][8 x 16 B]
+  const bool add = it.c > 0;
+#pragma unroll 1
+  for (int j = 0; j < hw / 32; ++j) {
+    float v[32];
+    tmem_ld32(taddr + cb + j * 32, v);
+    if (j > 0) {
+      if (lane == 0) bulk_wait_read<0>();  // previous box has left the staging tile
+      __syncwarp();
+    }
+#pragma unroll
+    for (int q4 = 0; q4 < 8; ++q4)
+      stg[lane * 8 + (q4 ^ (lane & 7))] = make_uint4(__float_as_uint(v[4 * q4]), __float_as_uint(v[4 * q4 + 1]),
+                                                     __float_as_uint(v[4 * q4 + 2]), __float_as_uint(v[4 * q4 + 3]));
+    fence_proxy_async_shared();
+    __syncwarp();
+    if (lane == 0) {
+      const int d0 = it.n0 + cb + j * 32;
+      if (add) tma_reduce_add_2d(tmDH, stg, d0, row0);
+      else tma_store_2d(tmDH, stg, d0, row0);
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
+}
+
 // ------------------------------------------------------------------ MMA issue (leader warp)
 // All 32 lanes wait on the full barrier; one elected lane issues the 4 K=16 pair MMAs
 // of a 64-wide k-block and commits the stage back to both CTAs' empty barriers.  The
@@ -323,13 +372,15 @@ __device__ __forceinline__ void epi_dh(const GemmParams& p, uint32_t taddr, cons
 template <bool A_MN, bool B_MN>
 __device__ __forceinline__ void mma_item(const PItem& it, uint64_t* full_bar, uint64_t* empty_bar, uint32_t a_base,
                                          uint32_t b_base, uint32_t tmem_d, uint32_t& stage, uint32_t& phase,
-                                         unsigned long long* wait_ns) {
+                                         unsigned long long* wait_ns, volatile unsigned long long* t_issue,
+                                         unsigned long long* lat_sum) {
   const uint32_t idesc = idesc_bf16_f32(PM, it.N, A_MN ? 1 : 0, B_MN ? 1 : 0);
   for (int kb = 0; kb < it.num_kb; ++kb) {
     if (wait_ns) {
       const unsigned long long w0 = gtimer();
       mbar_wait(&full_bar[stage], phase);
       *wait_ns += gtimer() - w0;
+      *lat_sum += clock64() - t_issue[stage];  // issue -> data landed (upper bound when not waiting)
     }
     mbar_wait(&full_bar[stage], phase);
     tc_fence_after();
@@ -352,7 +403,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     cce_pair_kernel(const __grid_constant__ CUtensorMap tmHcK, const __grid_constant__ CUtensorMap tmWK,
                     const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
                     const __grid_constant__ CUtensorMap tmGK, const __grid_constant__ CUtensorMap tmWMN,
-                    const PairParams P) {
+                    const __grid_constant__ CUtensorMap tmDH, const PairParams P) {
   const GemmParams& g = P.g;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -367,6 +418,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   uint64_t* rempty_p = rempty_l + PRING;    // leader: peer consumers (producer + epilogue warps)
   PItem* ring = reinterpret_cast<PItem*>(rempty_p + PRING);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + PRING);
+  // trace only: clock64 at which the leader's producer issued each stage's loads
+  volatile unsigned long long* t_issue =
+      reinterpret_cast<volatile unsigned long long*>(smem + PSTAGES * PSTAGE_BYTES + 512);
   float* xchg = reinterpret_cast<float*>(smem + PSTAGES * PSTAGE_BYTES + 1024);
   uint8_t* stage_base = smem + PSTAGES * PSTAGE_BYTES + 2048;
 
@@ -383,6 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     tma_prefetch_desc(&tmHcK); tma_prefetch_desc(&tmWK);
     if (P.mode == 1) {
       tma_prefetch_desc(&tmGMN); tma_prefetch_desc(&tmHcMN); tma_prefetch_desc(&tmGK); tma_prefetch_desc(&tmWMN);
+      tma_prefetch_desc(&tmDH);
     }
     for (int s = 0; s < PSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 2 * PEPI_WARPS); }
@@ -415,6 +470,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       while (true) {
         const int q = atomicAdd(head, 1);
         PItem it = decode(P, k, q);
+        // debug bits 256 / 512 / 1024: run only the G / DW / DH items (no dependencies;
+        // measures one item type's throughput in isolation, results are garbage)
+        if ((P.strict & 1792) && it.type != PT_END && !((P.strict >> (8 + it.type - PT_G)) & 1)) continue;
         if (P.trace) it.t_deq = gtimer();
         mbar_wait(&rempty_l[rs], rph ^ 1);
         mbar_wait(&rempty_p[rs], rph ^ 1);
@@ -434,6 +492,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       // ===== TMA producer (both CTAs): next item from the local ring, dependencies, loads
       uint32_t stage = 0, phase = 0, rs = 0, rph = 0;
       const uint32_t full_leader0 = mapa_shared(smem_u32(&full_bar[0]), 0);
+      const bool hints = P.mode == 1 && !(P.strict & 2048);
+      const uint64_t pol_keep = hints ? policy_evict_last() : policy_evict_normal();
+      const uint64_t pol_g = (P.strict & 4096) ? policy_evict_first() : policy_evict_normal();
       while (true) {
         if (rank == 0) mbar_wait(&rfull_bar[rs], rph);
         else mbar_wait_cluster(&rfull_bar[rs], rph);
@@ -442,7 +503,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         else mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&rempty_p[rs]), 0));
         if (++rs == PRING) { rs = 0; rph ^= 1; }
         if (it.type == PT_END) break;
-        if (P.mode == 1) {
+        if (P.mode == 1 && !(P.strict & 1792)) {
           // dependencies: only on items earlier in the queue (deadlock-free)
           if (P.strict & 1) wait_ge(done_total, 2 * it.q);
           if (it.type == PT_G) {
@@ -452,7 +513,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
             }
           } else {
             wait_ge(&g_done[it.c], 2 * p_n_g(k, p_chunk_width(g, it.c)));
-            if (it.type == PT_DH) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
+            // DH(c, tile) after DH(c-1, tile) is enforced where the epilogue issues its
+            // reduce-add; debug bit 8 also holds the operand loads back
+            if (it.type == PT_DH && (P.strict & 8)) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
           }
           fence_proxy_async_global();
         }
@@ -473,6 +536,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           // the leader arms its full barrier with BOTH CTAs' bytes; the peer's TMA only
           // signals completion bytes there (no per-stage remote arrive / release fence)
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
+          if (P.trace && rank == 0) t_issue[stage] = clock64();
           // L2 prefetch `prefetch` k-blocks ahead of this load (hides HBM latency beyond
           // the 6-stage SMEM ring; no SMEM or barrier involved)
           const int pk = kb + P.prefetch;
@@ -489,19 +553,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
               for (int j = 0; j < it.N / 2 / 64; ++j) tma_prefetch_2d(&tmWMN, it.n0 + hn + j * 64, c0 + pk * BK);
             }
           }
+          // L2 policies (backward): the reused operands (Hc, the W chunk) evict_last, the
+          // dlogits ring per pol_g (debug bits 2048 / 4096 switch the hints off / G to evict_first)
           if (it.type == PT_FWD || it.type == PT_G) {
-            tma_load_2d_pair(&tmHcK, fb, a, kb * BK, it.m0 + hr);
-            tma_load_2d_pair(&tmWK, fb, b, kb * BK, it.n0 + hn);
+            tma_load_2d_pair_hint(&tmHcK, fb, a, kb * BK, it.m0 + hr, pol_keep);
+            tma_load_2d_pair_hint(&tmWK, fb, b, kb * BK, it.n0 + hn, pol_keep);
           } else if (it.type == PT_DW) {
 #pragma unroll
             for (int j = 0; j < HM / 64; ++j)
-              tma_load_3d_pair(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j);
+              tma_load_3d_pair_hint(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j, pol_g);
             for (int j = 0; j < it.N / 2 / 64; ++j)
-              tma_load_2d_pair(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK);
+              tma_load_2d_pair_hint(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK, pol_keep);
           } else {  // PT_DH
-            tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb);
+            tma_load_3d_pair_hint(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb, pol_g);
             for (int j = 0; j < it.N / 2 / 64; ++j)
-              tma_load_2d_pair(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK);
+              tma_load_2d_pair_hint(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK, pol_keep);
           }
           if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
         }
@@ -533,14 +599,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         const uint32_t tmem_d = tmem_base + acc * PN;
         const unsigned long long tm0 = P.trace ? gtimer() : 0ull;
         const unsigned long long cm0 = P.trace ? clock64() : 0ull;
-        unsigned long long fw = 0;
+        unsigned long long fw = 0, lat = 0;
         unsigned long long* fwp = P.trace ? &fw : nullptr;
         if (it.type == PT_DW)
-          mma_item<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+          mma_item<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp, t_issue, &lat);
         else if (it.type == PT_DH)
-          mma_item<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+          mma_item<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp, t_issue, &lat);
         else
-          mma_item<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+          mma_item<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp, t_issue, &lat);
         if (elect_one()) umma_commit_pair(&tfull_bar[acc]);
         __syncwarp();
         if (P.trace && lane == 0 && it.q < P.trace_cap) {
@@ -548,6 +614,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           P.trace[it.q].t_mma1 = gtimer();
           P.trace[it.q].t_full_wait = fw;
           P.trace[it.q].r0 = clock64() - cm0;
+          P.trace[it.q].r2 = lat;
         }
       }
     }
@@ -602,9 +669,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         epi_dw(g, taddr, e, it, have_acc);
       } else {
         // DH(c-1, tile) halves published; re-acquire so the .cg loads below see them
-        if (leader) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
+        if (leader && !(P.strict & 1792)) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
         named_bar_sync(2, PEPI_THREADS);
-        if (!(P.strict & 64)) epi_dh(g, taddr, e, it, k.nv);
+        fence_proxy_async_global();  // the acquired flag orders the TMA reduce below
+        if (!(P.strict & 64)) epi_dh_tma(&tmDH, taddr, e, it);
       }
       if (have_acc) {
         tc_fence_before();

@@ -147,7 +147,7 @@ __device__ __forceinline__ pairk::PItem sub_item(const QItem& it, int p) {
   return s;
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int NP>
 __device__ __forceinline__ void q_mma_item(int N, int num_kb, uint64_t* full_bar, uint64_t* empty_bar,
                                            uint32_t a_base, uint32_t b_base, uint32_t tmem_d, uint32_t& stage,
                                            uint32_t& phase, unsigned long long* wait_ns) {
@@ -167,18 +167,30 @@ __device__ __forceinline__ void q_mma_item(int N, int num_kb, uint64_t* full_bar
       for (int kk = 0; kk < BK / 16; ++kk)
         umma_bf16_pair(tmem_d, ad + (uint64_t)(A_MN ? 128 * kk : 2 * kk), bd + (uint64_t)(B_MN ? 128 * kk : 2 * kk),
                        idesc, (kb | kk) ? 1u : 0u);
-      umma_commit_mask(&empty_bar[stage], 0xF);  // both pairs must release a stage (multicast slots)
+      // every pair of the cluster must release a stage (multicast slots)
+      umma_commit_mask(&empty_bar[stage], NP == 2 ? 0xF : 0x3);
     }
     __syncwarp();
     if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
   }
 }
 
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
+// NP = pairs per cluster.  NP = 2: the quad kernel proper (4-CTA clusters, shared
+// operand multicast).  NP = 1: the same queue consumed by ONE CTA pair, which runs the
+// item's two sub-tiles one after the other and loads the common operand itself.  A
+// 4-CTA cluster cannot use every SM (GPCs hold 16-22 SMs: 33 clusters = 132 of 148
+// SMs on B200), so the host co-launches NP = 1 clusters on the stranded SMs; both
+// kernels pull from the one work queue and count 4 completions per item (NP = 2:
+// 4 CTAs x 1; NP = 1: 2 CTAs x 2 sub-tiles), so the dependency protocol is unchanged.
+template <int NP>
+__global__ void __launch_bounds__(QTHREADS, 1)
     cce_quad_kernel(const __grid_constant__ CUtensorMap tmHcK, const __grid_constant__ CUtensorMap tmWK64,
                     const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
                     const __grid_constant__ CUtensorMap tmGK64, const __grid_constant__ CUtensorMap tmWMN,
-                    const pairk::PairParams P) {
+                    const __grid_constant__ CUtensorMap tmDH, const pairk::PairParams P) {
+  static_assert(NP == 1 || NP == 2, "pairs per cluster");
+  constexpr int NCTA = 2 * NP;
+  constexpr int NSUB = NP == 2 ? 1 : 2;  // sub-tiles each pair runs per item
   const GemmParams& g = P.g;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -189,7 +201,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
   uint64_t* tfull_bar = empty_bar + PSTAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* rfull_bar = tempty_bar + 2;
-  uint64_t* rempty_bar = rfull_bar + PRING;  // rank 0 only: all consumers of all four CTAs
+  uint64_t* rempty_bar = rfull_bar + PRING;  // rank 0 only: all consumers of all CTAs
   QItem* ring = reinterpret_cast<QItem*>(rempty_bar + PRING);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + PRING);
   float* xchg = reinterpret_cast<float*>(smem + PSTAGES * PSTAGE_BYTES + 1024);
@@ -199,7 +211,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const int pr = rank & 1;          // rank within the pair
-  const int pp = rank >> 1;         // which pair (sub-tile) this CTA works on
+  const int pp = rank >> 1;         // which pair (sub-tile) this CTA works on (NP = 2)
   const uint32_t pair_leader = rank & ~1u;
   int* head = P.sched;
   int* done_total = P.sched + 1;
@@ -211,13 +223,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
     tma_prefetch_desc(&tmHcK); tma_prefetch_desc(&tmWK64);
     if (P.mode == 1) {
       tma_prefetch_desc(&tmGMN); tma_prefetch_desc(&tmHcMN); tma_prefetch_desc(&tmGK64); tma_prefetch_desc(&tmWMN);
+      tma_prefetch_desc(&tmDH);
     }
-    for (int s = 0; s < PSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 2); }
+    for (int s = 0; s < PSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], NP); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 2 * PEPI_WARPS); }
     for (int r = 0; r < PRING; ++r) {
       mbar_init(&rfull_bar[r], 1);
-      // consumers per item: 4 producers + 2 MMA warps + 4 x 8 epilogue warps
-      mbar_init(&rempty_bar[r], 4 + 2 + 4 * PEPI_WARPS);
+      // consumers per item: NCTA producers + NP MMA warps + NCTA x 8 epilogue warps
+      mbar_init(&rempty_bar[r], NCTA + NP + NCTA * PEPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -240,40 +253,43 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
 
   if (warp == 3) {
     if (lane == 0 && rank == 0) {
-      // ===== scheduler: dequeue quad items, publish them into all four rings =====
+      // ===== scheduler: dequeue quad items, publish them into every CTA's ring =====
       uint32_t rs = 0, rph = 0;
       while (true) {
         const int q = atomicAdd(head, 1);
         QItem it = q_decode(P, k, q);
+        // debug bits 256 / 512 / 1024: run only the G / DW / DH items (no dependencies;
+        // measures one item type's throughput in isolation, results are garbage)
+        if ((P.strict & 1792) && it.type != PT_END && !((P.strict >> (8 + it.type - PT_G)) & 1)) continue;
         if (P.trace) it.t_deq = gtimer();
         mbar_wait(&rempty_bar[rs], rph ^ 1);
         ring[rs] = it;
         const uint32_t* w = reinterpret_cast<const uint32_t*>(&it);
-        for (int dst = 1; dst < 4; ++dst) {
+        for (int dst = 1; dst < NCTA; ++dst) {
           const uint32_t remote = mapa_shared(smem_u32(&ring[rs]), dst);
 #pragma unroll
           for (int i = 0; i < (int)(sizeof(QItem) / 4); ++i) st_cluster_u32(remote + 4 * i, w[i]);
         }
         mbar_arrive(&rfull_bar[rs]);
-        for (int dst = 1; dst < 4; ++dst) mbar_arrive_cluster(mapa_shared(smem_u32(&rfull_bar[rs]), dst));
+        for (int dst = 1; dst < NCTA; ++dst) mbar_arrive_cluster(mapa_shared(smem_u32(&rfull_bar[rs]), dst));
         if (++rs == PRING) { rs = 0; rph ^= 1; }
         if (it.type == PT_END) break;
       }
     }
   } else if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer (all four CTAs) =====
+      // ===== TMA producer (every CTA) =====
       uint32_t stage = 0, phase = 0, rs = 0, rph = 0;
       const uint32_t full_leader0 = mapa_shared(smem_u32(&full_bar[0]), pair_leader);
       const uint32_t full_local0 = smem_u32(&full_bar[0]);
-      const uint16_t mc = (uint16_t)((1u << rank) | (1u << (rank ^ 2u)));  // me + my counterpart
+      const uint16_t mc = (uint16_t)((1u << rank) | (1u << (rank ^ 2u)));  // me + my counterpart (NP = 2)
       while (true) {
         mbar_wait_cluster(&rfull_bar[rs], rph);
         const QItem it = ring[rs];
         mbar_arrive_cluster_relaxed(rempty0 + rs * 8);
         if (++rs == PRING) { rs = 0; rph ^= 1; }
         if (it.type == PT_END) break;
-        if (P.mode == 1) {
+        if (P.mode == 1 && !(P.strict & 1792)) {
           if (P.strict & 1) wait_ge(done_total, 4 * it.q);
           if (it.type == PT_G) {
             if (it.c >= P.slots) {
@@ -282,7 +298,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
             }
           } else {
             wait_ge(&g_done[it.c], 4 * q_n_g(k, pairk::p_chunk_width(g, it.c)));
-            if (it.type == PT_DH) {
+            // DH(c, tile) after DH(c-1, tile) is enforced at the epilogue's reduce only;
+            // debug bit 8 also holds the operand loads back (the old RMW protocol)
+            if (it.type == PT_DH && (P.strict & 8)) {
 #pragma unroll
               for (int p = 0; p < 2; ++p)
                 if (it.active[p]) wait_ge(&dh_flag[it.tile_id[p]], 2 * it.c);
@@ -292,44 +310,66 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
         }
         if (P.trace && rank == 0 && it.q < P.trace_cap) P.trace[it.q].t_ready = gtimer();
         const int hr = pr * HM;                 // this CTA's first tile row of its pair's tile
-        const int N = it.N[pp];
-        const int hn = pr * (N / 2);            // this CTA's first B row / column
-        const int b_bytes = (N / 2) * BK * 2;
         const int slot_blk0 = (it.c % P.slots) * (g.C / 64);
         const int c0 = it.c * g.C;
-        const int m0 = it.m0[pp], n0 = it.n0[pp];
         unsigned long long tl0 = 0;
-        for (int kb = 0; kb < it.num_kb; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (P.trace && kb == 0) tl0 = gtimer();
-          uint8_t* a = sA + stage * PA_BYTES;
-          uint8_t* b = sB + stage * PB_BYTES;
-          const uint32_t fb = full_leader0 + stage * 8;
-          const uint32_t fl = full_local0 + stage * 8;
-          if (pr == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
-          // L2 prefetch of the HBM-resident dlogits operand only (the other operand of
-          // DW / DH items is L2-resident and a prefetch would only add L2 requests)
-          const int pk = kb + P.prefetch;
-          if (P.prefetch > 0 && pk < it.num_kb) {
-            if (it.type == PT_DW) tma_prefetch_3d(&tmGMN, 0, pk * BK, slot_blk0 + (m0 + hr) / 64 + pp);
-            else if (it.type == PT_DH) tma_prefetch_3d(&tmGK64, 0, m0 + hr + pp * 64, slot_blk0 + pk);
+        for (int sp = 0; sp < NSUB; ++sp) {
+          const int p = NP == 2 ? pp : sp;      // the sub-tile this pass loads
+          if (NP == 1 && !it.active[p]) continue;
+          const int N = it.N[p];
+          const int hn = pr * (N / 2);          // this CTA's first B row / column
+          const int b_bytes = (N / 2) * BK * 2;
+          const int m0 = it.m0[p], n0 = it.n0[p];
+          for (int kb = 0; kb < it.num_kb; ++kb) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            if (P.trace && kb == 0 && sp == 0) tl0 = gtimer();
+            uint8_t* a = sA + stage * PA_BYTES;
+            uint8_t* b = sB + stage * PB_BYTES;
+            const uint32_t fb = full_leader0 + stage * 8;
+            const uint32_t fl = full_local0 + stage * 8;
+            if (pr == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
+            // L2 prefetch of the HBM-resident dlogits operand only (the other operand of
+            // DW / DH items is L2-resident and a prefetch would only add L2 requests)
+            const int pk = kb + P.prefetch;
+            if (NP == 2 && P.prefetch > 0 && pk < it.num_kb) {
+              if (it.type == PT_DW) tma_prefetch_3d(&tmGMN, 0, pk * BK, slot_blk0 + (m0 + hr) / 64 + pp);
+              else if (it.type == PT_DH) tma_prefetch_3d(&tmGK64, 0, m0 + hr + pp * 64, slot_blk0 + pk);
+            }
+            if (it.type == PT_FWD || it.type == PT_G) {
+              // A (rows) private to the pair; B (vocabulary rows) common: with NP = 2 this CTA
+              // loads the 64-row half `pp` of its 128-row share and multicasts it to its
+              // counterpart; with NP = 1 it loads both halves
+              tma_load_2d_pair(&tmHcK, fb, a, kb * BK, m0 + hr);
+              if (NP == 2) {
+                tma_load_2d_pair_mc(&tmWK64, fl, b + pp * 8192, kb * BK, n0 + hn + pp * 64, mc);
+              } else {
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) tma_load_2d_pair(&tmWK64, fb, b + h2 * 8192, kb * BK, n0 + hn + h2 * 64);
+              }
+            } else if (it.type == PT_DW) {
+              // A = G^T (vocabulary block) common: 64-column box `pp` (NP = 2) or both
+              if (NP == 2) {
+                tma_load_3d_pair_mc(&tmGMN, fl, a + pp * 8192, 0, kb * BK, slot_blk0 + (m0 + hr) / 64 + pp, mc);
+              } else {
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2)
+                  tma_load_3d_pair(&tmGMN, fb, a + h2 * 8192, 0, kb * BK, slot_blk0 + (m0 + hr) / 64 + h2);
+              }
+              for (int j = 0; j < N / 2 / 64; ++j)
+                tma_load_2d_pair(&tmHcMN, fb, b + j * 8192, n0 + hn + j * 64, kb * BK);
+            } else {  // PT_DH: A = G rows common (64-row half `pp`, or both), B = W chunk columns private
+              if (NP == 2) {
+                tma_load_3d_pair_mc(&tmGK64, fl, a + pp * 8192, 0, m0 + hr + pp * 64, slot_blk0 + kb, mc);
+              } else {
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2)
+                  tma_load_3d_pair(&tmGK64, fb, a + h2 * 8192, 0, m0 + hr + h2 * 64, slot_blk0 + kb);
+              }
+              for (int j = 0; j < N / 2 / 64; ++j)
+                tma_load_2d_pair(&tmWMN, fb, b + j * 8192, n0 + hn + j * 64, c0 + kb * BK);
+            }
+            if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
           }
-          if (it.type == PT_FWD || it.type == PT_G) {
-            // A (rows) private to the pair; B (vocabulary rows) shared: this CTA loads the
-            // 64-row half `pp` of its 128-row share and multicasts it to its counterpart
-            tma_load_2d_pair(&tmHcK, fb, a, kb * BK, m0 + hr);
-            tma_load_2d_pair_mc(&tmWK64, fl, b + pp * 8192, kb * BK, n0 + hn + pp * 64, mc);
-          } else if (it.type == PT_DW) {
-            // A = G^T (vocabulary block) shared: box `pp` of this CTA's two 64-column boxes
-            tma_load_3d_pair_mc(&tmGMN, fl, a + pp * 8192, 0, kb * BK, slot_blk0 + (m0 + hr) / 64 + pp, mc);
-            for (int j = 0; j < N / 2 / 64; ++j)
-              tma_load_2d_pair(&tmHcMN, fb, b + j * 8192, n0 + hn + j * 64, kb * BK);
-          } else {  // PT_DH: A = G rows shared (64-row half `pp`), B = W chunk columns private
-            tma_load_3d_pair_mc(&tmGK64, fl, a + pp * 8192, 0, m0 + hr + pp * 64, slot_blk0 + kb, mc);
-            for (int j = 0; j < N / 2 / 64; ++j)
-              tma_load_2d_pair(&tmWMN, fb, b + j * 8192, n0 + hn + j * 64, c0 + kb * BK);
-          }
-          if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
         }
         if (P.trace && rank == 0 && it.q < P.trace_cap) {
           P.trace[it.q].t_load0 = tl0;
@@ -339,7 +379,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
     }
   } else if (warp == 1) {
     if (pr == 0) {
-      // ===== MMA issuer (both pair leaders; whole warp, elected lane issues) =====
+      // ===== MMA issuer (every pair leader; whole warp, elected lane issues) =====
       uint32_t stage = 0, phase = 0, rs = 0, rph = 0;
       int acc_it = 0;
       const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
@@ -352,24 +392,31 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
         if (++rs == PRING) { rs = 0; rph ^= 1; }
         if (it.type == PT_END) break;
         if (it.num_kb == 0) continue;
-        const uint32_t acc = acc_it & 1, acc_phase = (acc_it >> 1) & 1;
-        ++acc_it;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * PN;
-        const int N = it.N[pp];
         const bool tr = P.trace && rank == 0 && it.q < P.trace_cap;
         unsigned long long fw = 0;
         const unsigned long long tm0 = tr ? gtimer() : 0ull;
         const unsigned long long cm0 = tr ? clock64() : 0ull;
-        if (it.type == PT_DW)
-          q_mma_item<true, true>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, tr ? &fw : nullptr);
-        else if (it.type == PT_DH)
-          q_mma_item<false, true>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, tr ? &fw : nullptr);
-        else
-          q_mma_item<false, false>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, tr ? &fw : nullptr);
-        if (elect_one()) umma_commit_mask(&tfull_bar[acc], pair_mask);
-        __syncwarp();
+        for (int sp = 0; sp < NSUB; ++sp) {
+          const int p = NP == 2 ? pp : sp;
+          if (NP == 1 && !it.active[p]) continue;
+          const uint32_t acc = acc_it & 1, acc_phase = (acc_it >> 1) & 1;
+          ++acc_it;
+          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t tmem_d = tmem_base + acc * PN;
+          const int N = it.N[p];
+          if (it.type == PT_DW)
+            q_mma_item<true, true, NP>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase,
+                                       tr ? &fw : nullptr);
+          else if (it.type == PT_DH)
+            q_mma_item<false, true, NP>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase,
+                                        tr ? &fw : nullptr);
+          else
+            q_mma_item<false, false, NP>(N, it.num_kb, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase,
+                                         tr ? &fw : nullptr);
+          if (elect_one()) umma_commit_mask(&tfull_bar[acc], pair_mask);
+          __syncwarp();
+        }
         if (tr && lane == 0) {
           P.trace[it.q].t_mma0 = tm0;
           P.trace[it.q].t_mma1 = gtimer();
@@ -379,7 +426,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===== epilogue (all four CTAs) =====
+    // ===== epilogue (every CTA) =====
     pairk::PEpi e;
     e.q = warp & 3;
     e.half = (warp - 4) >> 2;
@@ -400,60 +447,69 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(QTHREADS, 1)
       if (++rs == PRING) { rs = 0; rph ^= 1; }
       if (qit.type == PT_END) break;
       const bool have_acc = qit.num_kb > 0;
-      uint32_t acc = 0;
-      if (have_acc) {
-        acc = acc_it & 1;
-        const uint32_t acc_phase = (acc_it >> 1) & 1;
-        ++acc_it;
-        mbar_wait(&tfull_bar[acc], acc_phase);
-        tc_fence_after();
-      }
-      const pairk::PItem it = sub_item(qit, pp);
-      const bool active = qit.active[pp] != 0;
-      const uint32_t taddr = tmem_base + acc * PN + ((uint32_t)(e.q * 32) << 16);
-      const unsigned long long t_epi0 = P.trace ? gtimer() : 0ull;
-      if (!active) {
-        // out-of-range sub-tile (odd tile counts): MMAs ran on zero-filled operands, no output
-      } else if (it.type == PT_FWD) {
-        pairk::epi_fwd(g, taddr, e, it, k.nv);
-      } else if (it.type == PT_G) {
-        pairk::epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
-      } else if (it.type == PT_DW) {
-        pairk::epi_dw(g, taddr, e, it, have_acc);
-      } else {
-        if (leader) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
-        named_bar_sync(2, PEPI_THREADS);
-        pairk::epi_dh(g, taddr, e, it, k.nv);
-      }
-      if (have_acc) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (pr == 0) mbar_arrive(&tempty_bar[acc]);
-          else mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);
+      for (int sp = 0; sp < NSUB; ++sp) {
+        const int p = NP == 2 ? pp : sp;
+        const bool active = qit.active[p] != 0;
+        // NP = 1 skips inactive sub-tiles entirely (no MMAs were issued for them)
+        const bool use_acc = have_acc && (NP == 2 || active);
+        uint32_t acc = 0;
+        if (use_acc) {
+          acc = acc_it & 1;
+          const uint32_t acc_phase = (acc_it >> 1) & 1;
+          ++acc_it;
+          mbar_wait(&tfull_bar[acc], acc_phase);
+          tc_fence_after();
         }
-      }
-      if (P.trace && leader && rank == 0 && qit.q < P.trace_cap) {
-        TraceRec& r = P.trace[qit.q];
-        r.q_type_c = ((unsigned long long)qit.q << 32) | ((unsigned long long)qit.type << 16) | (unsigned)qit.c;
-        r.smid = smid();
-        r.t_deq = qit.t_deq;
-        r.t_epi0 = t_epi0;
-        r.t_epi1 = gtimer();
-        r.tile = ((unsigned long long)qit.m0[0] << 32) | (unsigned)qit.n0[0];
-        r.pad = qit.num_kb;
-      }
-      if (P.mode == 1) {
-        fence_proxy_async_global();
-        named_bar_sync(1, PEPI_THREADS);
-        if (leader) {
-          __threadfence();
-          if (it.type == PT_G) atomicAdd(&g_done[it.c], 1);
-          else {
-            if (it.type == PT_DH && active) atomicAdd(&dh_flag[it.tile_id], 1);
-            atomicAdd(&w_done[it.c], 1);
+        const pairk::PItem it = sub_item(qit, p);
+        const uint32_t taddr = tmem_base + acc * PN + ((uint32_t)(e.q * 32) << 16);
+        const unsigned long long t_epi0 = P.trace ? gtimer() : 0ull;
+        if (!active) {
+          // out-of-range sub-tile (odd tile counts): no output
+        } else if (it.type == PT_FWD) {
+          pairk::epi_fwd(g, taddr, e, it, k.nv);
+        } else if (it.type == PT_G) {
+          pairk::epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
+        } else if (it.type == PT_DW) {
+          pairk::epi_dw(g, taddr, e, it, have_acc);
+        } else {
+          if (leader && !(P.strict & 1792)) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
+          named_bar_sync(2, PEPI_THREADS);
+          fence_proxy_async_global();  // the acquired flag orders the TMA reduce below
+          pairk::epi_dh_tma(&tmDH, taddr, e, it);
+        }
+        if (use_acc) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (pr == 0) mbar_arrive(&tempty_bar[acc]);
+            else mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);
           }
-          atomicAdd(done_total, 1);
+        }
+        if (P.trace && leader && rank == 0 && sp == 0 && qit.q < P.trace_cap) {
+          TraceRec& r = P.trace[qit.q];
+          r.q_type_c = ((unsigned long long)qit.q << 32) | ((unsigned long long)qit.type << 16) | (unsigned)qit.c;
+          r.smid = smid();
+          r.t_deq = qit.t_deq;
+          r.t_epi0 = t_epi0;
+          r.t_epi1 = gtimer();
+          r.tile = ((unsigned long long)qit.m0[0] << 32) | (unsigned)qit.n0[0];
+          // k-blocks this cluster's MMA window covered (NP = 1 runs both sub-tiles)
+          r.pad = NP == 2 ? qit.num_kb : qit.num_kb * ((qit.active[0] != 0) + (qit.active[1] != 0));
+          r.r1 = NP;
+        }
+        if (P.mode == 1) {
+          // publish this CTA's share of the sub-tile (4 completions per item in total)
+          fence_proxy_async_global();
+          named_bar_sync(1, PEPI_THREADS);
+          if (leader) {
+            __threadfence();
+            if (it.type == PT_G) atomicAdd(&g_done[it.c], 1);
+            else {
+              if (it.type == PT_DH && active) atomicAdd(&dh_flag[it.tile_id], 1);
+              atomicAdd(&w_done[it.c], 1);
+            }
+            atomicAdd(done_total, 1);
+          }
         }
       }
     }

@@ -1,0 +1,117 @@
+#!/usr/bin/env python
+"""A/B timing of kernel variants on the bench workload, interleaved in one process
+so that box-to-box and clock drift affect every variant alike.
+
+  python scripts/ab.py name=flags[:ENV=VAL,...] ... [--rounds 3] [--steps 20] [--config qwen05b]
+
+Each variant gets its own handle (env vars are applied while its handle makes its
+first launch, which is when the library reads them).  Prints per-variant median
+step / forward / backward times in ms.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("variants", nargs="+")
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="qwen05b")
+    ap.add_argument("--sample-ms", type=int, default=20)
+    ap.add_argument("--rest", type=float, default=1.0, help="idle seconds before each measurement")
+    args = ap.parse_args()
+
+    import numpy as np
+    import torch
+
+    import paper_2601_02609_b200 as cce
+    import workload
+    from paper_2601_02609_b200 import build as cce_build
+
+    cce_build.build()
+    dev = torch.device("cuda:0")
+    c = workload.CONFIGS[args.config]
+    p = workload.make_config(args.config, seed=42)
+    H = torch.from_numpy(p["H"].view(np.int16)).view(torch.bfloat16).to(dev)
+    W = torch.from_numpy(p["W"].view(np.int16)).view(torch.bfloat16).to(dev)
+    y = torch.from_numpy(p["labels"]).to(dev)
+    loss = torch.empty((), dtype=torch.float32, device=dev)
+    lse = torch.empty(c.N, dtype=torch.float32, device=dev)
+    nvt = torch.empty((), dtype=torch.int32, device=dev)
+    dH = torch.empty((c.N, c.D), dtype=torch.bfloat16, device=dev)
+    dW = torch.empty((c.V, c.D), dtype=torch.bfloat16, device=dev)
+    one = torch.ones((), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    vs = []
+    for spec in args.variants:
+        name, rest = spec.split("=", 1)
+        flags, _, envs = rest.partition(":")
+        env = dict(kv.split("=", 1) for kv in envs.split(",") if kv)
+        vs.append((name, int(flags), env))
+
+    handles = {}
+    for name, flags, env in vs:
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        h = cce.CCEHandle(vocab_total=c.V, flags=flags)
+        ws = h.workspace(c.N, c.D, c.V, dev)
+        cce.cce_forward(h.h, H, W, y, loss, lse, nvt, ws, stream)
+        cce.cce_backward(h.h, one, dH, dW, stream)
+        torch.cuda.synchronize()
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        handles[name] = (h, ws)
+
+    from bench import ClockSampler
+    import time
+    res = {name: {"step": [], "fwd": [], "bwd": [], "mhz": []} for name, _, _ in vs}
+    for r in range(args.rounds):
+        for name, _, _ in vs:
+            h, ws = handles[name]
+            time.sleep(args.rest)
+            smp = ClockSampler(0, period_ms=args.sample_ms)
+            smp.start()
+            time.sleep(0.2)
+            for _ in range(args.warmup):
+                cce.cce_forward(h.h, H, W, y, loss, lse, nvt, ws, stream)
+                cce.cce_backward(h.h, one, dH, dW, stream)
+            torch.cuda.synchronize()
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                cce.cce_forward(h.h, H, W, y, loss, lse, nvt, ws, stream)
+                ev[i][1].record(stream)
+                cce.cce_backward(h.h, one, dH, dW, stream)
+                ev[i][2].record(stream)
+            torch.cuda.synchronize()
+            ck = smp.stop()
+            if ck and ck["sm_mhz"]:
+                res[name]["mhz"].append((ck["sm_mhz"], ck.get("power_w_max"), ck.get("reasons")))
+            res[name]["step"] += [a.elapsed_time(c_) for a, b, c_ in ev]
+            res[name]["fwd"] += [a.elapsed_time(b) for a, b, c_ in ev]
+            res[name]["bwd"] += [b.elapsed_time(c_) for a, b, c_ in ev]
+    for name, _, _ in vs:
+        d = res[name]
+        print(f"{name:24s} step {statistics.median(d['step']):7.3f} ms  fwd {statistics.median(d['fwd']):7.3f}"
+              f"  bwd {statistics.median(d['bwd']):7.3f}  (min step {min(d['step']):.3f})  sm MHz {d['mhz']}", flush=True)
+    for h, _ in handles.values():
+        h.close()
+
+
+if __name__ == "__main__":
+    main()

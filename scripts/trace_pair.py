@@ -18,7 +18,7 @@ dev = torch.device("cuda:0")
 c = workload.CONFIGS[cfg]
 p = workload.make_config(cfg, seed=42)
 H, W, y = to_dev(p, dev)
-h = cce.CCEHandle(vocab_total=c.V)
+h = cce.CCEHandle(vocab_total=c.V, flags=int(os.environ.get("CCE_FLAGS", "0")))
 dH = torch.empty(H.shape, dtype=torch.bfloat16, device=dev)
 dW = torch.empty(W.shape, dtype=torch.bfloat16, device=dev)
 one = torch.ones((), dtype=torch.float32, device=dev)
@@ -51,11 +51,13 @@ for name, rec in (("forward", allrec[1]), ("backward", allrec[0])):
     fw = rec[:, 12].astype(np.float64) / 1e3
     kb = rec[:, 7].astype(np.float64)
     cyc = rec[:, 13].astype(np.float64)
-    print(f" {name}: items {len(rec)} span {ep1.max():.1f} us")
-    for t in sorted(set(typ.tolist())):
-        m = typ == t
-        print(f"   {NAMES[t]:3s} n={m.sum():6d} kb={kb[m].mean():5.1f} | mma window {np.mean(m1[m]-m0[m]):7.2f} us "
+    lat = rec[:, 15].astype(np.float64)
+    print(f" {name}: items {len(rec)} span {ep1.max():.1f} us; sum of dep-wait {np.sum(rdy-deq):.0f} us")
+    npk = rec[:, 14].astype(np.int64)
+    for t, npv in sorted(set(zip(typ.tolist(), npk.tolist()))):
+        m = (typ == t) & (npk == npv)
+        print(f"   {NAMES[t]:3s}{'/NP' + str(npv) if npv else '':5s} n={m.sum():6d} kb={kb[m].mean():5.1f} | mma window {np.mean(m1[m]-m0[m]):7.2f} us "
               f"(full-wait {np.mean(fw[m]):6.2f}) | load window {np.mean(l1[m]-l0[m]):7.2f} | "
-              f"mma_end->epi0 {np.mean(ep0[m]-m1[m]):6.2f} | epi {np.mean(ep1[m]-ep0[m]):6.2f} | "
+              f"mma_end->epi0 {np.mean(ep0[m]-m1[m]):6.2f} | epi {np.mean(ep1[m]-ep0[m]):6.2f} | dep-wait {np.mean(rdy[m]-deq[m]):6.2f} | "
               f"per-kb {np.mean((m1[m]-m0[m])/np.maximum(kb[m],1)):.3f} us, {np.mean(cyc[m]/np.maximum(kb[m],1)):.0f} cyc"
-              f" (clock {np.sum(cyc[m])/np.sum((m1[m]-m0[m])*1e3):.2f} GHz)")
+              f" (clock {np.sum(cyc[m])/np.sum((m1[m]-m0[m])*1e3):.2f} GHz) | issue->full {np.mean(lat[m]/np.maximum(kb[m],1)):.0f} cyc")

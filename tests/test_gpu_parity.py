@@ -33,7 +33,8 @@ def test_tiny_config(dev, seed):
     _check(workload.make_config("tiny", seed=seed), dev)
 
 
-@pytest.mark.parametrize("flags", [0, 8, 4, 6], ids=["quad", "pair", "cta1_queue", "cta1_per_chunk"])
+@pytest.mark.parametrize("flags", [0, 32, 16, "pairs_only", 4, 6],
+                         ids=["pair", "quad+pairs", "quad_only", "quad_queue_on_pairs", "cta1_queue", "cta1_per_chunk"])
 @pytest.mark.parametrize("N,D,V,ign", [
     (700, 128, 3000, "bern40"),        # ragged rows (5.5 tiles), ragged vocab (11.7 tiles)
     (257, 64, 256, "none"),             # exactly one vocab tile, one ragged row
@@ -41,9 +42,25 @@ def test_tiny_config(dev, seed):
     (384, 896, 9000, "bern40"),         # Qwen hidden size, 2 chunks
     (1000, 128, 41000, "bern40"),       # 6 chunks: Gbuf ring slots reused, dH accumulated 6x
 ])
-def test_multi_tile_shapes(dev, N, D, V, ign, flags):
+def test_multi_tile_shapes(dev, N, D, V, ign, flags, monkeypatch):
     p = workload.make_problem(N, D, V, seed=N + V, ignore=ign)
+    if flags == "pairs_only":
+        # the quad work queue drained by single CTA pairs only (the co-launch variant)
+        monkeypatch.setenv("CCE_QUAD_CLUSTERS", "0")
+        flags = 32
     _check(p, dev, flags=flags)
+
+
+@pytest.mark.parametrize("N,D,V,ign", [
+    (520, 2048, 9000, "none"),     # configs[2] hidden size (paper memory example), 0% ignored
+    (300, 4096, 5000, "bern40"),   # configs[3] hidden size (Llama-3-8B head), ragged rows / vocabulary
+    (700, 3584, 6100, "bern40"),   # configs[4] hidden size (Qwen2.5-7B head), 14 x 256 hidden tiles
+])
+def test_large_hidden_sizes(dev, N, D, V, ign):
+    """The wide-hidden configurations: D = 2048 / 3584 / 4096 (8 / 14 / 16 hidden tiles
+    of 256, i.e. 4 / 7 / 8 quad items per dW / dH row or vocabulary tile)."""
+    p = workload.make_problem(N, D, V, seed=D + V, ignore=ign)
+    _check(p, dev)
 
 
 @pytest.mark.parametrize("regime", ["peaked", "extreme", "zero"])
