@@ -56,6 +56,10 @@ def lib():
         L.oracle_cce.restype = ctypes.c_int
         L.oracle_dlogits.argtypes = [p, p, p, i64, i64, i64, i32, f64, p]
         L.oracle_dlogits.restype = ctypes.c_int
+        L.oracle_cce_reg.argtypes = [p, p, p, i64, i64, i64, i32, f64, f64, f64, p, p, p, p, p]
+        L.oracle_cce_reg.restype = ctypes.c_int
+        L.oracle_dlogits_reg.argtypes = [p, p, p, i64, i64, i64, i32, f64, f64, f64, p]
+        L.oracle_dlogits_reg.restype = ctypes.c_int
         L.oracle_cce_rows.argtypes = [p, p, p, i64, i64, f64, p, i64, p, p, p]
         L.oracle_cce_rows.restype = ctypes.c_int
         L.oracle_dW_rows.argtypes = [p, p, p, i64, i64, i32, p, f64, p, i64, p]
@@ -97,8 +101,9 @@ def num_threads() -> int:
     return int(lib().oracle_num_threads())
 
 
-def cce(H_bits, W_bits, labels, ignore_index=-100, dloss=1.0, grads=True):
-    """Full forward+backward.  Returns dict(loss, lse[N], n_valid, dH[N,D], dW[V,D]) in fp64."""
+def cce(H_bits, W_bits, labels, ignore_index=-100, dloss=1.0, grads=True, label_smoothing=0.0, z_loss=0.0):
+    """Full forward+backward.  Returns dict(loss, lse[N], n_valid, dH[N,D], dW[V,D]) in fp64.
+    label_smoothing (eps) and z_loss (lambda) follow oracle_cce_reg."""
     H = _bits(H_bits); W = _bits(W_bits)
     y = np.ascontiguousarray(labels, dtype=np.int32)
     N, D = H.shape
@@ -109,18 +114,19 @@ def cce(H_bits, W_bits, labels, ignore_index=-100, dloss=1.0, grads=True):
     nv = np.zeros(1, np.int64)
     dH = np.zeros((N, D), np.float64) if grads else None
     dW = np.zeros((V, D), np.float64) if grads else None
-    _check(lib().oracle_cce(_ptr(H), _ptr(W), _ptr(y), N, D, V, ignore_index, float(dloss),
-                            _ptr(loss), _ptr(lse), _ptr(nv), _ptr(dH), _ptr(dW)))
+    _check(lib().oracle_cce_reg(_ptr(H), _ptr(W), _ptr(y), N, D, V, ignore_index, float(label_smoothing),
+                                float(z_loss), float(dloss), _ptr(loss), _ptr(lse), _ptr(nv), _ptr(dH), _ptr(dW)))
     return {"loss": float(loss[0]), "lse": lse, "n_valid": int(nv[0]), "dH": dH, "dW": dW}
 
 
-def dlogits(H_bits, W_bits, labels, ignore_index=-100, dloss=1.0):
+def dlogits(H_bits, W_bits, labels, ignore_index=-100, dloss=1.0, label_smoothing=0.0, z_loss=0.0):
     H = _bits(H_bits); W = _bits(W_bits)
     y = np.ascontiguousarray(labels, dtype=np.int32)
     N, D = H.shape
     V = W.shape[0]
     G = np.zeros((N, V), np.float64)
-    _check(lib().oracle_dlogits(_ptr(H), _ptr(W), _ptr(y), N, D, V, ignore_index, float(dloss), _ptr(G)))
+    _check(lib().oracle_dlogits_reg(_ptr(H), _ptr(W), _ptr(y), N, D, V, ignore_index, float(label_smoothing),
+                                    float(z_loss), float(dloss), _ptr(G)))
     return G
 
 

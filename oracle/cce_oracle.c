@@ -23,6 +23,13 @@
  *                                                    P:254-258 (Prop. CE Gradient)
  *   dH[n,:] = sum_v G[n,v] W[v,:]                    P:666 (grad_h += probs @ W[chunk])
  *   dW[v,:] = sum_n G[n,v] H[n,:]                    P:667 (grad_W[chunk] += probs^T @ h)
+ * Regularised variant (oracle_cce_reg), the paper's definitions
+ * with label smoothing eps and z-loss weight lam (both 0 gives the above exactly):
+ *   l_n     = (1-eps) (lse_n - z[n,y_n])                     (1-eps) L(z, c)
+ *           + eps (lse_n - (1/V) sum_v z[n,v])               eps L_uniform(z)
+ *           + lam lse_n^2                                    Z-loss, added
+ *   G[n,v]  = s [ (1-eps)(p - 1[v==y]) + eps (p - 1/V) + 2 lam lse_n p ],  p = exp(z - lse_n)
+ *             (the three terms' gradients: P:254-258; d/dz of -mean z = -1/V)
  * Rows whose label equals ignore_index are skipped:
  * they get lse = 0, dH row = 0 and contribute nothing to dW or to the mean.
  *
@@ -96,10 +103,20 @@ static double lse_two_pass(const double *z, int64_t V) {
  *   dH[N,D], dW[V,D], all fp64.  With n_valid == 0: loss = 0 and zero grads
  *   (reading R2).
  */
-int oracle_cce(const double *H, const double *W, const int32_t *labels,
-               int64_t N, int64_t D, int64_t V, int32_t ignore_index,
-               double dloss, double *loss, double *lse, int64_t *n_valid,
-               double *dH, double *dW) {
+/* dL/dz[v] of one valid row's loss (before the mean scale), R11/R12. */
+static double row_grad(double zv, double lse, int is_target, double eps, double lam, int64_t V) {
+    double p = exp(zv - lse);
+    double ce = p - (is_target ? 1.0 : 0.0);
+    double uni = p - 1.0 / (double)V;                 /* d/dz of lse - mean z */
+    double zl = 2.0 * lam * lse * p;
+    return (1.0 - eps) * ce + eps * uni + zl;
+}
+
+int oracle_cce_reg(const double *H, const double *W, const int32_t *labels,
+                   int64_t N, int64_t D, int64_t V, int32_t ignore_index,
+                   double eps, double lam,
+                   double dloss, double *loss, double *lse, int64_t *n_valid,
+                   double *dH, double *dW) {
     if (N < 0 || D <= 0 || V <= 0) return ORACLE_ERR_INVALID;
     int64_t nv = 0;
     int rc = oracle_validate(labels, N, V, ignore_index, &nv);
@@ -132,12 +149,14 @@ int oracle_cce(const double *H, const double *W, const int32_t *labels,
             logit_row(h, W, D, V, z);
             double l = lse_two_pass(z, V);
             lse[n] = l;
-            row_loss[n] = l - z[y];
+            double zsum = 0.0;
+            for (int64_t v = 0; v < V; ++v) zsum += z[v];
+            row_loss[n] = (1.0 - eps) * (l - z[y]) + eps * (l - zsum / (double)V) + lam * l * l;
             if (dH) {
                 double *out = dH + n * D;
                 for (int64_t d = 0; d < D; ++d) out[d] = 0.0;
                 for (int64_t v = 0; v < V; ++v) {
-                    double g = scale * (exp(z[v] - l) - (v == y ? 1.0 : 0.0));
+                    double g = scale * row_grad(z[v], l, v == y, eps, lam, V);
                     const double *w = W + v * D;
                     for (int64_t d = 0; d < D; ++d) out[d] += g * w[d];
                 }
@@ -167,7 +186,7 @@ int oracle_cce(const double *H, const double *W, const int32_t *labels,
                 const double *hr = H + n * D;
                 double zv = 0.0;
                 for (int64_t d = 0; d < D; ++d) zv += hr[d] * w[d];
-                double g = scale * (exp(zv - lse[n]) - (v == y ? 1.0 : 0.0));
+                double g = scale * row_grad(zv, lse[n], v == y, eps, lam, V);
                 for (int64_t d = 0; d < D; ++d) out[d] += g * hr[d];
             }
         }
@@ -175,14 +194,22 @@ int oracle_cce(const double *H, const double *W, const int32_t *labels,
     return ORACLE_OK;
 }
 
+/* The unregularised loss (eps = lam = 0). */
+int oracle_cce(const double *H, const double *W, const int32_t *labels,
+               int64_t N, int64_t D, int64_t V, int32_t ignore_index,
+               double dloss, double *loss, double *lse, int64_t *n_valid,
+               double *dH, double *dW) {
+    return oracle_cce_reg(H, W, labels, N, D, V, ignore_index, 0.0, 0.0, dloss, loss, lse, n_valid, dH, dW);
+}
+
 /*
  * The dlogits matrix itself, G[N,V] (fp64), for tiny problems only: the
  * quantity the paper's backward forms chunk by chunk.  Ignored
  * rows are all-zero.
  */
-int oracle_dlogits(const double *H, const double *W, const int32_t *labels,
-                   int64_t N, int64_t D, int64_t V, int32_t ignore_index,
-                   double dloss, double *G) {
+int oracle_dlogits_reg(const double *H, const double *W, const int32_t *labels,
+                       int64_t N, int64_t D, int64_t V, int32_t ignore_index,
+                       double eps, double lam, double dloss, double *G) {
     int64_t nv = 0;
     int rc = oracle_validate(labels, N, V, ignore_index, &nv);
     if (rc) return rc;
@@ -200,11 +227,17 @@ int oracle_dlogits(const double *H, const double *W, const int32_t *labels,
         logit_row(h, W, D, V, z);
         double l = lse_two_pass(z, V);
         for (int64_t v = 0; v < V; ++v)
-            G[n * V + v] = scale * (exp(z[v] - l) - (v == y ? 1.0 : 0.0));
+            G[n * V + v] = scale * row_grad(z[v], l, v == y, eps, lam, V);
     }
     free(h);
     free(z);
     return ORACLE_OK;
+}
+
+int oracle_dlogits(const double *H, const double *W, const int32_t *labels,
+                   int64_t N, int64_t D, int64_t V, int32_t ignore_index,
+                   double dloss, double *G) {
+    return oracle_dlogits_reg(H, W, labels, N, D, V, ignore_index, 0.0, 0.0, dloss, G);
 }
 
 /*

@@ -6,13 +6,18 @@ cd "$(dirname "$0")/.."
 cp oracle/cce_oracle.c /tmp/oracle_orig.c
 trap 'cp /tmp/oracle_orig.c oracle/cce_oracle.c; python -c "import oracle; oracle.build(force=True)"' EXIT
 muts=(
- 's/(v == y ? 1.0 : 0.0)/(v == y ? 0.0 : 0.0)/'                       # dropped one-hot
+ 's/double ce = p - (is_target ? 1.0 : 0.0);/double ce = p;/'            # dropped one-hot
  's/dloss \/ (double)nv/dloss \/ (double)N/'                           # wrong mean divisor
  's/for (int64_t v = 0; v < V; ++v) s += exp(z\[v\] - m);/for (int64_t v = 1; v < V; ++v) s += exp(z[v] - m);/'  # dropped term
  's/out\[d\] += g \* hr\[d\];/out[d] += g * w[d];/'                   # transposed operand in dW
- 's/row_loss\[n\] = l - z\[y\];/row_loss[n] = l + z[y];/'             # sign
+ 's/row_loss\[n\] = (1.0 - eps) \* (l - z\[y\])/row_loss[n] = (1.0 - eps) * (l + z[y])/'  # sign
  's/return m + log(s);/return log(s);/'                                # dropped max shift
- 's/double g = scale \* (exp(zv - lse\[n\])/double g = scale * (exp(zv - lse[0])/'  # wrong index
+ 's/double g = scale \* row_grad(zv, lse\[n\]/double g = scale * row_grad(zv, lse[0]/'  # wrong index
+ 's/return (1.0 - eps) \* ce + eps \* uni + zl;/return (1.0 - eps) * (ce + zl) + eps * uni;/'  # z-loss grad blended (Liger order)
+ 's/+ lam \* l \* l;/+ (1.0 - eps) * lam * l * l;/'                  # z-loss term blended (Liger order)
+ 's/double uni = p - 1.0 \/ (double)V;/double uni = p - 1.0 \/ (double)(V - 1);/'  # wrong uniform mass
+ 's/eps \* (l - zsum \/ (double)V)/eps * (l - zsum \/ (double)(V + 1))/'  # wrong mean of logits
+ 's/double zl = 2.0 \* lam \* lse \* p;/double zl = lam * lse * p;/'  # dropped factor 2
 )
 fail=0
 for m in "${muts[@]}"; do

@@ -338,3 +338,95 @@ def test_workload_packed_padding_recipe():
     a = workload.normal_bf16(1, 2, 3, 5, 1.0)
     b = workload.normal_bf16(1, 2, 3, 5, 1.0, chunk_elems=4)
     assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- regularised loss (NEXT #1)
+# Label smoothing (Def. Smoothed CE) and z-loss (Def. Z-Loss, P:281-287;
+# gradient Prop. P:2686-2691); readings R11 / R12.
+def test_golden_zloss_zero_logits():
+    """all-zero logits, lambda_z = 1e-4, V = 97 -> the z-loss adds 1e-4 (ln 97)^2 =
+    2.093e-3; with W = 0 label smoothing leaves the loss at ln V (z_y = mean z = 0)."""
+    g = GOLD["zloss_zero_logits_V97"]
+    V = g["V"]
+    H = np.ones((4, 8))
+    W = np.zeros((V, 8))
+    y = np.array([0, 5, V - 1, 40], np.int32)
+    base = oracle.cce(H, W, y)["loss"]
+    r = oracle.cce(H, W, y, z_loss=g["z_weight"])
+    assert abs((r["loss"] - base) - g["extra"]) <= g["tol"]
+    for eps in (0.1, 0.5):
+        r2 = oracle.cce(H, W, y, z_loss=g["z_weight"], label_smoothing=eps)
+        assert abs(r2["loss"] - r["loss"]) <= 1e-14
+        # W = 0: p = 1/V, so G = s [(1 + 2 lam ln V)/V - (1-eps) 1[y] - eps/V]
+        s = 1.0 / len(y)
+        G = oracle.dlogits(H, W, y, label_smoothing=eps, z_loss=g["z_weight"])
+        want = s * ((1 + 2 * g["z_weight"] * math.log(V)) / V - eps / V)
+        assert abs(G[0, 1] - want) <= 1e-15
+        assert abs(G[0, 0] - (want - s * (1 - eps))) <= 1e-15
+
+
+@pytest.mark.parametrize("eps,lam", [(0.1, 0.0), (0.0, 1e-2), (0.1, 1e-4), (0.3, 5e-2)])
+def test_regularised_matches_torch_fp64(eps, lam):
+    """Library routine: torch fp64 cross_entropy(label_smoothing=eps) -- its definition
+    (1-eps) nll + eps (lse - mean z) is P:272-276 -- plus lam * mean_valid(lse^2),
+    autograd for the gradients."""
+    torch = pytest.importorskip("torch")
+    N, D, V = 20, 24, 531
+    H, W, y = _rand_problem(N, D, V, 300 + int(eps * 10) + int(lam * 1e4), ignore_n=4)
+    Ht = torch.tensor(H, requires_grad=True)
+    Wt = torch.tensor(W, requires_grad=True)
+    yt = torch.tensor(y, dtype=torch.long)
+    z = Ht @ Wt.T
+    ce = torch.nn.functional.cross_entropy(z, yt, ignore_index=-100, label_smoothing=eps)
+    valid = yt != -100
+    lse = torch.logsumexp(z[valid], dim=1)
+    lt = ce + lam * (lse * lse).mean()
+    lt.backward()
+    r = oracle.cce(H, W, y, label_smoothing=eps, z_loss=lam)
+    assert abs(r["loss"] - lt.item()) <= 1e-12
+    np.testing.assert_allclose(r["dH"], Ht.grad.numpy(), rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(r["dW"], Wt.grad.numpy(), rtol=1e-10, atol=1e-14)
+
+
+def test_regularised_finite_differences():
+    N, D, V = 5, 7, 60
+    H, W, y = _rand_problem(N, D, V, 31, ignore_n=1)
+    eps_ls, lam = 0.2, 3e-2
+    r = oracle.cce(H, W, y, label_smoothing=eps_ls, z_loss=lam)
+    h = 1e-6
+
+    def loss(Hx, Wx):
+        return oracle.cce(Hx, Wx, y, grads=False, label_smoothing=eps_ls, z_loss=lam)["loss"]
+
+    fdH = np.zeros_like(H)
+    for n in range(N):
+        for d in range(D):
+            Hp = H.copy(); Hp[n, d] += h
+            Hm = H.copy(); Hm[n, d] -= h
+            fdH[n, d] = (loss(Hp, W) - loss(Hm, W)) / (2 * h)
+    assert np.linalg.norm(fdH - r["dH"]) <= 1e-6 * np.linalg.norm(r["dH"])
+    for v in (0, 7, int(y[0]) if y[0] >= 0 else int(y[1]), V - 1):
+        fd = np.zeros(D)
+        for d in range(D):
+            Wp = W.copy(); Wp[v, d] += h
+            Wm = W.copy(); Wm[v, d] -= h
+            fd[d] = (loss(H, Wp) - loss(H, Wm)) / (2 * h)
+        assert np.linalg.norm(fd - r["dW"][v]) <= 1e-6 * max(np.linalg.norm(r["dW"][v]), 1e-3)
+
+
+def test_regularised_row_sums_and_limits():
+    """Row sums of the regularised dlogits: (1-eps)*0 + eps*(1 - 1) + 2 lam lse * 1, so
+    sum_v G[n,v] = s 2 lam lse_n (label smoothing drops out); eps = lam = 0 is the
+    plain loss bit for bit."""
+    N, D, V = 9, 12, 300
+    H, W, y = _rand_problem(N, D, V, 41, ignore_n=2)
+    eps, lam = 0.15, 7e-3
+    G = oracle.dlogits(H, W, y, label_smoothing=eps, z_loss=lam)
+    r = oracle.cce(H, W, y, label_smoothing=eps, z_loss=lam, grads=False)
+    s = 1.0 / int((y != -100).sum())
+    for n in range(N):
+        want = 0.0 if y[n] == -100 else s * 2 * lam * r["lse"][n]
+        assert abs(G[n].sum() - want) <= 1e-14
+    a = oracle.cce(H, W, y)
+    b = oracle.cce(H, W, y, label_smoothing=0.0, z_loss=0.0)
+    assert a["loss"] == b["loss"] and np.array_equal(a["dH"], b["dH"]) and np.array_equal(a["dW"], b["dW"])
