@@ -96,6 +96,16 @@ typedef struct {
   int32_t world;          /* number of vocabulary shards (ranks), 1 if unsharded */
   void *nccl_comm;        /* ncclComm_t from cce_nccl_comm_init when world > 1, else NULL */
   uint32_t flags;         /* CCE_FLAG_* */
+  /* Regularised loss, both 0 by default (the paper's CCE kernels
+   * apply neither):
+   *   label_smoothing eps in [0, 1): Def. Smoothed CE,
+   *     l_n = (1-eps)(lse_n - z_y) + eps (lse_n - mean_v z_v)
+   *   z_loss lambda >= 0: Def. Z-Loss, added: l_n += lambda lse_n^2
+   * and their gradients.  mean_v runs over the GLOBAL
+   * vocabulary (vocab_total).  The CTA-pair / quad kernels support both; with
+   * CCE_FLAG_ONE_CTA a non-zero value makes cce_forward return CCE_ERR_UNSUPPORTED. */
+  float label_smoothing;
+  float z_loss;
 } cce_config;
 
 /* Fill `cfg` with defaults: ignore_index=-100, vocab_total=0 (must be set),

@@ -48,7 +48,7 @@ class CCEError(RuntimeError):
 class cce_config(ctypes.Structure):
     _fields_ = [("ignore_index", ctypes.c_int32), ("vocab_total", ctypes.c_int64), ("vocab_offset", ctypes.c_int64),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("label_smoothing", ctypes.c_float), ("z_loss", ctypes.c_float)]
 
 
 _lib = None
@@ -121,7 +121,7 @@ def _stream(stream):
 
 # ----------------------------------------------------------------- C-ABI mirrors
 def cce_create(vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0, rank: int = 0, world: int = 1,
-               nccl_comm=None, flags: int = 0) -> ctypes.c_void_p:
+               nccl_comm=None, flags: int = 0, label_smoothing: float = 0.0, z_loss: float = 0.0) -> ctypes.c_void_p:
     cfg = cce_config()
     lib().cce_config_default(ctypes.byref(cfg))
     cfg.ignore_index = ignore_index
@@ -131,6 +131,8 @@ def cce_create(vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0
     cfg.world = world
     cfg.nccl_comm = nccl_comm
     cfg.flags = flags
+    cfg.label_smoothing = label_smoothing
+    cfg.z_loss = z_loss
     h = ctypes.c_void_p()
     _check(lib().cce_create(ctypes.byref(h), ctypes.byref(cfg)), "cce_create")
     return h
@@ -226,8 +228,9 @@ class CCEHandle:
     """A library handle plus a cached device workspace (torch-allocated)."""
 
     def __init__(self, vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0, rank: int = 0,
-                 world: int = 1, nccl_comm=None, flags: int = 0):
-        self.h = cce_create(vocab_total, ignore_index, vocab_offset, rank, world, nccl_comm, flags)
+                 world: int = 1, nccl_comm=None, flags: int = 0, label_smoothing: float = 0.0, z_loss: float = 0.0):
+        self.h = cce_create(vocab_total, ignore_index, vocab_offset, rank, world, nccl_comm, flags, label_smoothing,
+                            z_loss)
         self.vocab_total = vocab_total
         self.ignore_index = ignore_index
         self._ws = None
@@ -306,7 +309,7 @@ _CCEFunction = None
 
 
 def linear_cross_entropy(H, W, labels, ignore_index: int = -100, handle: CCEHandle | None = None,
-                         return_lse: bool = False):
+                         return_lse: bool = False, label_smoothing: float = 0.0, z_loss: float = 0.0):
     """Mean cross-entropy of softmax(H W^T) against labels, fused and never
     materialising the [N, V] logits.  H [N,D] bf16, W [V,D] bf16, labels [N] int32."""
     global _CCEFunction
@@ -314,6 +317,7 @@ def linear_cross_entropy(H, W, labels, ignore_index: int = -100, handle: CCEHand
     if _CCEFunction is None:
         _CCEFunction = _make_function()
     if handle is None:
-        handle = CCEHandle(vocab_total=W.shape[0], ignore_index=ignore_index)
+        handle = CCEHandle(vocab_total=W.shape[0], ignore_index=ignore_index, label_smoothing=label_smoothing,
+                           z_loss=z_loss)
     loss, lse, nv = _CCEFunction.apply(H, W, labels, handle)
     return (loss, lse) if return_lse else loss

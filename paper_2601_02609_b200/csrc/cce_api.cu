@@ -196,7 +196,8 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   int64_t Npad, Tv, C;
   int64_t n_chunks, sched_ints;
-  size_t scal, pos, idx, labels_c, Hc, part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32, sched, total;
+  size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32, sched,
+      total;
 };
 
 Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots) {
@@ -220,6 +221,7 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
   L.labels_c = take((size_t)L.Npad * 4);
   L.Hc = take((size_t)L.Npad * D * 2);
   L.part = take((size_t)L.Tv * L.Npad * 8);
+  L.zs_part = take((size_t)L.Tv * L.Npad * 4);  // label smoothing only: per-tile logit sums
   L.zy_c = take((size_t)L.Npad * 4);
   L.stats = take((size_t)L.Npad * 16);
   L.stats_all = take((size_t)world * L.Npad * 16);
@@ -413,6 +415,8 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
     return CCE_ERR_INVALID_VALUE;
   if ((cfg->world > 1) != (cfg->nccl_comm != nullptr)) return CCE_ERR_INVALID_VALUE;
   if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
+  if (!(cfg->label_smoothing >= 0.f && cfg->label_smoothing < 1.f) || !(cfg->z_loss >= 0.f && cfg->z_loss < 1e30f))
+    return CCE_ERR_INVALID_VALUE;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return CCE_ERR_UNSUPPORTED;
   int major = 0, sms = 0;
@@ -545,7 +549,12 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
     p.labels_c = at<int>(ws, L.labels_c);
     p.part = at<float2>(ws, L.part);
     p.zy_c = at<float>(ws, L.zy_c);
+    p.ls_eps = h->cfg.label_smoothing;
+    p.z_loss = h->cfg.z_loss;
+    p.inv_vtotal = (float)(1.0 / (double)h->cfg.vocab_total);
+    p.zs_part = h->cfg.label_smoothing > 0.f ? at<float>(ws, L.zs_part) : nullptr;
     if (h->cfg.flags & CCE_FLAG_ONE_CTA) {
+      if (h->cfg.label_smoothing != 0.f || h->cfg.z_loss != 0.f) return CCE_ERR_UNSUPPORTED;
       CUtensorMap tA, tB;
       if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, BM)) return CCE_ERR_CUDA;
       if (!make_map(&tB, W, D, V_local, ldw, BN)) return CCE_ERR_CUDA;
@@ -580,7 +589,8 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
     // an empty shard (V_local == 0) merges zero tiles: (m=-inf, d=0, z_y=0) for every row
     ProfScope ps(h, s, 4);
     k_merge_tiles<<<(unsigned)((L.Npad + 31) / 32), 1024, 0, s>>>(
-        at<float2>(ws, L.part), V_local > 0 ? (int)L.Tv : 0, (int)L.Npad, at<float>(ws, L.zy_c), nvp, stats);
+        at<float2>(ws, L.part), V_local > 0 ? (int)L.Tv : 0, (int)L.Npad, at<float>(ws, L.zy_c), nvp,
+        (h->cfg.label_smoothing > 0.f && V_local > 0) ? at<float>(ws, L.zs_part) : nullptr, stats);
   }
   const float4* stats_all = stats;
   if (h->cfg.world > 1) {
@@ -594,7 +604,9 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
     ProfScope ps(h, s, 4);
     k_finalize<<<grid_for(N, 256, 8 * h->num_sms), 256, 0, s>>>(stats_all, h->cfg.world, (int)L.Npad,
                                                                 at<int>(ws, L.pos), (int)N, lse, at<float>(ws, L.lse_c),
-                                                                at<float>(ws, L.loss_rows));
+                                                                at<float>(ws, L.loss_rows), h->cfg.label_smoothing,
+                                                                h->cfg.z_loss,
+                                                                (float)(1.0 / (double)h->cfg.vocab_total));
   }
   {
     ProfScope ps(h, s, 4);
@@ -641,6 +653,9 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     p.gbuf = at<__nv_bfloat16>(ws, L.gbuf);
     p.dW = static_cast<__nv_bfloat16*>(dW);
     p.dH32 = dH32;
+    p.ls_eps = h->cfg.label_smoothing;
+    p.z_loss = h->cfg.z_loss;
+    p.inv_vtotal = (float)(1.0 / (double)h->cfg.vocab_total);
     int slots = h->slots, strict = 0;
     if (const char* e = getenv("CCE_DEBUG_SLOTS")) slots = atoi(e) >= 2 && atoi(e) <= h->slots ? atoi(e) : h->slots;
     if (const char* e = getenv("CCE_DEBUG_STRICT")) strict = atoi(e);

@@ -93,14 +93,17 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ H, long long ldh
 // thread (lane, w) folds tiles t = w, w+32, ... of row i0+lane in a single pass
 // (coalesced: part is [tile][row]), then warp 0 folds the 32 slices in order.
 // Fixed order -> deterministic.  Out: (m, d, z_y) per compact row.
+// With label smoothing the per-tile logit sums (zs_part, may be nullptr) are summed in
+// the same fixed order into the 4th stat (sum_v z_v of the row over this shard).
 __global__ void __launch_bounds__(1024) k_merge_tiles(const float2* __restrict__ part, int Tv, int Npad,
                                                       const float* __restrict__ zy_c, const int* __restrict__ n_valid,
-                                                      float4* __restrict__ stats) {
+                                                      const float* __restrict__ zs_part, float4* __restrict__ stats) {
   __shared__ float2 red[32][33];
+  __shared__ float redz[32][33];
   const int nv = *n_valid;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
-  float m = -INFINITY, d = 0.f;
+  float m = -INFINITY, d = 0.f, zs = 0.f;
   if (i < nv) {
     for (int t = w; t < Tv; t += 32) {
       const float2 pd = part[(size_t)t * Npad + i];
@@ -109,12 +112,14 @@ __global__ void __launch_bounds__(1024) k_merge_tiles(const float2* __restrict__
         d = d * expf(m - mn) + pd.y * expf(pd.x - mn);
         m = mn;
       }
+      if (zs_part) zs += zs_part[(size_t)t * Npad + i];
     }
   }
   red[w][lane] = make_float2(m, d);
+  redz[w][lane] = zs;
   __syncthreads();
   if (w == 0 && i < nv) {
-    float M = -INFINITY, S = 0.f;
+    float M = -INFINITY, S = 0.f, Z = 0.f;
     for (int k = 0; k < 32; ++k) {
       const float2 pd = red[k][lane];
       if (pd.y > 0.f) {
@@ -122,28 +127,32 @@ __global__ void __launch_bounds__(1024) k_merge_tiles(const float2* __restrict__
         S = S * expf(M - mn) + pd.y * expf(pd.x - mn);
         M = mn;
       }
+      Z += redz[k][lane];
     }
-    stats[i] = make_float4(M, S, zy_c[i], 0.f);
+    stats[i] = make_float4(M, S, zy_c[i], Z);
   }
 }
 
 // a4 (global part) + a9 combine: merge the per-rank stats in rank order (empty
 // shards contribute m=-inf, d=0), lse = m + log d (Theorem), per-row loss
 // lse - z_y.  Ignored rows get lse = 0 (reading R4).
+// With label smoothing eps / z-loss lambda the row loss is
+//   (1 - eps)(lse - z_y) + eps (lse - sum_v z_v / V_total) + lambda lse^2.
 __global__ void k_finalize(const float4* __restrict__ stats_all, int world, int Npad, const int* __restrict__ pos,
                            int N, float* __restrict__ lse_out, float* __restrict__ lse_c,
-                           float* __restrict__ loss_rows) {
+                           float* __restrict__ loss_rows, float ls_eps, float z_loss, float inv_vtotal) {
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     const int i = pos[n];
     if (i < 0) {
       if (lse_out) lse_out[n] = 0.f;
       continue;
     }
-    float m = -INFINITY, zy = 0.f;
+    float m = -INFINITY, zy = 0.f, zs = 0.f;
     for (int r = 0; r < world; ++r) {
       const float4 s = stats_all[(size_t)r * Npad + i];
       m = fmaxf(m, s.x);
       zy += s.z;
+      zs += s.w;
     }
     float d = 0.f;
     for (int r = 0; r < world; ++r) {
@@ -152,7 +161,10 @@ __global__ void k_finalize(const float4* __restrict__ stats_all, int world, int 
     }
     const float lse = m + logf(d);
     lse_c[i] = lse;
-    loss_rows[i] = lse - zy;
+    float l = lse - zy;
+    if (ls_eps != 0.f || z_loss != 0.f)
+      l = (1.f - ls_eps) * l + ls_eps * (lse - zs * inv_vtotal) + z_loss * lse * lse;
+    loss_rows[i] = l;
     if (lse_out) lse_out[n] = lse;
   }
 }

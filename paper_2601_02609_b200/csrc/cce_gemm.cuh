@@ -64,6 +64,11 @@ struct GemmParams {
   __nv_bfloat16* dW;    // DW: [V_local][D]
   float* dH32;          // DH: [Npad][D]
   int dh_accumulate;    // DH: 0 = overwrite (first chunk), 1 = add
+  // regularised loss (pair / quad kernels only; cce.h cce_config)
+  float ls_eps;         // label smoothing eps
+  float z_loss;         // z-loss weight lambda
+  float inv_vtotal;     // 1 / vocab_total (the mean of the logits runs over the global vocabulary)
+  float* zs_part;       // FWD: [ceil(V_local/256)][Npad] per-tile logit sums, or nullptr (eps == 0)
 };
 
 struct TileGeom {

@@ -154,6 +154,7 @@ struct PEpi {
   int q, half;  // lane quarter, column half
   int rank;
   float* xchg;
+  float* xz;    // forward only: 128 floats for the column-half merge of the logit sums
   uint8_t* stage;  // this warp's 4 KB store-staging tile
 };
 
@@ -163,12 +164,20 @@ __device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, con
   const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
   const int cb = e.half * (PN / 2);
   float m = -INFINITY, d = 0.f;
+  float zs = 0.f;  // sum of the logits (label smoothing's mean z)
+  const bool want_zs = p.zs_part != nullptr;
 #pragma unroll 1
   for (int j = 0; j < PN / 2 / 32; ++j) {
     float v[32];
     tmem_ld32(taddr + cb + j * 32, v);
     const int col0 = it.n0 + cb + j * 32;
     if (col0 >= p.V_local) break;  // warp-uniform
+    if (want_zs) {
+      float cs = 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) cs += (col0 + i < p.V_local) ? v[i] : 0.f;
+      zs += cs;
+    }
     if (col0 + 32 > p.V_local) {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
@@ -197,27 +206,39 @@ __device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, con
     }
   }
   float2* x = reinterpret_cast<float2*>(e.xchg);
-  if (e.half == 1) x[e.rit] = make_float2(m, d);
+  if (e.half == 1) {
+    x[e.rit] = make_float2(m, d);
+    if (want_zs) e.xz[e.rit] = zs;
+  }
   named_bar_sync(3 + e.q, 64);
   if (e.half == 0) {
     const float2 o = x[e.rit];
     const float mn = fmaxf(m, o.x);
     const float dd = (d > 0.f ? d * ex2((m - mn) * LOG2E) : 0.f) + (o.y > 0.f ? o.y * ex2((o.x - mn) * LOG2E) : 0.f);
-    if (rv) p.part[(size_t)(it.n0 / PN) * p.Npad + row] = make_float2(mn, dd);
+    if (rv) {
+      p.part[(size_t)(it.n0 / PN) * p.Npad + row] = make_float2(mn, dd);
+      if (want_zs) p.zs_part[(size_t)(it.n0 / PN) * p.Npad + row] = zs + e.xz[e.rit];
+    }
   }
   named_bar_sync(3 + e.q, 64);
 }
 
 __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv,
                                       float scale, __nv_bfloat16* gslot) {
-  // G = s (exp(S - lse) - 1[v = y]) with s folded into the exponent.
+  // G = s (exp(S - lse) - 1[v = y]) with s folded into the exponent.  With
+  // label smoothing eps and z-loss lambda:
+  //   G = s [(1 + 2 lambda lse) exp(S - lse) - (1 - eps) 1[v = y] - eps / V]
   // Each warp converts 64 columns of its 32 rows at a time into a 4 KB SMEM tile
   // (16-byte chunks XOR-swizzled by row: conflict-free), then writes it out as
   // fully coalesced 512-byte runs of the column-blocked G ring.
   const int row = it.m0 + e.rank * HM + e.rit;
   const bool rv = row < nv;
   const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
-  const float off2 = rv ? (p.lse_c[row] * LOG2E - __log2f(fabsf(scale))) : INFINITY;
+  const float lse = rv ? p.lse_c[row] : 0.f;
+  const float sa = scale * (1.f + 2.f * p.z_loss * lse);  // scale of the softmax term
+  const float off2 = rv ? (lse * LOG2E - __log2f(fabsf(sa))) : INFINITY;
+  const float cu = rv ? -scale * p.ls_eps * p.inv_vtotal : 0.f;  // uniform term
+  const float tgt = scale * (1.f - p.ls_eps);                     // one-hot term
   const int c0 = it.c * p.C;
   const int width = min(p.C, p.V_local - c0);
   const int cb = e.half * (PN / 2);
@@ -236,15 +257,19 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
       float gg[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) gg[i] = ex2(fmaf(v[i], LOG2E, -off2));
-      if (scale < 0.f) {
+      if (sa < 0.f) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) gg[i] = -gg[i];
+      }
+      if (cu != 0.f) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) gg[i] += cu;
       }
       const unsigned toff = (unsigned)(y - col0);
       if (toff < 32u) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (toff == (unsigned)i) gg[i] -= scale;
+          if (toff == (unsigned)i) gg[i] -= tgt;
       }
       if (lcol0 + 32 > width) {
 #pragma unroll
@@ -626,6 +651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     e.rit = e.q * 32 + lane;
     e.rank = rank;
     e.xchg = xchg;
+    e.xz = reinterpret_cast<float*>(stage_base);  // forward items never use the store staging
     e.stage = stage_base + (warp - 4) * 4096;
     const bool leader = (threadIdx.x == 128);
     const float scale = (P.mode == 1 && k.nv > 0) ? (*g.dloss) / (float)k.nv : 0.f;

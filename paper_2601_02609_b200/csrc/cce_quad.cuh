@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(QTHREADS, 1)
     e.rit = e.q * 32 + lane;
     e.rank = pr;  // the pair epilogues index rows by the rank within the pair
     e.xchg = xchg;
+    e.xz = reinterpret_cast<float*>(stage_base);  // forward items never use the store staging
     e.stage = stage_base + (warp - 4) * 4096;
     const bool leader = (threadIdx.x == 128);
     const float scale = (P.mode == 1 && k.nv > 0) ? (*g.dloss) / (float)k.nv : 0.f;

@@ -26,12 +26,13 @@ def rel_fro(got, want):
     return float(np.linalg.norm(got - want) / nw)
 
 
-def run_gpu(H, W, y, dloss=1.0, handle=None, vocab_total=None, flags=0):
+def run_gpu(H, W, y, dloss=1.0, handle=None, vocab_total=None, flags=0, label_smoothing=0.0, z_loss=0.0):
     """Forward + backward through the C ABI. Returns numpy results."""
     import torch
     import paper_2601_02609_b200 as cce
     dev = H.device
-    h = handle or cce.CCEHandle(vocab_total=vocab_total or W.shape[0], flags=flags)
+    h = handle or cce.CCEHandle(vocab_total=vocab_total or W.shape[0], flags=flags, label_smoothing=label_smoothing,
+                                z_loss=z_loss)
     loss, lse, nv = h.forward(H, W, y)
     dH = torch.empty(H.shape, dtype=torch.bfloat16, device=dev)
     dW = torch.empty(W.shape, dtype=torch.bfloat16, device=dev)

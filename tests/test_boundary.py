@@ -63,6 +63,12 @@ def test_host_validation_without_gpu(lib):
     cfg.vocab_total = 1000
     cfg.world = 2                                                       # world > 1 without a comm
     assert lib.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 1
+    cfg.world = 1
+    assert cfg.label_smoothing == 0.0 and cfg.z_loss == 0.0                # regularisers off by default
+    for ls, zl in ((1.0, 0.0), (-0.1, 0.0), (0.0, -1e-4), (float("nan"), 0.0), (0.0, float("inf"))):
+        cfg.label_smoothing, cfg.z_loss = ls, zl
+        assert lib.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 1    # eps in [0, 1), lambda >= 0 finite
+    cfg.label_smoothing, cfg.z_loss = 0.0, 0.0
     assert lib.cce_forward(None, None, 0, 64, 64, None, 0, 64, None, None, None, None, None, 0, None) == 1
     assert lib.cce_backward(None, None, None, None, None) == 1
     assert lib.cce_workspace_bytes(None, 10, 64, 10) == 0

@@ -19,10 +19,10 @@ def dev():
     return torch.device("cuda:0")
 
 
-def _check(p, dev, dloss=1.0, flags=0):
+def _check(p, dev, dloss=1.0, flags=0, label_smoothing=0.0, z_loss=0.0):
     H, W, y = to_dev(p, dev)
-    got = run_gpu(H, W, y, dloss=dloss, flags=flags)
-    ref = oracle.cce(p["H"], p["W"], p["labels"], dloss=dloss)
+    got = run_gpu(H, W, y, dloss=dloss, flags=flags, label_smoothing=label_smoothing, z_loss=z_loss)
+    ref = oracle.cce(p["H"], p["W"], p["labels"], dloss=dloss, label_smoothing=label_smoothing, z_loss=z_loss)
     assert_parity(got, ref, p["labels"])
     return got, ref
 
@@ -61,6 +61,38 @@ def test_large_hidden_sizes(dev, N, D, V, ign):
     of 256, i.e. 4 / 7 / 8 quad items per dW / dH row or vocabulary tile)."""
     p = workload.make_problem(N, D, V, seed=D + V, ignore=ign)
     _check(p, dev)
+
+
+@pytest.mark.parametrize("eps,lam", [(0.1, 0.0), (0.0, 1e-4), (0.1, 1e-4), (0.3, 1e-2)])
+@pytest.mark.parametrize("N,D,V,ign,flags", [
+    (700, 128, 3000, "bern40", 0),       # ragged rows / vocabulary
+    (384, 896, 9000, "bern40", 0),       # Qwen hidden size, 2 chunks
+    (1000, 128, 41000, "bern40", 0),     # 6 chunks
+    (384, 896, 9000, "bern40", 32),      # quad kernels share the epilogues
+])
+def test_label_smoothing_and_z_loss(dev, N, D, V, ign, flags, eps, lam):
+    """the regularised loss (Def. Smoothed CE P:266-276, Def. Z-Loss
+    P:281-287) against oracle_cce_reg, same tolerances as the plain loss."""
+    p = workload.make_problem(N, D, V, seed=N + V + 1, ignore=ign)
+    _check(p, dev, flags=flags, label_smoothing=eps, z_loss=lam)
+
+
+@pytest.mark.parametrize("regime", ["peaked", "zero"])
+def test_label_smoothing_and_z_loss_regimes(dev, regime):
+    """W = 0 (loss = ln V + lam ln^2 V exactly) and confident targets."""
+    p = workload.make_problem(300, 128, 5000, seed=17, ignore="bern40", regime=regime)
+    _check(p, dev, label_smoothing=0.1, z_loss=1e-3)
+
+
+def test_regularised_loss_rejected_by_one_cta_kernels(dev):
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(100, 64, 500, seed=12, ignore="bern10")
+    H, W, y = to_dev(p, dev)
+    h = cce.CCEHandle(vocab_total=500, flags=cce.FLAG_ONE_CTA, label_smoothing=0.1)
+    with pytest.raises(cce.CCEError) as ei:
+        h.forward(H, W, y)
+    assert ei.value.status == 2     # CCE_ERR_UNSUPPORTED
+    h.close()
 
 
 @pytest.mark.parametrize("regime", ["peaked", "extreme", "zero"])
