@@ -196,8 +196,8 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   int64_t Npad, Tv, C;
   int64_t n_chunks, sched_ints;
-  size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32, sched,
-      total;
+  size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32,
+      sched, total;
 };
 
 Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots) {

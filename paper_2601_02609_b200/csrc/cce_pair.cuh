@@ -560,7 +560,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           const uint32_t fb = full_leader0 + stage * 8;
           // the leader arms its full barrier with BOTH CTAs' bytes; the peer's TMA only
           // signals completion bytes there (no per-stage remote arrive / release fence)
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
+          // debug bits 32768 / 65536: load only A / only B of DW and DH items (the other
+          // operand stays stale in SMEM; garbage results, isolates one operand's cost)
+          const bool skipB = (P.strict & 32768) && (it.type == PT_DW || it.type == PT_DH);
+          const bool skipA = (P.strict & 65536) && (it.type == PT_DW || it.type == PT_DH);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * ((skipA ? 0 : PA_BYTES) + (skipB ? 0 : b_bytes)));
           if (P.trace && rank == 0) t_issue[stage] = clock64();
           // L2 prefetch `prefetch` k-blocks ahead of this load (hides HBM latency beyond
           // the 6-stage SMEM ring; no SMEM or barrier involved)
@@ -584,15 +588,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
             tma_load_2d_pair_hint(&tmHcK, fb, a, kb * BK, it.m0 + hr, pol_keep);
             tma_load_2d_pair_hint(&tmWK, fb, b, kb * BK, it.n0 + hn, pol_keep);
           } else if (it.type == PT_DW) {
+            if (!skipA) {
 #pragma unroll
-            for (int j = 0; j < HM / 64; ++j)
-              tma_load_3d_pair_hint(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j, pol_g);
-            for (int j = 0; j < it.N / 2 / 64; ++j)
-              tma_load_2d_pair_hint(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK, pol_keep);
+              for (int j = 0; j < HM / 64; ++j)
+                tma_load_3d_pair_hint(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j, pol_g);
+            }
+            if (!skipB)
+              for (int j = 0; j < it.N / 2 / 64; ++j)
+                tma_load_2d_pair_hint(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK, pol_keep);
           } else {  // PT_DH
-            tma_load_3d_pair_hint(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb, pol_g);
-            for (int j = 0; j < it.N / 2 / 64; ++j)
-              tma_load_2d_pair_hint(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK, pol_keep);
+            if (!skipA) tma_load_3d_pair_hint(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb, pol_g);
+            if (!skipB)
+              for (int j = 0; j < it.N / 2 / 64; ++j)
+                tma_load_2d_pair_hint(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK, pol_keep);
           }
           if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
         }
@@ -692,7 +700,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       } else if (it.type == PT_G) {
         if (!(P.strict & 32)) epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
       } else if (it.type == PT_DW) {
-        epi_dw(g, taddr, e, it, have_acc);
+        if (!(P.strict & 16384)) epi_dw(g, taddr, e, it, have_acc);  // debug: skip the dW stores
       } else {
         // DH(c-1, tile) halves published; re-acquire so the .cg loads below see them
         if (leader && !(P.strict & 1792)) wait_ge(&dh_flag[it.tile_id], 2 * it.c);

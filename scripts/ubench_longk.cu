@@ -17,8 +17,10 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static PFN_encodeTiled enc;
-static void mk(CUtensorMap* m, void* p, uint64_t cols, uint64_t rows, uint32_t box_rows) {
-  cuuint64_t d[2] = {cols, rows}, s[1] = {cols * 2};
+static uint64_t g_ldb = 0;
+static int g_rot = 0;       // rotate each pair's k-loop start (desynchronises operand sharing)  // row stride (elements) override for the MN-major B map
+static void mk(CUtensorMap* m, void* p, uint64_t cols, uint64_t rows, uint32_t box_rows, uint64_t ld = 0) {
+  cuuint64_t d[2] = {cols, rows}, s[1] = {(ld ? ld : cols) * 2};
   cuuint32_t b[2] = {64, box_rows}, e[2] = {1, 1};
   enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p, d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -31,7 +33,7 @@ template <int WIDE, int MN = 0>
 __global__ void __launch_bounds__(256, 1) klk(const __grid_constant__ CUtensorMap ta,
                                               const __grid_constant__ CUtensorMap tb, int K, int tiles_v,
                                               int tiles_d, __nv_bfloat16* C, int ldc, unsigned long long* out,
-                                              int epi_mode, const __grid_constant__ CUtensorMap tc) {
+                                              int epi_mode, const __grid_constant__ CUtensorMap tc, int rot) {
   constexpr int ST = WIDE ? 4 : 6;
   constexpr int NB = WIDE ? 2 : 1;                 // B boxes (N = 256 halves) per stage
   constexpr int STAGE = 16384 * (1 + NB);
@@ -61,7 +63,8 @@ __global__ void __launch_bounds__(256, 1) klk(const __grid_constant__ CUtensorMa
     const uint32_t fb0 = mapa_shared(smem_u32(&full[0]), 0);
     for (int x = unit; x < items; x += nunits) {
       const int vt = x / (tiles_d / dt_per), d0 = (x % (tiles_d / dt_per)) * dt_per;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb_ = 0; kb_ < num_kb; ++kb_) {
+        const int kb = rot ? (kb_ + unit * 13) % num_kb : kb_;
         mbar_wait(&empty[st], ph ^ 1);
         if (rank == 0) mbar_arrive_expect_tx(&full[st], 2 * STAGE);
         uint8_t* s = smem + st * STAGE;
@@ -241,7 +244,7 @@ void run(void* A, void* B, __nv_bfloat16* C, int MV, int ND, int K, int epi_mode
   CUtensorMap ta, tb;
   if (MN) {
     mk(&ta, A, MV, K, 64);
-    mk(&tb, B, ND, K, 64);
+    mk(&tb, B, ND, K, 64, g_ldb);
   } else {
     mk(&ta, A, K, MV, 128);
     mk(&tb, B, K, ND, 128);
@@ -276,7 +279,7 @@ void run(void* A, void* B, __nv_bfloat16* C, int MV, int ND, int K, int epi_mode
   cudaEventCreate(&e1);
   for (int r = 0; r < 3; ++r) {
     cudaEventRecord(e0);
-    cudaLaunchKernelEx(&cfg, k, ta, tb, K, MV / 256, ND / 256, C, ND, d, epi_mode, tcm);
+    cudaLaunchKernelEx(&cfg, k, ta, tb, K, MV / 256, ND / 256, C, ND, d, epi_mode, tcm, g_rot);
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms = 0;
@@ -308,18 +311,11 @@ int main() {
   fill_random<<<1024, 256>>>((uint16_t*)A, (size_t)MV * K, 1);
   fill_random<<<1024, 256>>>((uint16_t*)B, (size_t)ND * K, 2);
   cudaDeviceSynchronize();
-  // short-K items shaped like the forward / G items: A = rows (Hc, 5120 x 896), B = vocabulary
-  // rows (W, 151552 x 896), K = 896: 14 k-blocks per 256 x 256 tile
-  void *Hc, *Wv;
-  cudaMalloc(&Hc, (size_t)5120 * 896 * 2);
-  cudaMalloc(&Wv, (size_t)151552 * 896 * 2);
-  fill_random<<<1024, 256>>>((uint16_t*)Hc, (size_t)5120 * 896, 3);
-  fill_random<<<1024, 256>>>((uint16_t*)Wv, (size_t)151552 * 896, 4);
-  cudaDeviceSynchronize();
-  // tiles: v = row tile (20), d = vocabulary tile (592): vocabulary-inner here
-  run<0>(Wv, Hc, C, 151552, 5120, 896, 0);
-  run<0>(Wv, Hc, C, 151552, 5120, 896, 1);
-  run<0>(Wv, Hc, C, 151552, 5120, 896, 2);
-  run<0>(Wv, Hc, C, 151552, 5120, 896, 3);
+  // desynchronised operand sharing: each pair starts its k-loop at a different k-block
+  run<0, 1>(A, B, C, MV, 1024, K, 0);
+  g_rot = 1;
+  run<0, 1>(A, B, C, MV, 1024, K, 0);
+  run<0>(A, B, C, MV, 1024, K, 0);
+  g_rot = 0;
   return 0;
 }
