@@ -317,8 +317,8 @@ __device__ __forceinline__ void epi_dw(const GemmParams& p, uint32_t taddr, cons
       uint4* dst = reinterpret_cast<uint4*>(p.dW + (size_t)(c0 + vrow) * p.D + d0);
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4)
-        __stcs(dst + q4, make_uint4(pack_bf16(v[8 * q4], v[8 * q4 + 1]), pack_bf16(v[8 * q4 + 2], v[8 * q4 + 3]),
-                             pack_bf16(v[8 * q4 + 4], v[8 * q4 + 5]), pack_bf16(v[8 * q4 + 6], v[8 * q4 + 7])));
+        dst[q4] = make_uint4(pack_bf16(v[8 * q4], v[8 * q4 + 1]), pack_bf16(v[8 * q4 + 2], v[8 * q4 + 3]),
+                             pack_bf16(v[8 * q4 + 4], v[8 * q4 + 5]), pack_bf16(v[8 * q4 + 6], v[8 * q4 + 7]));
     }
   }
 }
@@ -397,15 +397,13 @@ __device__ __forceinline__ void epi_dh_tma(const CUtensorMap* tmDH, uint32_t tad
 template <bool A_MN, bool B_MN>
 __device__ __forceinline__ void mma_item(const PItem& it, uint64_t* full_bar, uint64_t* empty_bar, uint32_t a_base,
                                          uint32_t b_base, uint32_t tmem_d, uint32_t& stage, uint32_t& phase,
-                                         unsigned long long* wait_ns, volatile unsigned long long* t_issue,
-                                         unsigned long long* lat_sum) {
+                                         unsigned long long* wait_ns) {
   const uint32_t idesc = idesc_bf16_f32(PM, it.N, A_MN ? 1 : 0, B_MN ? 1 : 0);
   for (int kb = 0; kb < it.num_kb; ++kb) {
     if (wait_ns) {
       const unsigned long long w0 = gtimer();
       mbar_wait(&full_bar[stage], phase);
       *wait_ns += gtimer() - w0;
-      *lat_sum += clock64() - t_issue[stage];  // issue -> data landed (upper bound when not waiting)
     }
     mbar_wait(&full_bar[stage], phase);
     tc_fence_after();
@@ -443,9 +441,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   uint64_t* rempty_p = rempty_l + PRING;    // leader: peer consumers (producer + epilogue warps)
   PItem* ring = reinterpret_cast<PItem*>(rempty_p + PRING);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + PRING);
-  // trace only: clock64 at which the leader's producer issued each stage's loads
-  volatile unsigned long long* t_issue =
-      reinterpret_cast<volatile unsigned long long*>(smem + PSTAGES * PSTAGE_BYTES + 512);
   float* xchg = reinterpret_cast<float*>(smem + PSTAGES * PSTAGE_BYTES + 1024);
   uint8_t* stage_base = smem + PSTAGES * PSTAGE_BYTES + 2048;
 
@@ -517,7 +512,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       // ===== TMA producer (both CTAs): next item from the local ring, dependencies, loads
       uint32_t stage = 0, phase = 0, rs = 0, rph = 0;
       const uint32_t full_leader0 = mapa_shared(smem_u32(&full_bar[0]), 0);
-      const bool hints = P.mode == 1 && !(P.strict & 2048);
+      // debug bit 262144: L2 cache-policy hints on the backward's loads (measured: no gain;
+      // off by default -- the hinted instruction form itself cost ~2% in an A/B)
+      const bool hints = P.mode == 1 && (P.strict & 262144);
       const uint64_t pol_keep = hints ? policy_evict_last() : policy_evict_normal();
       const uint64_t pol_g = (P.strict & 4096) ? policy_evict_first() : policy_evict_normal();
       while (true) {
@@ -560,12 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           const uint32_t fb = full_leader0 + stage * 8;
           // the leader arms its full barrier with BOTH CTAs' bytes; the peer's TMA only
           // signals completion bytes there (no per-stage remote arrive / release fence)
-          // debug bits 32768 / 65536: load only A / only B of DW and DH items (the other
-          // operand stays stale in SMEM; garbage results, isolates one operand's cost)
-          const bool skipB = (P.strict & 32768) && (it.type == PT_DW || it.type == PT_DH);
-          const bool skipA = (P.strict & 65536) && (it.type == PT_DW || it.type == PT_DH);
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * ((skipA ? 0 : PA_BYTES) + (skipB ? 0 : b_bytes)));
-          if (P.trace && rank == 0) t_issue[stage] = clock64();
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
           // L2 prefetch `prefetch` k-blocks ahead of this load (hides HBM latency beyond
           // the 6-stage SMEM ring; no SMEM or barrier involved)
           const int pk = kb + P.prefetch;
@@ -585,22 +577,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           // L2 policies (backward): the reused operands (Hc, the W chunk) evict_last, the
           // dlogits ring per pol_g (debug bits 2048 / 4096 switch the hints off / G to evict_first)
           if (it.type == PT_FWD || it.type == PT_G) {
-            tma_load_2d_pair_hint(&tmHcK, fb, a, kb * BK, it.m0 + hr, pol_keep);
-            tma_load_2d_pair_hint(&tmWK, fb, b, kb * BK, it.n0 + hn, pol_keep);
-          } else if (it.type == PT_DW) {
-            if (!skipA) {
-#pragma unroll
-              for (int j = 0; j < HM / 64; ++j)
-                tma_load_3d_pair_hint(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j, pol_g);
+            if (hints) {
+              tma_load_2d_pair_hint(&tmHcK, fb, a, kb * BK, it.m0 + hr, pol_keep);
+              tma_load_2d_pair_hint(&tmWK, fb, b, kb * BK, it.n0 + hn, pol_keep);
+            } else {
+              tma_load_2d_pair(&tmHcK, fb, a, kb * BK, it.m0 + hr);
+              tma_load_2d_pair(&tmWK, fb, b, kb * BK, it.n0 + hn);
             }
-            if (!skipB)
-              for (int j = 0; j < it.N / 2 / 64; ++j)
-                tma_load_2d_pair_hint(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK, pol_keep);
+          } else if (it.type == PT_DW) {
+#pragma unroll
+            for (int j = 0; j < HM / 64; ++j) {
+              if (hints)
+                tma_load_3d_pair_hint(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j, pol_g);
+              else
+                tma_load_3d_pair(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j);
+            }
+            for (int j = 0; j < it.N / 2 / 64; ++j) {
+                if (hints) tma_load_2d_pair_hint(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK, pol_keep);
+                else tma_load_2d_pair(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK);
+              }
           } else {  // PT_DH
-            if (!skipA) tma_load_3d_pair_hint(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb, pol_g);
-            if (!skipB)
-              for (int j = 0; j < it.N / 2 / 64; ++j)
-                tma_load_2d_pair_hint(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK, pol_keep);
+            if (hints) tma_load_3d_pair_hint(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb, pol_g);
+            else tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb);
+            for (int j = 0; j < it.N / 2 / 64; ++j) {
+                if (hints) tma_load_2d_pair_hint(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK, pol_keep);
+                else tma_load_2d_pair(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK);
+              }
           }
           if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
         }
@@ -632,14 +634,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         const uint32_t tmem_d = tmem_base + acc * PN;
         const unsigned long long tm0 = P.trace ? gtimer() : 0ull;
         const unsigned long long cm0 = P.trace ? clock64() : 0ull;
-        unsigned long long fw = 0, lat = 0;
+        unsigned long long fw = 0;
         unsigned long long* fwp = P.trace ? &fw : nullptr;
         if (it.type == PT_DW)
-          mma_item<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp, t_issue, &lat);
+          mma_item<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
         else if (it.type == PT_DH)
-          mma_item<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp, t_issue, &lat);
+          mma_item<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
         else
-          mma_item<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp, t_issue, &lat);
+          mma_item<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
         if (elect_one()) umma_commit_pair(&tfull_bar[acc]);
         __syncwarp();
         if (P.trace && lane == 0 && it.q < P.trace_cap) {
@@ -647,7 +649,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           P.trace[it.q].t_mma1 = gtimer();
           P.trace[it.q].t_full_wait = fw;
           P.trace[it.q].r0 = clock64() - cm0;
-          P.trace[it.q].r2 = lat;
         }
       }
     }
@@ -700,13 +701,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       } else if (it.type == PT_G) {
         if (!(P.strict & 32)) epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
       } else if (it.type == PT_DW) {
-        if (!(P.strict & 16384)) epi_dw(g, taddr, e, it, have_acc);  // debug: skip the dW stores
+        epi_dw(g, taddr, e, it, have_acc);
       } else {
         // DH(c-1, tile) halves published; re-acquire so the .cg loads below see them
         if (leader && !(P.strict & 1792)) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
         named_bar_sync(2, PEPI_THREADS);
         fence_proxy_async_global();  // the acquired flag orders the TMA reduce below
-        if (!(P.strict & 64)) epi_dh_tma(&tmDH, taddr, e, it);
+        if (P.strict & 524288) epi_dh(g, taddr, e, it, k.nv);  // debug: the load-add-store epilogue
+        else if (!(P.strict & 64)) epi_dh_tma(&tmDH, taddr, e, it);
       }
       if (have_acc) {
         tc_fence_before();

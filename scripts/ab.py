@@ -54,18 +54,38 @@ def main():
     stream = torch.cuda.current_stream()
 
     vs = []
+    libs = {}
+    main_lib = cce.lib()
     for spec in args.variants:
+        spec, _, libpath = spec.partition("@")   # optional: another build of libcce.so
         name, rest = spec.split("=", 1)
         flags, _, envs = rest.partition(":")
         env = dict(kv.split("=", 1) for kv in envs.split(",") if kv)
         vs.append((name, int(flags), env))
+        if libpath:
+            saved = cce.LIB_PATH
+            cce.LIB_PATH, cce._lib = libpath, None
+            libs[name] = cce.lib()
+            cce.LIB_PATH, cce._lib = saved, main_lib
+        else:
+            libs[name] = main_lib
 
     handles = {}
     for name, flags, env in vs:
+        cce._lib = libs[name]
         old = {k: os.environ.get(k) for k in env}
         os.environ.update(env)
         h = cce.CCEHandle(vocab_total=c.V, flags=flags)
-        ws = h.workspace(c.N, c.D, c.V, dev)
+        # WSOFF=<bytes>: place the workspace at this offset from a 2 MiB-aligned base
+        off = int(env.get("WSOFF", "-1"))
+        if off >= 0:
+            need = cce.cce_workspace_bytes(h.h, c.N, c.D, c.V)
+            raw = torch.empty(need + off + (4 << 20), dtype=torch.uint8, device=dev)
+            base = (-raw.data_ptr()) % (2 << 20)
+            ws = raw[base + off: base + off + need]
+            h._ws_keep = raw
+        else:
+            ws = h.workspace(c.N, c.D, c.V, dev)
         cce.cce_forward(h.h, H, W, y, loss, lse, nvt, ws, stream)
         cce.cce_backward(h.h, one, dH, dW, stream)
         torch.cuda.synchronize()
@@ -79,9 +99,14 @@ def main():
     from bench import ClockSampler
     import time
     res = {name: {"step": [], "fwd": [], "bwd": [], "mhz": []} for name, _, _ in vs}
+    import random
+    rng = random.Random(1234)
     for r in range(args.rounds):
-        for name, _, _ in vs:
+        order = list(vs)
+        rng.shuffle(order)          # no position bias from the GPU's thermal / power drift
+        for name, _, _ in order:
             h, ws = handles[name]
+            cce._lib = libs[name]
             time.sleep(args.rest)
             smp = ClockSampler(0, period_ms=args.sample_ms)
             smp.start()
@@ -109,7 +134,8 @@ def main():
         d = res[name]
         print(f"{name:24s} step {statistics.median(d['step']):7.3f} ms  fwd {statistics.median(d['fwd']):7.3f}"
               f"  bwd {statistics.median(d['bwd']):7.3f}  (min step {min(d['step']):.3f})  sm MHz {d['mhz']}", flush=True)
-    for h, _ in handles.values():
+    for name, (h, _) in handles.items():
+        cce._lib = libs[name]
         h.close()
 
 

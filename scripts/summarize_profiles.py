@@ -24,6 +24,8 @@ METRICS = [
     "lts__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",
     "launch__cluster_dim_x", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "derived__lts__lts2xbar_bytes.sum.per_second", "l1tex__m_xbar2l1tex_read_bytes.sum",
+    "lts__t_sectors_srcunit_ltcfabric.sum", "l1tex__data_bank_reads.avg.pct_of_peak_sustained_elapsed",
 ]
 
 

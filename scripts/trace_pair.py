@@ -9,6 +9,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_2601_02609_b200 as cce  # noqa: E402
+
+if os.environ.get("CCE_LIB"):  # trace another build of libcce.so
+    cce.LIB_PATH = os.environ["CCE_LIB"]
 import workload  # noqa: E402
 from cce_testutil import to_dev  # noqa: E402
 

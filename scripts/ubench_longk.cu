@@ -312,10 +312,11 @@ int main() {
   fill_random<<<1024, 256>>>((uint16_t*)B, (size_t)ND * K, 2);
   cudaDeviceSynchronize();
   // desynchronised operand sharing: each pair starts its k-loop at a different k-block
-  run<0, 1>(A, B, C, MV, 1024, K, 0);
   g_rot = 1;
   run<0, 1>(A, B, C, MV, 1024, K, 0);
+  run<1, 1>(A, B, C, MV, 1024, K, 0);
   run<0>(A, B, C, MV, 1024, K, 0);
+  run<1>(A, B, C, MV, 1024, K, 0);
   g_rot = 0;
   return 0;
 }
