@@ -57,6 +57,8 @@ def lib():
         L.oracle_dlogits.argtypes = [p, p, p, i64, i64, i64, i32, f64, p]
         L.oracle_dlogits.restype = ctypes.c_int
         L.oracle_cce_reg.argtypes = [p, p, p, i64, i64, i64, i32, f64, f64, f64, p, p, p, p, p]
+        L.oracle_cce_full.argtypes = [p, p, p, i64, i64, i64, i32, f64, f64, ctypes.c_int, f64, p, p, p, p, p, p]
+        L.oracle_cce_full.restype = ctypes.c_int
         L.oracle_cce_reg.restype = ctypes.c_int
         L.oracle_dlogits_reg.argtypes = [p, p, p, i64, i64, i64, i32, f64, f64, f64, p]
         L.oracle_dlogits_reg.restype = ctypes.c_int
@@ -101,22 +103,32 @@ def num_threads() -> int:
     return int(lib().oracle_num_threads())
 
 
-def cce(H_bits, W_bits, labels, ignore_index=-100, dloss=1.0, grads=True, label_smoothing=0.0, z_loss=0.0):
+def cce(H_bits, W_bits, labels, ignore_index=-100, dloss=1.0, grads=True, label_smoothing=0.0, z_loss=0.0,
+        reduction="mean"):
     """Full forward+backward.  Returns dict(loss, lse[N], n_valid, dH[N,D], dW[V,D]) in fp64.
-    label_smoothing (eps) and z_loss (lambda) follow oracle_cce_reg."""
+    label_smoothing (eps) and z_loss (lambda) follow oracle_cce_reg.
+    reduction "mean" | "sum" | "none"; with "none" loss is the [N] per-row array and
+    dloss an [N] array of upstream gradients."""
     H = _bits(H_bits); W = _bits(W_bits)
     y = np.ascontiguousarray(labels, dtype=np.int32)
     N, D = H.shape
     V = W.shape[0]
     assert W.shape[1] == D and y.shape == (N,)
-    loss = np.zeros(1, np.float64)
+    red = {"mean": 0, "sum": 1, "none": 2}[reduction]
+    loss = np.zeros(N if red == 2 else 1, np.float64)
     lse = np.zeros(N, np.float64)
     nv = np.zeros(1, np.int64)
     dH = np.zeros((N, D), np.float64) if grads else None
     dW = np.zeros((V, D), np.float64) if grads else None
-    _check(lib().oracle_cce_reg(_ptr(H), _ptr(W), _ptr(y), N, D, V, ignore_index, float(label_smoothing),
-                                float(z_loss), float(dloss), _ptr(loss), _ptr(lse), _ptr(nv), _ptr(dH), _ptr(dW)))
-    return {"loss": float(loss[0]), "lse": lse, "n_valid": int(nv[0]), "dH": dH, "dW": dW}
+    if red == 2:
+        drows = np.ascontiguousarray(np.broadcast_to(np.asarray(dloss, np.float64), (N,)))
+        dscal = 0.0
+    else:
+        drows, dscal = None, float(dloss)
+    _check(lib().oracle_cce_full(_ptr(H), _ptr(W), _ptr(y), N, D, V, ignore_index, float(label_smoothing),
+                                 float(z_loss), red, dscal, _ptr(drows), _ptr(loss), _ptr(lse), _ptr(nv), _ptr(dH),
+                                 _ptr(dW)))
+    return {"loss": loss if red == 2 else float(loss[0]), "lse": lse, "n_valid": int(nv[0]), "dH": dH, "dW": dW}
 
 
 def dlogits(H_bits, W_bits, labels, ignore_index=-100, dloss=1.0, label_smoothing=0.0, z_loss=0.0):

@@ -112,19 +112,31 @@ static double row_grad(double zv, double lse, int is_target, double eps, double 
     return (1.0 - eps) * ce + eps * uni + zl;
 }
 
-int oracle_cce_reg(const double *H, const double *W, const int32_t *labels,
-                   int64_t N, int64_t D, int64_t V, int32_t ignore_index,
-                   double eps, double lam,
-                   double dloss, double *loss, double *lse, int64_t *n_valid,
-                   double *dH, double *dW) {
-    if (N < 0 || D <= 0 || V <= 0) return ORACLE_ERR_INVALID;
+/*
+ * reduction: 0 = mean over valid rows, 1 = sum, 2 = none.
+ * The upstream gradient of row n's loss is dloss / n_valid (mean), dloss (sum) or
+ * dloss_rows[n] (none); with "none" *loss receives the [N] per-row losses (0 for
+ * ignored rows).
+ */
+int oracle_cce_full(const double *H, const double *W, const int32_t *labels,
+                    int64_t N, int64_t D, int64_t V, int32_t ignore_index,
+                    double eps, double lam, int reduction,
+                    double dloss, const double *dloss_rows,
+                    double *loss, double *lse, int64_t *n_valid,
+                    double *dH, double *dW) {
+    if (N < 0 || D <= 0 || V <= 0 || reduction < 0 || reduction > 2) return ORACLE_ERR_INVALID;
+    if (reduction == 2 && !dloss_rows && (dH || dW)) return ORACLE_ERR_INVALID;
     int64_t nv = 0;
     int rc = oracle_validate(labels, N, V, ignore_index, &nv);
     if (rc) return rc;
     *n_valid = nv;
-    double scale = nv > 0 ? dloss / (double)nv : 0.0;   /* reading R6 */
     double *row_loss = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
-    if (!row_loss) return ORACLE_ERR_NOMEM;
+    double *rscale = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
+    if (!row_loss || !rscale) { free(row_loss); free(rscale); return ORACLE_ERR_NOMEM; }
+    for (int64_t n = 0; n < N; ++n) {                   /* reading R6 */
+        if (labels[n] == ignore_index) continue;
+        rscale[n] = reduction == 0 ? dloss / (double)nv : (reduction == 1 ? dloss : (dloss_rows ? dloss_rows[n] : 0.0));
+    }
     int nomem = 0;
 
     /* Pass 1, parallel over rows: materialise z, lse, l_n, G row, dH row. */
@@ -156,7 +168,7 @@ int oracle_cce_reg(const double *H, const double *W, const int32_t *labels,
                 double *out = dH + n * D;
                 for (int64_t d = 0; d < D; ++d) out[d] = 0.0;
                 for (int64_t v = 0; v < V; ++v) {
-                    double g = scale * row_grad(z[v], l, v == y, eps, lam, V);
+                    double g = rscale[n] * row_grad(z[v], l, v == y, eps, lam, V);
                     const double *w = W + v * D;
                     for (int64_t d = 0; d < D; ++d) out[d] += g * w[d];
                 }
@@ -165,12 +177,16 @@ int oracle_cce_reg(const double *H, const double *W, const int32_t *labels,
         free(h);
         free(z);
     }
-    if (nomem) { free(row_loss); return ORACLE_ERR_NOMEM; }
+    if (nomem) { free(row_loss); free(rscale); return ORACLE_ERR_NOMEM; }
 
-    /* Mean over valid rows, summed in row order. */
-    double acc = 0.0;
-    for (int64_t n = 0; n < N; ++n) if (labels[n] != ignore_index) acc += row_loss[n];
-    *loss = nv > 0 ? acc / (double)nv : 0.0;
+    /* Mean / sum over valid rows, summed in row order; or the rows themselves. */
+    if (reduction == 2) {
+        for (int64_t n = 0; n < N; ++n) loss[n] = labels[n] != ignore_index ? row_loss[n] : 0.0;
+    } else {
+        double acc = 0.0;
+        for (int64_t n = 0; n < N; ++n) if (labels[n] != ignore_index) acc += row_loss[n];
+        *loss = reduction == 1 ? acc : (nv > 0 ? acc / (double)nv : 0.0);
+    }
     free(row_loss);
 
     /* Pass 2, parallel over vocabulary rows: recompute z[n,v], G[n,v], dW[v,:]. */
@@ -186,12 +202,22 @@ int oracle_cce_reg(const double *H, const double *W, const int32_t *labels,
                 const double *hr = H + n * D;
                 double zv = 0.0;
                 for (int64_t d = 0; d < D; ++d) zv += hr[d] * w[d];
-                double g = scale * row_grad(zv, lse[n], v == y, eps, lam, V);
+                double g = rscale[n] * row_grad(zv, lse[n], v == y, eps, lam, V);
                 for (int64_t d = 0; d < D; ++d) out[d] += g * hr[d];
             }
         }
     }
+    free(rscale);
     return ORACLE_OK;
+}
+
+int oracle_cce_reg(const double *H, const double *W, const int32_t *labels,
+                   int64_t N, int64_t D, int64_t V, int32_t ignore_index,
+                   double eps, double lam,
+                   double dloss, double *loss, double *lse, int64_t *n_valid,
+                   double *dH, double *dW) {
+    return oracle_cce_full(H, W, labels, N, D, V, ignore_index, eps, lam, 0, dloss, NULL, loss, lse, n_valid,
+                           dH, dW);
 }
 
 /* The unregularised loss (eps = lam = 0). */

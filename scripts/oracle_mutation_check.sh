@@ -18,6 +18,9 @@ muts=(
  's/double uni = p - 1.0 \/ (double)V;/double uni = p - 1.0 \/ (double)(V - 1);/'  # wrong uniform mass
  's/eps \* (l - zsum \/ (double)V)/eps * (l - zsum \/ (double)(V + 1))/'  # wrong mean of logits
  's/double zl = 2.0 \* lam \* lse \* p;/double zl = lam * lse * p;/'  # dropped factor 2
+ 's/(reduction == 1 ? dloss : (dloss_rows ? dloss_rows\[n\]/(reduction == 1 ? dloss \/ (double)nv : (dloss_rows ? dloss_rows[n]/'  # sum divided by n_valid
+ 's/(dloss_rows ? dloss_rows\[n\] : 0.0)/(dloss_rows ? dloss_rows[0] : 0.0)/'  # none: wrong row of dloss
+ 's/loss\[n\] = labels\[n\] != ignore_index ? row_loss\[n\] : 0.0;/loss[n] = labels[n] != ignore_index ? row_loss[n] \/ (double)nv : 0.0;/'  # none: per-row loss averaged
 )
 fail=0
 for m in "${muts[@]}"; do

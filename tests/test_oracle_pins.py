@@ -430,3 +430,36 @@ def test_regularised_row_sums_and_limits():
     a = oracle.cce(H, W, y)
     b = oracle.cce(H, W, y, label_smoothing=0.0, z_loss=0.0)
     assert a["loss"] == b["loss"] and np.array_equal(a["dH"], b["dH"]) and np.array_equal(a["dW"], b["dW"])
+
+
+# ---------------------------------------------------------------- reductions (NEXT #3)
+@pytest.mark.parametrize("reduction,eps,lam", [("sum", 0.0, 0.0), ("none", 0.0, 0.0), ("sum", 0.1, 1e-3),
+                                               ("none", 0.2, 5e-3)])
+def test_reductions_match_torch_fp64(reduction, eps, lam):
+    """Library routine: torch fp64 cross_entropy(reduction='sum'/'none', label_smoothing)
+    + lam lse^2 per valid row, autograd with per-row upstream gradients for 'none'."""
+    torch = pytest.importorskip("torch")
+    N, D, V = 18, 20, 401
+    H, W, y = _rand_problem(N, D, V, 500 + len(reduction) + int(eps * 10), ignore_n=4)
+    Ht = torch.tensor(H, requires_grad=True)
+    Wt = torch.tensor(W, requires_grad=True)
+    yt = torch.tensor(y, dtype=torch.long)
+    z = Ht @ Wt.T
+    valid = (yt != -100).double()
+    ce = torch.nn.functional.cross_entropy(z, yt, ignore_index=-100, label_smoothing=eps, reduction="none")
+    lse = torch.logsumexp(z, dim=1)
+    rows = (ce + lam * lse * lse) * valid
+    rng = np.random.default_rng(7)
+    if reduction == "sum":
+        lt = rows.sum()
+        lt.backward(torch.tensor(0.6, dtype=torch.float64))
+        r = oracle.cce(H, W, y, dloss=0.6, label_smoothing=eps, z_loss=lam, reduction="sum")
+        assert abs(r["loss"] - lt.item()) <= 1e-12
+    else:
+        g = rng.standard_normal(N)
+        rows.backward(torch.tensor(g))
+        r = oracle.cce(H, W, y, dloss=g, label_smoothing=eps, z_loss=lam, reduction="none")
+        np.testing.assert_allclose(r["loss"], rows.detach().numpy(), rtol=1e-12, atol=1e-14)
+        assert np.all(r["loss"][y == -100] == 0.0)
+    np.testing.assert_allclose(r["dH"], Ht.grad.numpy(), rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(r["dW"], Wt.grad.numpy(), rtol=1e-10, atol=1e-14)
