@@ -87,6 +87,19 @@ typedef enum {
 #define CCE_FLAG_QUAD 32u
 /* With CCE_FLAG_QUAD (or alone): quad kernels on the co-resident 4-CTA clusters only. */
 #define CCE_FLAG_QUAD_ONLY 16u
+/* Gradient modes (pair / quad kernels only, CCE_FLAG_ONE_CTA
+ * returns CCE_ERR_UNSUPPORTED): CCE_FLAG_GRAD_FP32 = dH and dW are float32 arrays;
+ * CCE_FLAG_ACCUMULATE = dH += gradient and dW += gradient (micro-batch accumulation
+ * into .grad, the paper's 4-8 step accumulation) instead of overwrite.
+ * Accumulation adds in fp32 and rounds once (bf16 outputs); ignored rows of dH are
+ * left untouched. */
+#define CCE_FLAG_GRAD_FP32 64u
+#define CCE_FLAG_ACCUMULATE 128u
+
+/* Reduction of the per-token losses (cce_config.reduction). */
+#define CCE_REDUCTION_MEAN 0  /* loss = sum_valid l_n / n_valid (default) */
+#define CCE_REDUCTION_SUM 1   /* loss = sum_valid l_n */
+#define CCE_REDUCTION_NONE 2  /* loss[n] = l_n per token (0 for ignored rows); dloss is [N] */
 
 typedef struct {
   int32_t ignore_index;   /* label value that marks a skipped row; -100 in the paper */
@@ -106,6 +119,10 @@ typedef struct {
    * CCE_FLAG_ONE_CTA a non-zero value makes cce_forward return CCE_ERR_UNSUPPORTED. */
   float label_smoothing;
   float z_loss;
+  /* CCE_REDUCTION_MEAN (default) / SUM / NONE.  With NONE, cce_forward's `loss` is an
+   * [N] float32 array and cce_backward's `dloss` an [N] float32 array (the upstream
+   * gradient of each token's loss); cce_step_host supports MEAN and SUM only. */
+  int32_t reduction;
 } cce_config;
 
 /* Fill `cfg` with defaults: ignore_index=-100, vocab_total=0 (must be set),
@@ -128,7 +145,9 @@ size_t cce_workspace_bytes(const cce_handle *h, int64_t N, int64_t D, int64_t V_
  *   H      [N, D] bf16, row stride ldh          (hidden states)
  *   W      [V_local, D] bf16, row stride ldw     (this rank's LM-head rows [off, off+V_local))
  *   labels [N] int32, global ids or ignore_index
- *   loss   device float scalar                   (mean over valid rows; 0 if none; NaN on label error)
+ *   loss   device float scalar                   (mean over valid rows; 0 if none; NaN on label error;
+ *                                                 the sum with CCE_REDUCTION_SUM; with CCE_REDUCTION_NONE
+ *                                                 an [N] array of per-token losses, 0 for ignored rows)
  *   lse    [N] device float, may be NULL         (global LSE; 0.0f for ignored rows)
  *   n_valid device int32 scalar, may be NULL     (number of non-ignored rows)
  * World > 1: every rank passes the same H/labels and its own W shard; loss
@@ -144,10 +163,13 @@ cce_status cce_forward(cce_handle *h,
 
 /*
  * Backward of the mean loss w.r.t. H and this rank's W shard.
- *   dloss  device float scalar, the upstream gradient of `loss`
- *   dH     [N, D] bf16 output, overwritten; ignored rows are written as 0
- *          (world > 1: the full dH, summed over ranks by NCCL all-reduce)
- *   dW     [V_local, D] bf16 output, overwritten (stays local to the rank)
+ *   dloss  device float scalar, the upstream gradient of `loss` ([N] array with
+ *          CCE_REDUCTION_NONE: the gradient of each token's loss)
+ *   dH     [N, D] bf16 output (float32 with CCE_FLAG_GRAD_FP32), overwritten; ignored
+ *          rows are written as 0 (with CCE_FLAG_ACCUMULATE: dH += gradient, ignored rows
+ *          untouched) (world > 1: the full dH, summed over ranks by NCCL all-reduce)
+ *   dW     [V_local, D] bf16 output (float32 with CCE_FLAG_GRAD_FP32), overwritten or,
+ *          with CCE_FLAG_ACCUMULATE, accumulated (stays local to the rank)
  * Uses the inputs and workspace saved by the last cce_forward on `h`.
  */
 cce_status cce_backward(cce_handle *h, const float *dloss, void *dH, void *dW, void *stream);

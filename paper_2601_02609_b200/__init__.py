@@ -37,6 +37,10 @@ FLAG_ONE_CTA = 4
 FLAG_PAIR = 8
 FLAG_QUAD_ONLY = 16
 FLAG_QUAD = 32
+FLAG_GRAD_FP32 = 64
+FLAG_ACCUMULATE = 128
+REDUCTION_MEAN, REDUCTION_SUM, REDUCTION_NONE = 0, 1, 2
+_REDUCTIONS = {"mean": REDUCTION_MEAN, "sum": REDUCTION_SUM, "none": REDUCTION_NONE}
 
 
 class CCEError(RuntimeError):
@@ -48,7 +52,8 @@ class CCEError(RuntimeError):
 class cce_config(ctypes.Structure):
     _fields_ = [("ignore_index", ctypes.c_int32), ("vocab_total", ctypes.c_int64), ("vocab_offset", ctypes.c_int64),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
-                ("flags", ctypes.c_uint32), ("label_smoothing", ctypes.c_float), ("z_loss", ctypes.c_float)]
+                ("flags", ctypes.c_uint32), ("label_smoothing", ctypes.c_float), ("z_loss", ctypes.c_float),
+                ("reduction", ctypes.c_int32)]
 
 
 _lib = None
@@ -121,7 +126,8 @@ def _stream(stream):
 
 # ----------------------------------------------------------------- C-ABI mirrors
 def cce_create(vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0, rank: int = 0, world: int = 1,
-               nccl_comm=None, flags: int = 0, label_smoothing: float = 0.0, z_loss: float = 0.0) -> ctypes.c_void_p:
+               nccl_comm=None, flags: int = 0, label_smoothing: float = 0.0, z_loss: float = 0.0,
+               reduction: int = REDUCTION_MEAN) -> ctypes.c_void_p:
     cfg = cce_config()
     lib().cce_config_default(ctypes.byref(cfg))
     cfg.ignore_index = ignore_index
@@ -133,6 +139,7 @@ def cce_create(vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0
     cfg.flags = flags
     cfg.label_smoothing = label_smoothing
     cfg.z_loss = z_loss
+    cfg.reduction = _REDUCTIONS.get(reduction, reduction) if isinstance(reduction, str) else reduction
     h = ctypes.c_void_p()
     _check(lib().cce_create(ctypes.byref(h), ctypes.byref(cfg)), "cce_create")
     return h
@@ -228,9 +235,11 @@ class CCEHandle:
     """A library handle plus a cached device workspace (torch-allocated)."""
 
     def __init__(self, vocab_total: int, ignore_index: int = -100, vocab_offset: int = 0, rank: int = 0,
-                 world: int = 1, nccl_comm=None, flags: int = 0, label_smoothing: float = 0.0, z_loss: float = 0.0):
+                 world: int = 1, nccl_comm=None, flags: int = 0, label_smoothing: float = 0.0, z_loss: float = 0.0,
+                 reduction="mean"):
         self.h = cce_create(vocab_total, ignore_index, vocab_offset, rank, world, nccl_comm, flags, label_smoothing,
-                            z_loss)
+                            z_loss, reduction)
+        self.reduction = _REDUCTIONS.get(reduction, reduction) if isinstance(reduction, str) else reduction
         self.vocab_total = vocab_total
         self.ignore_index = ignore_index
         self._ws = None
@@ -246,7 +255,8 @@ class CCEHandle:
         import torch
         N, D = H.shape
         ws = self.workspace(N, D, W.shape[0], H.device)
-        loss = torch.empty((), dtype=torch.float32, device=H.device)
+        loss = (torch.empty(N, dtype=torch.float32, device=H.device) if self.reduction == REDUCTION_NONE
+                else torch.empty((), dtype=torch.float32, device=H.device))
         lse = torch.empty(N, dtype=torch.float32, device=H.device) if want_lse else None
         nv = torch.empty((), dtype=torch.int32, device=H.device)
         cce_forward(self.h, H, W, labels, loss, lse, nv, ws, stream)
@@ -298,7 +308,8 @@ def _make_function():
             dH = torch.empty_like(H) if H.stride(0) == H.shape[1] else torch.empty(H.shape, dtype=H.dtype, device=H.device)
             dW = torch.empty(W.shape, dtype=W.dtype, device=W.device)
             if dloss is None:
-                dloss = torch.zeros((), dtype=torch.float32, device=H.device)
+                shape = (H.shape[0],) if ctx.handle.reduction == REDUCTION_NONE else ()
+                dloss = torch.zeros(shape, dtype=torch.float32, device=H.device)
             ctx.handle.backward(dloss.contiguous().float(), dH, dW)
             return dH, dW, None, None
 
@@ -309,15 +320,17 @@ _CCEFunction = None
 
 
 def linear_cross_entropy(H, W, labels, ignore_index: int = -100, handle: CCEHandle | None = None,
-                         return_lse: bool = False, label_smoothing: float = 0.0, z_loss: float = 0.0):
-    """Mean cross-entropy of softmax(H W^T) against labels, fused and never
-    materialising the [N, V] logits.  H [N,D] bf16, W [V,D] bf16, labels [N] int32."""
+                         return_lse: bool = False, label_smoothing: float = 0.0, z_loss: float = 0.0,
+                         reduction: str = "mean"):
+    """Cross-entropy of softmax(H W^T) against labels, fused and never materialising the
+    [N, V] logits.  H [N,D] bf16, W [V,D] bf16, labels [N] int32.  reduction: "mean"
+    (over non-ignored rows), "sum", or "none" (per-token losses, 0 for ignored rows)."""
     global _CCEFunction
     _check_inputs(H, W, labels)
     if _CCEFunction is None:
         _CCEFunction = _make_function()
     if handle is None:
         handle = CCEHandle(vocab_total=W.shape[0], ignore_index=ignore_index, label_smoothing=label_smoothing,
-                           z_loss=z_loss)
+                           z_loss=z_loss, reduction=reduction)
     loss, lse, nv = _CCEFunction.apply(H, W, labels, handle)
     return (loss, lse) if return_lse else loss

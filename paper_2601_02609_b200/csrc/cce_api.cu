@@ -196,8 +196,8 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   int64_t Npad, Tv, C;
   int64_t n_chunks, sched_ints;
-  size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, gbuf, dH32,
-      sched, total;
+  size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, dloss_c, gbuf,
+      dH32, sched, total;
 };
 
 Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots) {
@@ -227,6 +227,7 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
   L.stats_all = take((size_t)world * L.Npad * 16);
   L.lse_c = take((size_t)L.Npad * 4);
   L.loss_rows = take((size_t)L.Npad * 4);
+  L.dloss_c = take((size_t)L.Npad * 4);  // reduction "none": upstream gradients of the valid rows
   L.gbuf = take((size_t)slots * L.Npad * L.C * 2);  // ring of N x chunk dlogits (never N x V)
   L.dH32 = take((size_t)L.Npad * D * 4);
   L.n_chunks = (V_local + L.C - 1) / L.C;
@@ -417,6 +418,7 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
   if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
   if (!(cfg->label_smoothing >= 0.f && cfg->label_smoothing < 1.f) || !(cfg->z_loss >= 0.f && cfg->z_loss < 1e30f))
     return CCE_ERR_INVALID_VALUE;
+  if (cfg->reduction < CCE_REDUCTION_MEAN || cfg->reduction > CCE_REDUCTION_NONE) return CCE_ERR_INVALID_VALUE;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return CCE_ERR_UNSUPPORTED;
   int major = 0, sms = 0;
@@ -554,7 +556,9 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
     p.inv_vtotal = (float)(1.0 / (double)h->cfg.vocab_total);
     p.zs_part = h->cfg.label_smoothing > 0.f ? at<float>(ws, L.zs_part) : nullptr;
     if (h->cfg.flags & CCE_FLAG_ONE_CTA) {
-      if (h->cfg.label_smoothing != 0.f || h->cfg.z_loss != 0.f) return CCE_ERR_UNSUPPORTED;
+      if (h->cfg.label_smoothing != 0.f || h->cfg.z_loss != 0.f || h->cfg.reduction != CCE_REDUCTION_MEAN ||
+          (h->cfg.flags & (CCE_FLAG_GRAD_FP32 | CCE_FLAG_ACCUMULATE)))
+        return CCE_ERR_UNSUPPORTED;
       CUtensorMap tA, tB;
       if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, BM)) return CCE_ERR_CUDA;
       if (!make_map(&tB, W, D, V_local, ldw, BN)) return CCE_ERR_CUDA;
@@ -606,11 +610,14 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
                                                                 at<int>(ws, L.pos), (int)N, lse, at<float>(ws, L.lse_c),
                                                                 at<float>(ws, L.loss_rows), h->cfg.label_smoothing,
                                                                 h->cfg.z_loss,
-                                                                (float)(1.0 / (double)h->cfg.vocab_total));
+                                                                (float)(1.0 / (double)h->cfg.vocab_total),
+                                                                h->cfg.reduction == CCE_REDUCTION_NONE ? loss : nullptr);
   }
   {
     ProfScope ps(h, s, 4);
-    k_loss<<<1, 1024, 0, s>>>(at<float>(ws, L.loss_rows), nvp, errp, loss, n_valid);
+    k_loss<<<1, 1024, 0, s>>>(at<float>(ws, L.loss_rows), nvp, errp,
+                              h->cfg.reduction == CCE_REDUCTION_NONE ? nullptr : loss, n_valid,
+                              h->cfg.reduction == CCE_REDUCTION_SUM ? 1 : 0);
   }
   if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
 
@@ -651,7 +658,17 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     p.lse_c = at<float>(ws, L.lse_c);
     p.dloss = dloss;
     p.gbuf = at<__nv_bfloat16>(ws, L.gbuf);
-    p.dW = static_cast<__nv_bfloat16*>(dW);
+    p.dW = dW;
+    p.reduction = h->cfg.reduction;
+    p.dw_fp32 = (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0;
+    p.dw_accumulate = (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0;
+    p.dloss_c = nullptr;
+    if (h->cfg.reduction == CCE_REDUCTION_NONE) {
+      ProfScope ps(h, s, 4);
+      k_gather_dloss<<<grid_for(L.Npad, 256, 2 * h->num_sms), 256, 0, s>>>(dloss, at<int>(ws, L.idx), nvp,
+                                                                           (int)L.Npad, at<float>(ws, L.dloss_c));
+      p.dloss_c = at<float>(ws, L.dloss_c);
+    }
     p.dH32 = dH32;
     p.ls_eps = h->cfg.label_smoothing;
     p.z_loss = h->cfg.z_loss;
@@ -744,8 +761,10 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     }
     }
   } else if (V_local > 0 && N == 0) {
-    // no rows: dW = 0
-    if (cudaMemsetAsync(dW, 0, (size_t)V_local * D * 2, s) != cudaSuccess) return CCE_ERR_CUDA;
+    // no rows: dW = 0 (unchanged when accumulating)
+    if (!(h->cfg.flags & CCE_FLAG_ACCUMULATE) &&
+        cudaMemsetAsync(dW, 0, (size_t)V_local * D * ((h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 4 : 2), s) != cudaSuccess)
+      return CCE_ERR_CUDA;
   }
   if (N > 0) {
     if (V_local == 0 && cudaMemsetAsync(dH32, 0, (size_t)L.Npad * D * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
@@ -758,8 +777,9 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     }
     ProfScope ps(h, s, 4);
     k_scatter_dH<<<grid_for((long long)N * D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(dH32, at<int>(ws, L.pos), (int)N,
-                                                                                     (int)D,
-                                                                                     static_cast<__nv_bfloat16*>(dH));
+                                                                                     (int)D, dH,
+                                                                                     (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0,
+                                                                                     (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0);
   }
   if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
   return CCE_OK;
@@ -794,6 +814,7 @@ cce_status cce_step_host(cce_handle* h, const void* H_host, int64_t N, int64_t D
   if (N < 0 || D <= 0) return CCE_ERR_INVALID_VALUE;
   if (!dev_inputs || dev_inputs_bytes < cce_host_staging_bytes(N, D) || !aligned16(dev_inputs))
     return CCE_ERR_WORKSPACE;
+  if (h->cfg.reduction == CCE_REDUCTION_NONE) return CCE_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(dev_inputs);
   void* Hd = base;

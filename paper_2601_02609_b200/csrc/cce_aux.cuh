@@ -140,11 +140,14 @@ __global__ void __launch_bounds__(1024) k_merge_tiles(const float2* __restrict__
 //   (1 - eps)(lse - z_y) + eps (lse - sum_v z_v / V_total) + lambda lse^2.
 __global__ void k_finalize(const float4* __restrict__ stats_all, int world, int Npad, const int* __restrict__ pos,
                            int N, float* __restrict__ lse_out, float* __restrict__ lse_c,
-                           float* __restrict__ loss_rows, float ls_eps, float z_loss, float inv_vtotal) {
+                           float* __restrict__ loss_rows, float ls_eps, float z_loss, float inv_vtotal,
+                           float* __restrict__ loss_tok) {
+  // loss_tok (reduction "none"): the per-token loss at the original positions, 0 for ignored rows
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     const int i = pos[n];
     if (i < 0) {
       if (lse_out) lse_out[n] = 0.f;
+      if (loss_tok) loss_tok[n] = 0.f;
       continue;
     }
     float m = -INFINITY, zy = 0.f, zs = 0.f;
@@ -165,15 +168,17 @@ __global__ void k_finalize(const float4* __restrict__ stats_all, int world, int 
     if (ls_eps != 0.f || z_loss != 0.f)
       l = (1.f - ls_eps) * l + ls_eps * (lse - zs * inv_vtotal) + z_loss * lse * lse;
     loss_rows[i] = l;
+    if (loss_tok) loss_tok[n] = l;
     if (lse_out) lse_out[n] = lse;
   }
 }
 
 // Mean loss over the valid rows in a fixed reduction order (deterministic).
 // loss = 0 when n_valid == 0 (reading R2); NaN when a label was out of range.
+// mean (default) or sum (sum = 1); loss may be nullptr (reduction "none": only n_valid).
 __global__ void __launch_bounds__(1024) k_loss(const float* __restrict__ loss_rows, const int* __restrict__ n_valid,
                                                const int* __restrict__ err, float* __restrict__ loss,
-                                               int32_t* __restrict__ n_valid_out) {
+                                               int32_t* __restrict__ n_valid_out, int sum) {
   __shared__ float red[32];
   const int nv = *n_valid;
   float s = 0.f;
@@ -187,22 +192,57 @@ __global__ void __launch_bounds__(1024) k_loss(const float* __restrict__ loss_ro
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (threadIdx.x == 0) {
-      float l = nv > 0 ? s / (float)nv : 0.f;
+      float l = sum ? s : (nv > 0 ? s / (float)nv : 0.f);
       if (*err) l = __int_as_float(0x7fc00000);
-      *loss = l;
+      if (loss) *loss = l;
       if (n_valid_out) *n_valid_out = nv;
     }
   }
 }
 
 // a8: dH rows back to the original positions in bf16; ignored rows are bit-zero.
+// fp32 = 1: dH is float32; accumulate = 1: dH += gradient (ignored rows untouched).
 __global__ void k_scatter_dH(const float* __restrict__ dH32, const int* __restrict__ pos, int N, int D,
-                             __nv_bfloat16* __restrict__ dH) {
+                             void* __restrict__ dH_out, int fp32, int accumulate) {
   const int vec_per_row = D / 8;
   const long long total = (long long)N * vec_per_row;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const int n = (int)(i / vec_per_row), c = (int)(i % vec_per_row);
     const int r = pos[n];
+    if (fp32 || accumulate) {
+      if (accumulate && r < 0) continue;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      if (r >= 0) {
+        a = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8);
+        b = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8 + 4);
+      }
+      if (fp32) {
+        float4* d = reinterpret_cast<float4*>(static_cast<float*>(dH_out) + (long long)n * D + c * 8);
+        if (accumulate) {
+          const float4 o0 = d[0], o1 = d[1];
+          a.x += o0.x; a.y += o0.y; a.z += o0.z; a.w += o0.w;
+          b.x += o1.x; b.y += o1.y; b.z += o1.z; b.w += o1.w;
+        }
+        d[0] = a;
+        d[1] = b;
+      } else {  // bf16 accumulate: add in fp32, round once
+        uint4* d = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(dH_out) + (long long)n * D + c * 8);
+        const uint4 o = *d;
+        const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+        uint32_t q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float lo = f[2 * k] + __uint_as_float(w[k] << 16);
+          const float hi = f[2 * k + 1] + __uint_as_float(w[k] & 0xffff0000u);
+          __nv_bfloat162 p2 = __floats2bfloat162_rn(lo, hi);
+          q[k] = *reinterpret_cast<uint32_t*>(&p2);
+        }
+        *d = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+      continue;
+    }
+    __nv_bfloat16* dH = static_cast<__nv_bfloat16*>(dH_out);
     uint4 out = make_uint4(0, 0, 0, 0);
     if (r >= 0) {
       const float4 a = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8);
@@ -219,5 +259,13 @@ __global__ void k_scatter_dH(const float* __restrict__ dH32, const int* __restri
 }
 
 __global__ void k_set_scalar(float* p, float v) { *p = v; }
+
+// reduction "none": the per-token upstream gradients of the valid rows in compact order.
+__global__ void k_gather_dloss(const float* __restrict__ dloss, const int* __restrict__ idx,
+                               const int* __restrict__ n_valid, int Npad, float* __restrict__ dloss_c) {
+  const int nv = *n_valid;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Npad; i += gridDim.x * blockDim.x)
+    dloss_c[i] = i < nv ? dloss[idx[i]] : 0.f;
+}
 
 }  // namespace cce

@@ -61,7 +61,7 @@ struct GemmParams {
   const float* lse_c;   // G: [Npad]
   const float* dloss;   // G: device scalar
   __nv_bfloat16* gbuf;  // G: [Npad][C]
-  __nv_bfloat16* dW;    // DW: [V_local][D]
+  void* dW;             // DW: [V_local][D] bf16 (or float32 with dw_fp32)
   float* dH32;          // DH: [Npad][D]
   int dh_accumulate;    // DH: 0 = overwrite (first chunk), 1 = add
   // regularised loss (pair / quad kernels only; cce.h cce_config)
@@ -69,6 +69,11 @@ struct GemmParams {
   float z_loss;         // z-loss weight lambda
   float inv_vtotal;     // 1 / vocab_total (the mean of the logits runs over the global vocabulary)
   float* zs_part;       // FWD: [ceil(V_local/256)][Npad] per-tile logit sums, or nullptr (eps == 0)
+  // reduction / gradient modes (pair / quad kernels only; cce.h CCE_REDUCTION_*, CCE_FLAG_GRAD_*)
+  int reduction;        // 0 mean (dloss / n_valid), 1 sum (dloss), 2 none (dloss_c per row)
+  const float* dloss_c; // G: reduction "none": per-row upstream gradients (compact rows), else nullptr
+  int dw_fp32;          // DW: dW is float32 (else bf16)
+  int dw_accumulate;    // DW: dW += gradient (else overwrite)
 };
 
 struct TileGeom {
@@ -218,7 +223,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
       if (dcol < p.D) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          if (lcol0 + i < p.width) p.dW[(size_t)(p.c0 + lcol0 + i) * p.D + dcol] = __float2bfloat16_rn(v[i]);
+          if (lcol0 + i < p.width)
+            static_cast<__nv_bfloat16*>(p.dW)[(size_t)(p.c0 + lcol0 + i) * p.D + dcol] = __float2bfloat16_rn(v[i]);
         }
       }
     }

@@ -235,6 +235,7 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
   const bool rv = row < nv;
   const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
   const float lse = rv ? p.lse_c[row] : 0.f;
+  if (p.dloss_c) scale = rv ? p.dloss_c[row] : 0.f;       // reduction "none": per-row upstream gradient
   const float sa = scale * (1.f + 2.f * p.z_loss * lse);  // scale of the softmax term
   const float off2 = rv ? (lse * LOG2E - __log2f(fabsf(sa))) : INFINITY;
   const float cu = rv ? -scale * p.ls_eps * p.inv_vtotal : 0.f;  // uniform term
@@ -314,11 +315,40 @@ __device__ __forceinline__ void epi_dw(const GemmParams& p, uint32_t taddr, cons
     }
     const int d0 = it.n0 + cb + j * 32;
     if (vrow < width && d0 < p.D) {
-      uint4* dst = reinterpret_cast<uint4*>(p.dW + (size_t)(c0 + vrow) * p.D + d0);
+      const size_t off = (size_t)(c0 + vrow) * p.D + d0;
+      if (p.dw_fp32) {
+        // float32 gradient (CCE_FLAG_GRAD_FP32), optionally accumulated into the caller's
+        // buffer (CCE_FLAG_ACCUMULATE): each element has exactly one writer, so a plain
+        // load-add-store is race-free and deterministic
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.dW) + off);
+        if (p.dw_accumulate) {
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4)
-        dst[q4] = make_uint4(pack_bf16(v[8 * q4], v[8 * q4 + 1]), pack_bf16(v[8 * q4 + 2], v[8 * q4 + 3]),
-                             pack_bf16(v[8 * q4 + 4], v[8 * q4 + 5]), pack_bf16(v[8 * q4 + 6], v[8 * q4 + 7]));
+          for (int i = 0; i < 8; ++i) {
+            const float4 o = dst[i];
+            v[4 * i] += o.x; v[4 * i + 1] += o.y; v[4 * i + 2] += o.z; v[4 * i + 3] += o.w;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      } else {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.dW) + off);
+        if (p.dw_accumulate) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 o = dst[q4];
+            const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) {
+              v[8 * q4 + 2 * k2] += __uint_as_float(w[k2] << 16);
+              v[8 * q4 + 2 * k2 + 1] += __uint_as_float(w[k2] & 0xffff0000u);
+            }
+          }
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          dst[q4] = make_uint4(pack_bf16(v[8 * q4], v[8 * q4 + 1]), pack_bf16(v[8 * q4 + 2], v[8 * q4 + 3]),
+                               pack_bf16(v[8 * q4 + 4], v[8 * q4 + 5]), pack_bf16(v[8 * q4 + 6], v[8 * q4 + 7]));
+      }
     }
   }
 }
@@ -663,7 +693,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     e.xz = reinterpret_cast<float*>(stage_base);  // forward items never use the store staging
     e.stage = stage_base + (warp - 4) * 4096;
     const bool leader = (threadIdx.x == 128);
-    const float scale = (P.mode == 1 && k.nv > 0) ? (*g.dloss) / (float)k.nv : 0.f;
+    const float scale = (P.mode == 1 && k.nv > 0 && g.reduction != 2)
+                            ? (g.reduction == 1 ? *g.dloss : (*g.dloss) / (float)k.nv)
+                            : 0.f;  // reduction "none": per-row dloss_c in epi_g
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     uint32_t rs = 0, rph = 0;
     int acc_it = 0;

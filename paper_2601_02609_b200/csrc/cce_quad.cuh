@@ -436,7 +436,9 @@ __global__ void __launch_bounds__(QTHREADS, 1)
     e.xz = reinterpret_cast<float*>(stage_base);  // forward items never use the store staging
     e.stage = stage_base + (warp - 4) * 4096;
     const bool leader = (threadIdx.x == 128);
-    const float scale = (P.mode == 1 && k.nv > 0) ? (*g.dloss) / (float)k.nv : 0.f;
+    const float scale = (P.mode == 1 && k.nv > 0 && g.reduction != 2)
+                            ? (g.reduction == 1 ? *g.dloss : (*g.dloss) / (float)k.nv)
+                            : 0.f;  // reduction "none": per-row dloss_c in epi_g
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), pair_leader);
     uint32_t rs = 0, rph = 0;
     int acc_it = 0;

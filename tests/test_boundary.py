@@ -69,6 +69,11 @@ def test_host_validation_without_gpu(lib):
         cfg.label_smoothing, cfg.z_loss = ls, zl
         assert lib.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 1    # eps in [0, 1), lambda >= 0 finite
     cfg.label_smoothing, cfg.z_loss = 0.0, 0.0
+    assert cfg.reduction == 0                                              # CCE_REDUCTION_MEAN by default
+    for red in (-1, 3):
+        cfg.reduction = red
+        assert lib.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 1
+    cfg.reduction = 0
     assert lib.cce_forward(None, None, 0, 64, 64, None, 0, 64, None, None, None, None, None, 0, None) == 1
     assert lib.cce_backward(None, None, None, None, None) == 1
     assert lib.cce_workspace_bytes(None, 10, 64, 10) == 0

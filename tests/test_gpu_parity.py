@@ -19,10 +19,12 @@ def dev():
     return torch.device("cuda:0")
 
 
-def _check(p, dev, dloss=1.0, flags=0, label_smoothing=0.0, z_loss=0.0):
+def _check(p, dev, dloss=1.0, flags=0, label_smoothing=0.0, z_loss=0.0, reduction="mean"):
     H, W, y = to_dev(p, dev)
-    got = run_gpu(H, W, y, dloss=dloss, flags=flags, label_smoothing=label_smoothing, z_loss=z_loss)
-    ref = oracle.cce(p["H"], p["W"], p["labels"], dloss=dloss, label_smoothing=label_smoothing, z_loss=z_loss)
+    got = run_gpu(H, W, y, dloss=dloss, flags=flags, label_smoothing=label_smoothing, z_loss=z_loss,
+                  reduction=reduction)
+    ref = oracle.cce(p["H"], p["W"], p["labels"], dloss=dloss, label_smoothing=label_smoothing, z_loss=z_loss,
+                     reduction=reduction)
     assert_parity(got, ref, p["labels"])
     return got, ref
 
@@ -77,6 +79,48 @@ def test_label_smoothing_and_z_loss(dev, N, D, V, ign, flags, eps, lam):
     _check(p, dev, flags=flags, label_smoothing=eps, z_loss=lam)
 
 
+@pytest.mark.parametrize("reduction,eps,lam,flags", [
+    ("sum", 0.0, 0.0, 0), ("none", 0.0, 0.0, 0), ("sum", 0.1, 1e-4, 0), ("none", 0.1, 1e-3, 0),
+    ("none", 0.0, 0.0, 32),     # quad kernels
+])
+def test_reductions(dev, reduction, eps, lam, flags):
+    """SURVEY 8(f) NEXT #3: sum and per-token ("none", per-row upstream gradients) losses."""
+    p = workload.make_problem(700, 256, 9000, seed=21, ignore="bern40")
+    if reduction == "none":
+        dloss = np.random.default_rng(3).standard_normal(700).astype(np.float32).astype(np.float64) / 700
+    else:
+        dloss = 0.5 / 420
+    _check(p, dev, dloss=dloss, flags=flags, label_smoothing=eps, z_loss=lam, reduction=reduction)
+
+
+@pytest.mark.parametrize("flags", [64, 128, 192], ids=["fp32", "accumulate_bf16", "accumulate_fp32"])
+def test_grad_dtype_and_accumulation(dev, flags):
+    """NEXT #3: float32 gradients and accumulation into existing .grad buffers (the
+    result minus the initial buffer is the gradient; ignored rows of dH untouched)."""
+    import torch
+    import paper_2601_02609_b200 as cce
+    from cce_testutil import rel_fro
+    p = workload.make_problem(600, 192, 7000, seed=22, ignore="bern40")
+    H, W, y = to_dev(p, dev)
+    gdt = torch.float32 if flags & cce.FLAG_GRAD_FP32 else torch.bfloat16
+    g = torch.Generator(device="cpu").manual_seed(5)
+    dH0 = (torch.randn(H.shape, generator=g) * 1e-3).to(gdt).to(dev)
+    dW0 = (torch.randn(W.shape, generator=g) * 1e-3).to(gdt).to(dev)
+    init_H = dH0.double().cpu().numpy(); init_W = dW0.double().cpu().numpy()
+    got = run_gpu(H, W, y, flags=flags, dH_init=dH0.clone(), dW_init=dW0.clone())
+    ref = oracle.cce(p["H"], p["W"], p["labels"])
+    acc = bool(flags & cce.FLAG_ACCUMULATE)
+    dH = got["dH"] - (init_H if acc else 0.0)
+    dW = got["dW"] - (init_W if acc else 0.0)
+    tol = 1e-2 if gdt == torch.bfloat16 and not acc else 2e-2   # bf16 accumulation rounds once more
+    assert rel_fro(dH, ref["dH"]) <= tol and rel_fro(dW, ref["dW"]) <= tol
+    ign = p["labels"] == -100
+    if acc:
+        assert np.array_equal(got["dH"][ign], init_H[ign])      # ignored rows untouched
+    else:
+        assert np.all(got["dH"][ign] == 0)
+
+
 @pytest.mark.parametrize("regime", ["peaked", "zero"])
 def test_label_smoothing_and_z_loss_regimes(dev, regime):
     """W = 0 (loss = ln V + lam ln^2 V exactly, S:248) and confident targets."""
@@ -88,11 +132,14 @@ def test_regularised_loss_rejected_by_one_cta_kernels(dev):
     import paper_2601_02609_b200 as cce
     p = workload.make_problem(100, 64, 500, seed=12, ignore="bern10")
     H, W, y = to_dev(p, dev)
-    h = cce.CCEHandle(vocab_total=500, flags=cce.FLAG_ONE_CTA, label_smoothing=0.1)
-    with pytest.raises(cce.CCEError) as ei:
-        h.forward(H, W, y)
-    assert ei.value.status == 2     # CCE_ERR_UNSUPPORTED
-    h.close()
+    for kw in ({"label_smoothing": 0.1}, {"reduction": "sum"}, {"flags": cce.FLAG_GRAD_FP32}):
+        kw = dict(kw)
+        kw["flags"] = kw.get("flags", 0) | cce.FLAG_ONE_CTA
+        h = cce.CCEHandle(vocab_total=500, **kw)
+        with pytest.raises(cce.CCEError) as ei:
+            h.forward(H, W, y)
+        assert ei.value.status == 2     # CCE_ERR_UNSUPPORTED
+        h.close()
 
 
 @pytest.mark.parametrize("regime", ["peaked", "extreme", "zero"])
