@@ -107,7 +107,8 @@ typedef struct {
   int64_t vocab_offset;   /* first global vocabulary id owned by this rank (0 if unsharded) */
   int32_t rank;           /* this rank, 0 if unsharded */
   int32_t world;          /* number of vocabulary shards (ranks), 1 if unsharded */
-  void *nccl_comm;        /* ncclComm_t from cce_nccl_comm_init when world > 1, else NULL */
+  void *nccl_comm;        /* ncclComm_t from cce_nccl_comm_init: required when world > 1; optional with
+                           * world == 1 (the collectives then run on one rank: a test of that path) */
   uint32_t flags;         /* CCE_FLAG_* */
   /* Regularised loss, both 0 by default (the paper's CCE kernels
    * apply neither):

@@ -414,7 +414,9 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
   if (cfg->vocab_total <= 0 || cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world ||
       cfg->vocab_offset < 0 || cfg->vocab_offset > cfg->vocab_total)
     return CCE_ERR_INVALID_VALUE;
-  if ((cfg->world > 1) != (cfg->nccl_comm != nullptr)) return CCE_ERR_INVALID_VALUE;
+  // world > 1 needs a communicator; world == 1 may carry one (a 1-rank comm runs the
+  // same NCCL collectives -- identities -- which lets one GPU exercise that path)
+  if (cfg->world > 1 && cfg->nccl_comm == nullptr) return CCE_ERR_INVALID_VALUE;
   if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
   if (!(cfg->label_smoothing >= 0.f && cfg->label_smoothing < 1.f) || !(cfg->z_loss >= 0.f && cfg->z_loss < 1e30f))
     return CCE_ERR_INVALID_VALUE;
@@ -597,7 +599,7 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
         (h->cfg.label_smoothing > 0.f && V_local > 0) ? at<float>(ws, L.zs_part) : nullptr, stats);
   }
   const float4* stats_all = stats;
-  if (h->cfg.world > 1) {
+  if (h->cfg.nccl_comm) {
     Nccl& n = nccl();
     if (!n.ok) return CCE_ERR_NCCL;
     if (n.allgather(stats, at<float4>(ws, L.stats_all), (size_t)L.Npad * 4, kNcclFloat32, h->cfg.nccl_comm, s) != 0)
@@ -768,7 +770,7 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
   }
   if (N > 0) {
     if (V_local == 0 && cudaMemsetAsync(dH32, 0, (size_t)L.Npad * D * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
-    if (h->cfg.world > 1) {
+    if (h->cfg.nccl_comm) {
       // a10: dH partials summed over the vocabulary shards
       Nccl& n = nccl();
       if (!n.ok) return CCE_ERR_NCCL;

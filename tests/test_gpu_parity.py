@@ -271,3 +271,23 @@ def test_step_host_matches_device_path(dev):
     assert rel_fro(bf16_to_f64(dH), ref["dH"]) <= 1e-2
     assert rel_fro(bf16_to_f64(dW), ref["dW"]) <= 1e-2
     h.close()
+
+
+def test_nccl_path_on_one_rank(dev):
+    """The vocabulary-sharded combine (a9 stats allgather, a10 dH all-reduce) through a
+    real 1-rank NCCL communicator: the collectives are identities, so every output must
+    be bit-identical to the plain path.  (More ranks need more GPUs: bench.py --gpus N.)"""
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(700, 256, 9000, seed=23, ignore="bern40")
+    H, W, y = to_dev(p, dev)
+    comm = cce.cce_nccl_comm_init(1, cce.cce_nccl_unique_id(), 0)
+    try:
+        h1 = cce.CCEHandle(vocab_total=9000, nccl_comm=comm)
+        a = run_gpu(H, W, y, handle=h1)
+        h1.close()
+    finally:
+        cce.cce_nccl_comm_destroy(comm)
+    b = run_gpu(H, W, y)
+    assert a["loss"] == b["loss"]
+    for k in ("lse_bits", "dH_bits", "dW_bits"):
+        assert np.array_equal(a[k], b[k]), k
