@@ -70,6 +70,8 @@ def lib():
         L.oracle_online_lse.restype = f64
         L.oracle_partial_stats.argtypes = [p, p, p, i64, i64, i64, i64, i32, p, p, p]
         L.oracle_partial_stats.restype = ctypes.c_int
+        L.oracle_adamw_step.argtypes = [p, p, p, p, i64, f64, f64, f64, f64, f64, f64, f64, f64]
+        L.oracle_adamw_step.restype = None
         L.oracle_validate.argtypes = [p, i64, i64, i32, p]
         L.oracle_validate.restype = ctypes.c_int
         L.oracle_num_threads.argtypes = []
@@ -191,3 +193,18 @@ def validate(labels, V, ignore_index=-100) -> int:
     nv = np.zeros(1, np.int64)
     _check(lib().oracle_validate(_ptr(y), len(y), int(V), ignore_index, _ptr(nv)))
     return int(nv[0])
+
+
+def adamw_step(theta, grad, m, v, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, clip_coef=1.0, step=1):
+    """One AdamW step (oracle_adamw_step) on copies; returns (theta, m, v) in fp64.
+    Bias corrections 1 - beta^step are computed here (host side)."""
+    th = np.ascontiguousarray(theta, dtype=np.float64).copy()
+    g = np.ascontiguousarray(grad, dtype=np.float64)
+    mm = np.ascontiguousarray(m, dtype=np.float64).copy()
+    vv = np.ascontiguousarray(v, dtype=np.float64).copy()
+    assert th.shape == g.shape == mm.shape == vv.shape
+    bc1 = 1.0 - beta1 ** step
+    bc2 = 1.0 - beta2 ** step
+    lib().oracle_adamw_step(_ptr(th), _ptr(g), _ptr(mm), _ptr(vv), th.size, float(lr), float(beta1), float(beta2),
+                            float(eps), float(weight_decay), float(clip_coef), bc1, bc2)
+    return th, mm, vv

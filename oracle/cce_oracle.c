@@ -405,3 +405,27 @@ int oracle_partial_stats(const double *H, const double *W_local,
     }
     return nomem ? ORACLE_ERR_NOMEM : ORACLE_OK;
 }
+
+/*
+ * One AdamW step in the order of the paper's fused kernel,
+ * Alg. "Fused AdamW Triton Kernel (Complete)", which is Def. AdamW
+ * with a pre-supplied clipping coefficient:
+ *   g  = g * clip_coef
+ *   th = th * (1 - lr * wd)                       decoupled weight decay
+ *   m  = b1 m + (1 - b1) g ;  v = b2 v + (1 - b2) g^2
+ *   th = th - lr * (m / bc1) / (sqrt(v / bc2) + eps),   bc_i = 1 - b_i^t (host)
+ * In place over n elements, fp64.
+ */
+void oracle_adamw_step(double *theta, const double *grad, double *m, double *v, int64_t n,
+                       double lr, double b1, double b2, double eps, double wd, double clip_coef,
+                       double bc1, double bc2) {
+    for (int64_t i = 0; i < n; ++i) {
+        double g = grad[i] * clip_coef;
+        double th = theta[i] * (1.0 - lr * wd);
+        m[i] = b1 * m[i] + (1.0 - b1) * g;
+        v[i] = b2 * v[i] + (1.0 - b2) * g * g;
+        double mh = m[i] / bc1;
+        double vh = v[i] / bc2;
+        theta[i] = th - lr * (mh / (sqrt(vh) + eps));
+    }
+}

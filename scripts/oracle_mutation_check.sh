@@ -22,6 +22,13 @@ muts=(
  's/(dloss_rows ? dloss_rows\[n\] : 0.0)/(dloss_rows ? dloss_rows[0] : 0.0)/'  # none: wrong row of dloss
  's/loss\[n\] = labels\[n\] != ignore_index ? row_loss\[n\] : 0.0;/loss[n] = labels[n] != ignore_index ? row_loss[n] \/ (double)nv : 0.0;/'  # none: per-row loss averaged
 )
+# fused AdamW (oracle_adamw_step)
+muts+=(
+ 's/double th = theta\[i\] \* (1.0 - lr \* wd);/double th = theta[i];/'           # dropped weight decay
+ 's/double g = grad\[i\] \* clip_coef;/double g = grad[i];/'                    # dropped clipping
+ 's/double vh = v\[i\] \/ bc2;/double vh = v[i];/'                                # dropped bias correction
+ 's/theta\[i\] = th - lr \* (mh \/ (sqrt(vh) + eps));/theta[i] = th - lr * (mh \/ sqrt(vh + eps));/'  # eps inside sqrt
+)
 fail=0
 for m in "${muts[@]}"; do
   cp /tmp/oracle_orig.c oracle/cce_oracle.c

@@ -463,3 +463,36 @@ def test_reductions_match_torch_fp64(reduction, eps, lam):
         assert np.all(r["loss"][y == -100] == 0.0)
     np.testing.assert_allclose(r["dH"], Ht.grad.numpy(), rtol=1e-10, atol=1e-14)
     np.testing.assert_allclose(r["dW"], Wt.grad.numpy(), rtol=1e-10, atol=1e-14)
+
+
+# ---------------------------------------------------------------- fused AdamW (NEXT #2)
+def test_adamw_spec_worked_examples():
+    """S:332-333: theta=1, g=1, lr=0.1, wd=0, t=1 -> 0.9000; g=0, wd=0.01, lr=0.1 -> theta*0.999."""
+    th, m, v = oracle.adamw_step([1.0], [1.0], [0.0], [0.0], lr=0.1, weight_decay=0.0, step=1)
+    assert abs(th[0] - 0.9000) <= 5e-5 and abs(th[0] - (1 - 0.1 / (1 + 1e-8))) <= 1e-15
+    th, m, v = oracle.adamw_step([2.0, -3.0], [0.0, 0.0], [0.0, 0.0], [0.0, 0.0], lr=0.1, weight_decay=0.01)
+    np.testing.assert_allclose(th, [2.0 * 0.999, -3.0 * 0.999], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("step,clip", [(1, 1.0), (5, 0.5)])
+def test_adamw_matches_torch_fp64(step, clip):
+    """Library routine: torch.optim.AdamW (fp64) after `step - 1` warm-up steps, with the
+    clipping coefficient applied to the gradient first."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(step)
+    n = 257
+    th0 = rng.standard_normal(n)
+    grads = [rng.standard_normal(n) * 10.0 ** rng.uniform(-8, 0, n) for _ in range(step)]
+    p = torch.nn.Parameter(torch.tensor(th0))
+    opt = torch.optim.AdamW([p], lr=3e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    th, m, v = th0.copy(), np.zeros(n), np.zeros(n)
+    for t, g in enumerate(grads, start=1):
+        p.grad = torch.tensor(g * clip)
+        opt.step()
+        th, m, v = oracle.adamw_step(th, g, m, v, lr=3e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1,
+                                     clip_coef=clip, step=t)
+    np.testing.assert_allclose(th, p.detach().numpy(), rtol=1e-13, atol=1e-15)
+    st = opt.state[p]
+    # torch forms m with lerp (m + (1 - b1)(g - m)): same value, different rounding
+    np.testing.assert_allclose(m, st["exp_avg"].numpy(), rtol=1e-12, atol=1e-30)
+    np.testing.assert_allclose(v, st["exp_avg_sq"].numpy(), rtol=1e-12, atol=1e-30)
