@@ -175,6 +175,66 @@ cce_status cce_forward(cce_handle *h,
  */
 cce_status cce_backward(cce_handle *h, const float *dloss, void *dH, void *dW, void *stream);
 
+/*
+ * Fused AdamW.  The update is the paper's fused kernel,
+ * Alg. "Fused AdamW Triton Kernel (Complete)", which is Def. AdamW
+ * with a pre-computed clipping coefficient, per element:
+ *   g  = (grad_in + grad) * clip_coef
+ *   th = th * (1 - lr * weight_decay)              decoupled weight decay
+ *   m  = beta1 m + (1 - beta1) g ;  v = beta2 v + (1 - beta2) g^2
+ *   th = th - lr * (m / bias_correction1) / (sqrt(v / bias_correction2) + eps)
+ * in float32.  bias_correction_i = 1 - beta_i^t is computed by the caller from its
+ * host step counter (no device sync).
+ *   master  [n] float32 master weights (row stride D for the fused backward), or NULL:
+ *           then the bf16 weights themselves are theta (read, updated, rounded back)
+ *   m, v    [n] float32 moments (same layout as master), updated in place; required
+ *   grad_in [n] float32 gradient accumulated over earlier micro-batches,
+ *           added to this step's gradient; NULL = none
+ *   clip_coef device float scalar min(1, max_norm / global_norm), or NULL = 1.
+ *           Global-norm clipping needs the norm of the whole gradient before any update,
+ *           so a fused step takes the coefficient as an input (the caller's norm pass)
+ * All pointers are device pointers owned by the caller.
+ */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+  float bias_correction1, bias_correction2;
+  const float *clip_coef;
+  float *master;
+  float *m;
+  float *v;
+  const float *grad_in;
+  void *W_out;  /* bf16 [V_local, D] with W's row stride: receives bf16(theta_new); NULL = W itself
+                 * (in place).  A second buffer (weights double-buffered across steps) lets the
+                 * fused backward skip the wait described below */
+} cce_adamw_params;
+
+/*
+ * Backward with the optimizer step fused into the dW epilogue: when a
+ * vocabulary-stationary tile of dW = G^T H is complete in TMEM, the epilogue
+ * applies AdamW to those rows of W (and master / m / v) directly, so dW never
+ * goes to HBM (saves the dW write and re-read, and the optimizer launch).  dH as
+ * in cce_backward.  W is the buffer passed to the last cce_forward on `h`.  With
+ * opt->W_out == NULL it is UPDATED IN PLACE (bf16(theta_new)) and must be writable:
+ * the epilogue of a chunk's dW tiles then waits until that chunk's dH tiles (which
+ * read W) are complete, so the update never races the backward's own reads.  With
+ * opt->W_out a distinct buffer (same shape and row stride as W), W is only read.  Pair kernel (the default)
+ * only: CCE_FLAG_ONE_CTA / CCE_FLAG_QUAD / CCE_FLAG_ACCUMULATE return
+ * CCE_ERR_UNSUPPORTED.  opt->m / opt->v NULL -> CCE_ERR_INVALID_VALUE.
+ */
+cce_status cce_backward_adamw(cce_handle *h, const float *dloss, void *dH, const cce_adamw_params *opt,
+                              void *stream);
+
+/*
+ * Standalone fused AdamW over n elements (the paper's one-kernel optimizer step,
+ * P:2003-2046; also the unfused baseline for cce_backward_adamw): grad is [n]
+ * bf16 (grad_fp32 = 0) or float32 (grad_fp32 = 1), may be NULL (zero gradient:
+ * decay and moment decay only); W_bf16 [n] bf16 receives bf16(theta_new) and is
+ * theta itself when opt->master is NULL (W_bf16 may be NULL only if master is set).
+ * HBM-bound: one read and one write of each state array.
+ */
+cce_status cce_adamw_step(const cce_adamw_params *opt, const void *grad, int32_t grad_fp32, int64_t n,
+                          void *W_bf16, void *stream);
+
 /* Synchronises `stream` and returns CCE_ERR_LABEL_RANGE if the most recent
  * cce_forward on this handle saw an out-of-range label (the offending rows are
  * treated as ignored and loss is NaN), else CCE_OK.  Clears the flag. */

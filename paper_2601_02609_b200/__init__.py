@@ -28,7 +28,7 @@ STATUS = {0: "CCE_OK", 1: "CCE_ERR_INVALID_VALUE", 2: "CCE_ERR_UNSUPPORTED", 3: 
 EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_bytes", "cce_forward", "cce_backward",
            "cce_get_error", "cce_host_staging_bytes", "cce_step_host", "cce_nccl_unique_id", "cce_nccl_comm_init",
            "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info",
-           "cce_profile_enable", "cce_profile_read", "cce_debug_trace"]
+           "cce_profile_enable", "cce_profile_read", "cce_debug_trace", "cce_backward_adamw", "cce_adamw_step"]
 PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 # "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
 # FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
@@ -56,6 +56,15 @@ class cce_config(ctypes.Structure):
                 ("reduction", ctypes.c_int32)]
 
 
+class cce_adamw_params(ctypes.Structure):
+    """Mirror of cce.h cce_adamw_params (fused AdamW, Alg. Fused AdamW P:2003-2046)."""
+    _fields_ = [("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
+                ("weight_decay", ctypes.c_float), ("bias_correction1", ctypes.c_float),
+                ("bias_correction2", ctypes.c_float), ("clip_coef", ctypes.c_void_p), ("master", ctypes.c_void_p),
+                ("m", ctypes.c_void_p), ("v", ctypes.c_void_p), ("grad_in", ctypes.c_void_p),
+                ("W_out", ctypes.c_void_p)]
+
+
 _lib = None
 
 
@@ -80,6 +89,10 @@ def lib():
         L.cce_forward.restype = st
         L.cce_backward.argtypes = [p, p, p, p, p]
         L.cce_backward.restype = st
+        L.cce_backward_adamw.argtypes = [p, p, p, ctypes.POINTER(cce_adamw_params), p]
+        L.cce_backward_adamw.restype = st
+        L.cce_adamw_step.argtypes = [ctypes.POINTER(cce_adamw_params), p, i32, i64, p, p]
+        L.cce_adamw_step.restype = st
         L.cce_get_error.argtypes = [p, p]
         L.cce_get_error.restype = st
         L.cce_host_staging_bytes.argtypes = [i64, i64]
@@ -163,6 +176,34 @@ def cce_forward(h, H, W, labels, loss, lse, n_valid, workspace, stream=None):
 
 def cce_backward(h, dloss, dH, dW, stream=None):
     _check(lib().cce_backward(h, _ptr(dloss), _ptr(dH), _ptr(dW), _stream(stream)), "cce_backward")
+
+
+def adamw_params(m, v, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, clip_coef=None,
+                 master=None, grad_in=None, W_out=None) -> cce_adamw_params:
+    """Marshal the optimizer state (torch float32 tensors) into cce_adamw_params; the bias
+    corrections 1 - beta^t come from the host step counter (no device sync)."""
+    o = cce_adamw_params()
+    o.lr, o.beta1, o.beta2, o.eps, o.weight_decay = lr, beta1, beta2, eps, weight_decay
+    o.bias_correction1 = 1.0 - beta1 ** step
+    o.bias_correction2 = 1.0 - beta2 ** step
+    o.clip_coef = None if clip_coef is None else clip_coef.data_ptr()
+    o.master = None if master is None else master.data_ptr()
+    o.m, o.v = m.data_ptr(), v.data_ptr()
+    o.grad_in = None if grad_in is None else grad_in.data_ptr()
+    o.W_out = None if W_out is None else W_out.data_ptr()
+    return o
+
+
+def cce_backward_adamw(h, dloss, dH, opt: cce_adamw_params, stream=None):
+    _check(lib().cce_backward_adamw(h, _ptr(dloss), _ptr(dH), ctypes.byref(opt), _stream(stream)),
+           "cce_backward_adamw")
+
+
+def cce_adamw_step(opt: cce_adamw_params, grad, n: int, W_bf16=None, stream=None):
+    import torch
+    g32 = 1 if (grad is not None and grad.dtype == torch.float32) else 0
+    _check(lib().cce_adamw_step(ctypes.byref(opt), _ptr(grad), g32, n, _ptr(W_bf16), _stream(stream)),
+           "cce_adamw_step")
 
 
 def cce_get_error(h, stream=None) -> int:
@@ -264,6 +305,11 @@ class CCEHandle:
 
     def backward(self, dloss, dH, dW, stream=None):
         cce_backward(self.h, dloss, dH, dW, stream)
+
+    def backward_adamw(self, dloss, dH, opt: cce_adamw_params, stream=None):
+        """Backward with AdamW fused into the dW epilogue: the W given to the last forward
+        (and opt's master / m / v) is updated in place; dW is never materialised."""
+        cce_backward_adamw(self.h, dloss, dH, opt, stream)
 
     def launches(self) -> int:
         return cce_kernel_launches(self.h)

@@ -273,15 +273,20 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
                        const pairk::PairParams& pp, cudaStream_t s, int prof_class) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(pairk::cce_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pairk::PSMEM) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(pairk::cce_pair_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pairk::PSMEM) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(pairk::cce_pair_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pairk::PSMEM) !=
+            cudaSuccess)
       return CCE_ERR_CUDA;
     attr = true;
   }
   const int grid = (h->num_sms / 2) * 2;  // whole CTA pairs
   {
     ProfScope ps(h, s, prof_class);
-    pairk::cce_pair_kernel<<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
+    if (pp.g.adamw)
+      pairk::cce_pair_kernel<1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
+    else
+      pairk::cce_pair_kernel<0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
@@ -634,7 +639,59 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
   return CCE_OK;
 }
 
+static cce_status launch_adamw(const cce_adamw_params* opt, const void* grad, int grad_fp32, int64_t n, void* W_bf16,
+                               cudaStream_t s) {
+  if (n <= 0) return CCE_OK;
+  AdamwArgs a;
+  a.lr = opt->lr; a.b1 = opt->beta1; a.b2 = opt->beta2; a.eps = opt->eps; a.wd = opt->weight_decay;
+  a.bc1 = opt->bias_correction1; a.bc2 = opt->bias_correction2;
+  a.clip = opt->clip_coef; a.master = opt->master; a.m = opt->m; a.v = opt->v; a.grad_in = opt->grad_in;
+  a.grad = grad; a.grad_fp32 = grad_fp32; a.w = static_cast<__nv_bfloat16*>(W_bf16); a.n = n;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long groups = n / 8 > 0 ? n / 8 : 1;
+  k_adamw<<<grid_for(groups, 256, 8 * sms), 256, 0, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+}
+
+static bool adamw_params_ok(const cce_adamw_params* o) {
+  return o && o->m && o->v && o->bias_correction1 > 0.f && o->bias_correction2 > 0.f;
+}
+
+static bool adamw_aligned(const cce_adamw_params* o) {
+  return aligned16(o->m) && aligned16(o->v) && (!o->master || aligned16(o->master)) &&
+         (!o->grad_in || aligned16(o->grad_in));
+}
+
+static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, void* dW, const cce_adamw_params* opt,
+                                void* stream);
+
 cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, void* stream) {
+  return backward_impl(h, dloss, dH, dW, nullptr, stream);
+}
+
+cce_status cce_backward_adamw(cce_handle* h, const float* dloss, void* dH, const cce_adamw_params* opt,
+                              void* stream) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  if (!h->have_fwd) return CCE_ERR_NO_FORWARD;
+  if (!adamw_params_ok(opt)) return CCE_ERR_INVALID_VALUE;
+  if (h->cfg.flags & (CCE_FLAG_ONE_CTA | CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY | CCE_FLAG_ACCUMULATE))
+    return CCE_ERR_UNSUPPORTED;
+  if (!adamw_aligned(opt) || (h->D % 8) != 0 || (opt->W_out && !aligned16(opt->W_out))) return CCE_ERR_UNSUPPORTED;
+  return backward_impl(h, dloss, dH, const_cast<void*>(h->W), opt, stream);
+}
+
+cce_status cce_adamw_step(const cce_adamw_params* opt, const void* grad, int32_t grad_fp32, int64_t n, void* W_bf16,
+                          void* stream) {
+  if (!adamw_params_ok(opt) || n < 0 || (!opt->master && !W_bf16)) return CCE_ERR_INVALID_VALUE;
+  if (!adamw_aligned(opt) || (W_bf16 && !aligned16(W_bf16)) || (grad && !aligned16(grad)))
+    return CCE_ERR_UNSUPPORTED;
+  return launch_adamw(opt, grad, grad_fp32 ? 1 : 0, n, W_bf16, static_cast<cudaStream_t>(stream));
+}
+
+static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, void* dW, const cce_adamw_params* opt,
+                                void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   if (!h->have_fwd) return CCE_ERR_NO_FORWARD;
   if (!dloss || (h->N > 0 && !dH) || (h->V_local > 0 && !dW)) return CCE_ERR_INVALID_VALUE;
@@ -665,6 +722,17 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
     p.dw_fp32 = (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0;
     p.dw_accumulate = (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0;
     p.dloss_c = nullptr;
+    if (opt) {
+      p.adamw = 1;
+      p.lr = opt->lr; p.beta1 = opt->beta1; p.beta2 = opt->beta2; p.eps = opt->eps; p.wd = opt->weight_decay;
+      p.bc1 = opt->bias_correction1; p.bc2 = opt->bias_correction2;
+      p.clip_coef = opt->clip_coef; p.master = opt->master; p.am = opt->m; p.av = opt->v; p.grad_in = opt->grad_in;
+      p.Win = static_cast<const __nv_bfloat16*>(h->W);
+      p.Wout = static_cast<__nv_bfloat16*>(opt->W_out ? opt->W_out : dW);
+      p.adamw_inplace = (p.Wout == p.Win) ? 1 : 0;
+      p.ldw = (int)h->ldw;
+      p.dW = nullptr;
+    }
     if (h->cfg.reduction == CCE_REDUCTION_NONE) {
       ProfScope ps(h, s, 4);
       k_gather_dloss<<<grid_for(L.Npad, 256, 2 * h->num_sms), 256, 0, s>>>(dloss, at<int>(ws, L.idx), nvp,
@@ -762,6 +830,15 @@ cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, v
       if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
     }
     }
+  } else if (V_local > 0 && N == 0 && opt) {
+    // no rows: zero gradient, the optimizer step still applies (decay, moment decay)
+    if (h->ldw != D) return CCE_ERR_UNSUPPORTED;
+    void* wout = opt->W_out ? opt->W_out : dW;
+    if (wout != dW && !opt->master &&
+        cudaMemcpyAsync(wout, dW, (size_t)V_local * D * 2, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return CCE_ERR_CUDA;  // theta is read from W_out below
+    cce_status st = launch_adamw(opt, nullptr, 0, V_local * D, wout, s);
+    if (st != CCE_OK) return st;
   } else if (V_local > 0 && N == 0) {
     // no rows: dW = 0 (unchanged when accumulating)
     if (!(h->cfg.flags & CCE_FLAG_ACCUMULATE) &&

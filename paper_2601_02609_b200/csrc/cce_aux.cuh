@@ -268,4 +268,118 @@ __global__ void k_gather_dloss(const float* __restrict__ dloss, const int* __res
     dloss_c[i] = i < nv ? dloss[idx[i]] : 0.f;
 }
 
+// One AdamW element update in the order of the paper's fused kernel.
+__device__ __forceinline__ void adamw_elem(float g, float& th, float& m, float& v, float lr, float b1, float b2,
+                                           float eps, float wd, float bc1, float bc2) {
+  th = th * (1.f - lr * wd);
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  const float mh = m / bc1;
+  const float vh = v / bc2;
+  th = th - lr * (mh / (sqrtf(vh) + eps));
+}
+
+// Standalone fused AdamW (Alg. Fused AdamW P:2003-2046; cce.h cce_adamw_step): one
+// read and one write of each state array, 8 elements (32-byte vectors) per thread and
+// iteration, grid-stride over n / 8 groups plus a scalar tail.  HBM-bound.
+struct AdamwArgs {
+  float lr, b1, b2, eps, wd, bc1, bc2;
+  const float* clip;
+  float* master;
+  float* m;
+  float* v;
+  const float* grad_in;
+  const void* grad;
+  int grad_fp32;
+  __nv_bfloat16* w;
+  long long n;
+};
+
+__device__ __forceinline__ float adamw_grad_at(const AdamwArgs& a, long long i) {
+  float g = 0.f;
+  if (a.grad) g = a.grad_fp32 ? static_cast<const float*>(a.grad)[i]
+                              : __bfloat162float(static_cast<const __nv_bfloat16*>(a.grad)[i]);
+  if (a.grad_in) g += a.grad_in[i];
+  return g;
+}
+
+__global__ void k_adamw(const AdamwArgs a) {
+  const float clip = a.clip ? *a.clip : 1.f;
+  const long long ngrp = a.n / 8;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < ngrp; gi += stride) {
+    const long long i0 = gi * 8;
+    float g[8], th[8], m[8], v[8];
+    const float4* m4 = reinterpret_cast<const float4*>(a.m + i0);
+    const float4* v4 = reinterpret_cast<const float4*>(a.v + i0);
+    float4 t0 = m4[0], t1 = m4[1];
+    m[0] = t0.x; m[1] = t0.y; m[2] = t0.z; m[3] = t0.w; m[4] = t1.x; m[5] = t1.y; m[6] = t1.z; m[7] = t1.w;
+    t0 = v4[0]; t1 = v4[1];
+    v[0] = t0.x; v[1] = t0.y; v[2] = t0.z; v[3] = t0.w; v[4] = t1.x; v[5] = t1.y; v[6] = t1.z; v[7] = t1.w;
+    if (a.master) {
+      const float4* th4 = reinterpret_cast<const float4*>(a.master + i0);
+      t0 = th4[0]; t1 = th4[1];
+      th[0] = t0.x; th[1] = t0.y; th[2] = t0.z; th[3] = t0.w; th[4] = t1.x; th[5] = t1.y; th[6] = t1.z; th[7] = t1.w;
+    } else {
+      const uint4 wb = *reinterpret_cast<const uint4*>(a.w + i0);
+      const uint32_t w[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        th[2 * k] = __uint_as_float(w[k] << 16);
+        th[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+      }
+    }
+    if (!a.grad) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) g[k] = 0.f;
+    } else if (a.grad_fp32) {
+      const float4* g4 = reinterpret_cast<const float4*>(static_cast<const float*>(a.grad) + i0);
+      t0 = g4[0]; t1 = g4[1];
+      g[0] = t0.x; g[1] = t0.y; g[2] = t0.z; g[3] = t0.w; g[4] = t1.x; g[5] = t1.y; g[6] = t1.z; g[7] = t1.w;
+    } else {
+      const uint4 gb = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.grad) + i0);
+      const uint32_t w[4] = {gb.x, gb.y, gb.z, gb.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        g[2 * k] = __uint_as_float(w[k] << 16);
+        g[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+      }
+    }
+    if (a.grad_in) {
+      const float4* g4 = reinterpret_cast<const float4*>(a.grad_in + i0);
+      t0 = g4[0]; t1 = g4[1];
+      g[0] += t0.x; g[1] += t0.y; g[2] += t0.z; g[3] += t0.w; g[4] += t1.x; g[5] += t1.y; g[6] += t1.z; g[7] += t1.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) adamw_elem(g[k] * clip, th[k], m[k], v[k], a.lr, a.b1, a.b2, a.eps, a.wd, a.bc1, a.bc2);
+    float4* mo = reinterpret_cast<float4*>(a.m + i0);
+    float4* vo = reinterpret_cast<float4*>(a.v + i0);
+    mo[0] = make_float4(m[0], m[1], m[2], m[3]); mo[1] = make_float4(m[4], m[5], m[6], m[7]);
+    vo[0] = make_float4(v[0], v[1], v[2], v[3]); vo[1] = make_float4(v[4], v[5], v[6], v[7]);
+    if (a.master) {
+      float4* to = reinterpret_cast<float4*>(a.master + i0);
+      to[0] = make_float4(th[0], th[1], th[2], th[3]); to[1] = make_float4(th[4], th[5], th[6], th[7]);
+    }
+    if (a.w) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(th[0], th[1]), p1 = __floats2bfloat162_rn(th[2], th[3]);
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(th[4], th[5]), p3 = __floats2bfloat162_rn(th[6], th[7]);
+      *reinterpret_cast<uint4*>(a.w + i0) =
+          make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                     *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+    }
+  }
+  // scalar tail (n % 8 elements)
+  const long long tail = ngrp * 8 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (tail < a.n && tail < ngrp * 8 + 8) {
+    const long long i = tail;
+    float th = a.master ? a.master[i] : __bfloat162float(a.w[i]);
+    float m = a.m[i], v = a.v[i];
+    adamw_elem(adamw_grad_at(a, i) * clip, th, m, v, a.lr, a.b1, a.b2, a.eps, a.wd, a.bc1, a.bc2);
+    a.m[i] = m;
+    a.v[i] = v;
+    if (a.master) a.master[i] = th;
+    if (a.w) a.w[i] = __float2bfloat16_rn(th);
+  }
+}
+
 }  // namespace cce

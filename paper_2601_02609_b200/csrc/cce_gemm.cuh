@@ -74,7 +74,21 @@ struct GemmParams {
   const float* dloss_c; // G: reduction "none": per-row upstream gradients (compact rows), else nullptr
   int dw_fp32;          // DW: dW is float32 (else bf16)
   int dw_accumulate;    // DW: dW += gradient (else overwrite)
+  // fused AdamW in the dW epilogue (pair kernel only; cce.h cce_backward_adamw,
+  // Alg. Fused AdamW P:2003-2046): dW is consumed in registers, W / master / m / v updated
+  int adamw;
+  float lr, beta1, beta2, eps, wd, bc1, bc2;
+  const float* clip_coef;  // device scalar or nullptr (1)
+  float* master;           // [V_local][D] fp32 or nullptr (theta = the bf16 W)
+  float* am;               // [V_local][D] fp32 first moment
+  float* av;               // [V_local][D] fp32 second moment
+  const float* grad_in;    // [V_local][D] fp32 earlier micro-batches' gradient or nullptr
+  const __nv_bfloat16* Win;  // the forward's W (theta when master == nullptr), row stride ldw
+  __nv_bfloat16* Wout;       // bf16(theta_new), row stride ldw: == Win (in place) or a second buffer
+  int ldw;
+  int adamw_inplace;         // Wout == Win: the chunk's dW epilogue waits for its dH items
 };
+
 
 struct TileGeom {
   int tiles_m, tiles_n, num_kb;

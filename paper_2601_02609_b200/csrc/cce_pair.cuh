@@ -353,6 +353,102 @@ __device__ __forceinline__ void epi_dw(const GemmParams& p, uint32_t taddr, cons
   }
 }
 
+// Fused AdamW (Alg. Fused AdamW P:2003-2046): the finished dW
+// tile is the gradient of these W rows; apply the optimizer step to W (and master / m
+// / v) directly instead of writing dW.  Each thread owns one vocabulary row of the
+// tile and walks its columns in 8-wide groups (32-byte vectors per state array).  The
+// caller has already waited for this chunk's dH items, the only other readers of W_c.
+__device__ __forceinline__ void epi_dw_adamw(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it,
+                                             bool have_acc, float clip) {
+  // TMEM hands each thread one ROW of the dW tile (lane = row), which would make every
+  // state access a 32-row scatter (one L1/L2 request per lane: measured 70 us per item,
+  // LSU-bound).  So each warp transposes its 32 x 32 fp32 block through its 4 KB
+  // staging tile (XOR-swizzled, conflict-free both ways) and then walks the block row
+  // by row with lane = column: every m / v / master access is one 128-byte line, every
+  // W access one 64-byte run.  ROWS_IN_FLIGHT rows of state are loaded before use.
+#ifndef CCE_ADAMW_RIF
+#define CCE_ADAMW_RIF 16
+#endif
+  constexpr int RIF = CCE_ADAMW_RIF;
+  const int c0 = it.c * p.C;
+  const int width = min(p.C, p.V_local - c0);
+  const int hw = it.N / 2;
+  const int cb = e.half * hw;
+  const int lane = e.rit & 31;
+  const int row0 = it.m0 + e.rank * HM + e.q * 32;  // first vocabulary row (within the chunk) of this warp
+  const int nrows = max(0, min(32, width - row0));
+  float* stg = reinterpret_cast<float*>(e.stage);   // [32 rows][32 cols], column XOR row
+#pragma unroll 1
+  for (int j = 0; j < hw / 32; ++j) {
+    const int d0 = it.n0 + cb + j * 32;
+    float acc[32];
+    if (have_acc) {
+      tmem_ld32(taddr + cb + j * 32, acc);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+    }
+    if (d0 >= p.D || nrows == 0) continue;  // warp-uniform
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 32; ++c) stg[lane * 32 + (c ^ lane)] = acc[c];
+    __syncwarp();
+    const int d = d0 + lane;
+    if (p.grad_in) {  // earlier micro-batches' gradient, added in place in the staging tile
+#pragma unroll 4
+      for (int rr = 0; rr < nrows; ++rr)
+        stg[rr * 32 + (lane ^ rr)] += __ldcs(p.grad_in + (size_t)(c0 + row0 + rr) * p.D + d);
+    }
+#pragma unroll 1
+    for (int r0 = 0; r0 < nrows; r0 += RIF) {
+      float m[RIF], v[RIF], th[RIF];
+#pragma unroll
+      for (int r = 0; r < RIF; ++r) {
+        if (r0 + r < nrows) {
+          const size_t off = (size_t)(c0 + row0 + r0 + r) * p.D + d;
+          m[r] = __ldcs(p.am + off);
+          v[r] = __ldcs(p.av + off);
+          th[r] = p.master ? __ldcs(p.master + off)
+                           : __bfloat162float(p.Win[(size_t)(c0 + row0 + r0 + r) * p.ldw + d]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RIF; ++r) {
+        if (r0 + r < nrows) {
+          const int rr = r0 + r;
+          const float gr = stg[rr * 32 + (lane ^ rr)] * clip;
+          adamw_elem(gr, th[r], m[r], v[r], p.lr, p.beta1, p.beta2, p.eps, p.wd, p.bc1, p.bc2);
+          const size_t off = (size_t)(c0 + row0 + rr) * p.D + d;
+          __stcs(p.am + off, m[r]);
+          __stcs(p.av + off, v[r]);
+          if (p.master) __stcs(p.master + off, th[r]);
+          p.Wout[(size_t)(c0 + row0 + rr) * p.ldw + d] = __float2bfloat16_rn(th[r]);
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Fused AdamW: before waiting for a DW item's accumulator, each epilogue thread pulls its
+// row segment of the optimizer state (m, v, master or the bf16 theta) into L2, so the
+// epilogue's loads hit L2 instead of HBM and the HBM reads overlap the item's MMAs.
+__device__ __forceinline__ void prefetch_dw_adamw(const GemmParams& p, const PEpi& e, const PItem& it) {
+  const int c0 = it.c * p.C;
+  const int width = min(p.C, p.V_local - c0);
+  const int vrow = it.m0 + e.rank * HM + e.rit;
+  const int hw = it.N / 2;
+  const int d0 = it.n0 + e.half * hw;
+  if (vrow >= width || d0 >= p.D) return;
+  const int cols = min(hw, p.D - d0);
+  const size_t off = (size_t)(c0 + vrow) * p.D + d0;
+  bulk_prefetch_l2(p.am + off, cols * 4);
+  bulk_prefetch_l2(p.av + off, cols * 4);
+  if (p.master) bulk_prefetch_l2(p.master + off, cols * 4);
+  else bulk_prefetch_l2(p.Win + (size_t)(c0 + vrow) * p.ldw + d0, cols * 2);
+  if (p.grad_in) bulk_prefetch_l2(p.grad_in + off, cols * 4);
+}
+
 __device__ __forceinline__ void epi_dh(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv) {
   const int t = it.m0 + e.rank * HM + e.rit;  // compact row
   const int hw = it.N / 2;
@@ -452,6 +548,9 @@ __device__ __forceinline__ void mma_item(const PItem& it, uint64_t* full_bar, ui
 }
 
 // ------------------------------------------------------------------ kernel
+// ADAMW = 1: the backward queue with AdamW fused into the dW epilogue (cce_backward_adamw);
+// a separate instantiation so its epilogue's register demand leaves the default kernel alone.
+template <int ADAMW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     cce_pair_kernel(const __grid_constant__ CUtensorMap tmHcK, const __grid_constant__ CUtensorMap tmWK,
                     const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
@@ -696,6 +795,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     const float scale = (P.mode == 1 && k.nv > 0 && g.reduction != 2)
                             ? (g.reduction == 1 ? *g.dloss : (*g.dloss) / (float)k.nv)
                             : 0.f;  // reduction "none": per-row dloss_c in epi_g
+    const float clip = (ADAMW && g.clip_coef) ? *g.clip_coef : 1.f;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     uint32_t rs = 0, rph = 0;
     int acc_it = 0;
@@ -711,6 +811,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       if (++rs == PRING) { rs = 0; rph ^= 1; }
       if (it.type == PT_END) break;
       const bool have_acc = it.num_kb > 0;
+      if (ADAMW && it.type == PT_DW && !(P.strict & 8192)) prefetch_dw_adamw(g, e, it);
       uint32_t acc = 0;
       if (have_acc) {
         acc = acc_it & 1;
@@ -729,11 +830,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       if (P.strict & 4) {
         // debug: skip the epilogue entirely (no TMEM reads, no stores)
       } else if (it.type == PT_FWD) {
-        epi_fwd(g, taddr, e, it, k.nv);
+        if constexpr (!ADAMW) epi_fwd(g, taddr, e, it, k.nv);
       } else if (it.type == PT_G) {
         if (!(P.strict & 32)) epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
       } else if (it.type == PT_DW) {
-        epi_dw(g, taddr, e, it, have_acc);
+        if constexpr (ADAMW) {
+          // the chunk's dH tiles read W_c through the TMA: the update waits until every
+          // DH(c, row tile, this hidden tile) item is complete (earlier in the queue)
+          if (g.adamw_inplace && warp == 4 && !(P.strict & 1792)) {
+            const int dt = it.n0 / PN;
+            for (int rt = lane; rt < k.t256; rt += 32) wait_ge(&dh_flag[rt * k.n_dt + dt], 2 * (it.c + 1));
+          }
+          named_bar_sync(2, PEPI_THREADS);
+          epi_dw_adamw(g, taddr, e, it, have_acc, clip);
+        } else {
+          epi_dw(g, taddr, e, it, have_acc);
+        }
       } else {
         // DH(c-1, tile) halves published; re-acquire so the .cg loads below see them
         if (leader && !(P.strict & 1792)) wait_ge(&dh_flag[it.tile_id], 2 * it.c);

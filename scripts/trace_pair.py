@@ -25,9 +25,24 @@ h = cce.CCEHandle(vocab_total=c.V, flags=int(os.environ.get("CCE_FLAGS", "0")))
 dH = torch.empty(H.shape, dtype=torch.bfloat16, device=dev)
 dW = torch.empty(W.shape, dtype=torch.bfloat16, device=dev)
 one = torch.ones((), dtype=torch.float32, device=dev)
+ADAMW = os.environ.get("CCE_ADAMW")  # "1": fused AdamW, W in place; "2": W_out double buffer
+if ADAMW:
+    st = {k: torch.zeros(W.shape, dtype=torch.float32, device=dev) for k in ("m", "v")}
+    master = W.float()
+    W2 = torch.empty_like(W)
+    opt = cce.adamw_params(st["m"], st["v"], lr=1e-6, step=1, master=master, W_out=W2 if ADAMW == "2" else None)
+
+
+def bwd():
+    if ADAMW:
+        h.backward_adamw(one, dH, opt)
+    else:
+        h.backward(one, dH, dW)
+
+
 for _ in range(3):
     h.forward(H, W, y)
-    h.backward(one, dH, dW)
+    bwd()
 CAP = 60000
 buf = torch.zeros(2 * CAP * 128, dtype=torch.uint8, device=dev)
 cce.cce_debug_trace(h.h, buf)
@@ -35,7 +50,7 @@ ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 ev[0].record()
 h.forward(H, W, y)
 ev[1].record()
-h.backward(one, dH, dW)
+bwd()
 ev[2].record()
 torch.cuda.synchronize()
 cce.cce_debug_trace(h.h, None)

@@ -76,6 +76,21 @@ def test_host_validation_without_gpu(lib):
     cfg.reduction = 0
     assert lib.cce_forward(None, None, 0, 64, 64, None, 0, 64, None, None, None, None, None, 0, None) == 1
     assert lib.cce_backward(None, None, None, None, None) == 1
+    # fused AdamW entry points: NULL handle / params, missing moments,
+    # bias corrections not in (0, 1], theta missing (no master and no bf16 W)
+    opt = cce.cce_adamw_params()
+    assert lib.cce_backward_adamw(None, None, None, ctypes.byref(opt), None) == 1
+    assert lib.cce_adamw_step(None, None, 0, 16, None, None) == 1
+    opt.bias_correction1 = opt.bias_correction2 = 0.1
+    assert lib.cce_adamw_step(ctypes.byref(opt), None, 0, 16, None, None) == 1           # m, v NULL
+    opt.m, opt.v = 16, 16
+    assert lib.cce_adamw_step(ctypes.byref(opt), None, 0, 16, None, None) == 1           # no theta
+    assert lib.cce_adamw_step(ctypes.byref(opt), None, 0, -1, ctypes.c_void_p(16), None) == 1  # n < 0
+    opt.bias_correction2 = 0.0
+    assert lib.cce_adamw_step(ctypes.byref(opt), None, 0, 16, ctypes.c_void_p(16), None) == 1
+    opt.bias_correction2 = 0.1
+    opt.m = 8                                                                               # misaligned
+    assert lib.cce_adamw_step(ctypes.byref(opt), None, 0, 16, ctypes.c_void_p(16), None) == 2
     assert lib.cce_workspace_bytes(None, 10, 64, 10) == 0
     assert lib.cce_host_staging_bytes(-1, 64) == 0
     assert lib.cce_status_string(3) == b"CCE_ERR_LABEL_RANGE"

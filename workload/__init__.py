@@ -251,3 +251,16 @@ def make_config(name: str, seed: int = 42, regime: str = "flat", ignore: str | N
     c = CONFIGS[name]
     return make_problem(c.N, c.D, c.V, seed=seed, regime=regime, n_rows=c.n_rows,
                         ignore=ignore if ignore is not None else c.ignore, w_rows=w_rows)
+
+
+S_ADAM_M, S_ADAM_V = 101, 102
+
+
+def make_adamw_state(seed: int, shape, g_scale: float):
+    """Warm AdamW moments (SURVEY 8(f) NEXT #2 test inputs), float32 arrays of `shape`:
+    m ~ 0.5 g_scale N(0,1) and v ~ g_scale^2 U(0.5, 2), i.e. the state after a few steps
+    with gradients of rms g_scale (v > 0 keeps the update a smooth function of g)."""
+    n = int(np.prod(shape))
+    m = (0.5 * g_scale * normal_f64(seed, S_ADAM_M, 0, n)).astype(np.float32).reshape(shape)
+    v = ((g_scale * g_scale) * (0.5 + 1.5 * uniform01(seed, S_ADAM_V, 0, n))).astype(np.float32).reshape(shape)
+    return m, v
