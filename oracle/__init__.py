@@ -72,6 +72,12 @@ def lib():
         L.oracle_partial_stats.restype = ctypes.c_int
         L.oracle_adamw_step.argtypes = [p, p, p, p, i64, f64, f64, f64, f64, f64, f64, f64, f64]
         L.oracle_adamw_step.restype = None
+        L.oracle_rmsnorm_fwd.argtypes = [p, p, i64, i64, f64, p, p]
+        L.oracle_rmsnorm_fwd.restype = None
+        L.oracle_rmsnorm_bwd.argtypes = [p, p, p, p, p, i64, i64, p, p]
+        L.oracle_rmsnorm_bwd.restype = None
+        L.oracle_to_bf16.argtypes = [p, i64, p]
+        L.oracle_to_bf16.restype = None
         L.oracle_validate.argtypes = [p, i64, i64, i32, p]
         L.oracle_validate.restype = ctypes.c_int
         L.oracle_num_threads.argtypes = []
@@ -208,3 +214,53 @@ def adamw_step(theta, grad, m, v, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_d
     lib().oracle_adamw_step(_ptr(th), _ptr(g), _ptr(mm), _ptr(vv), th.size, float(lr), float(beta1), float(beta2),
                             float(eps), float(weight_decay), float(clip_coef), bc1, bc2)
     return th, mm, vv
+
+
+# ----------------------------------------------------------------- RMSNorm prologue (NEXT #4)
+def rmsnorm_fwd(x, gamma, eps=1e-6):
+    """Def. RMSNorm (P:220-224): returns (y [N,D], rstd [N]) in fp64 (oracle_rmsnorm_fwd)."""
+    X = _bits(x)
+    if X.ndim == 1:
+        X = X[None, :]
+    g = _bits(gamma)
+    N, D = X.shape
+    assert g.shape == (D,)
+    y = np.zeros((N, D), np.float64)
+    r = np.zeros(N, np.float64)
+    lib().oracle_rmsnorm_fwd(_ptr(X), _ptr(g), N, D, float(eps), _ptr(y), _ptr(r))
+    return y, r
+
+
+def rmsnorm_bwd(dy, x, gamma, rstd, skip=None):
+    """Exact gradient of Def. RMSNorm (oracle_rmsnorm_bwd; reading R18): (dx, dgamma) fp64."""
+    X = _bits(x)
+    g = _bits(gamma)
+    dY = np.ascontiguousarray(dy, dtype=np.float64)
+    N, D = X.shape
+    r = np.ascontiguousarray(rstd, dtype=np.float64)
+    sk = None if skip is None else np.ascontiguousarray(skip, dtype=np.int32)
+    dx = np.zeros((N, D), np.float64)
+    dg = np.zeros(D, np.float64)
+    lib().oracle_rmsnorm_bwd(_ptr(dY), _ptr(X), _ptr(g), _ptr(r), _ptr(sk), N, D, _ptr(dx), _ptr(dg))
+    return dx, dg
+
+
+def to_bf16(a):
+    """fp64 -> bf16 bit patterns (uint16), round to nearest even via fp32."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    out = np.zeros(a.shape, np.uint16)
+    lib().oracle_to_bf16(_ptr(a), a.size, _ptr(out))
+    return out
+
+
+def cce_rmsnorm(X_bits, gamma_bits, W_bits, labels, eps=1e-6, ignore_index=-100, dloss=1.0):
+    """The path with the RMSNorm prologue: H = bf16(RMSNorm(X)) (the CE path consumes bf16
+    H), the plain CE oracle on H, then the RMSNorm backward of its dH.  Returns
+    oracle.cce's dict plus dX [N,D], dgamma [D], rstd [N] and H_bits."""
+    y, rstd = rmsnorm_fwd(X_bits, gamma_bits, eps)
+    H_bits = to_bf16(y)
+    out = cce(H_bits, W_bits, labels, ignore_index=ignore_index, dloss=dloss)
+    skip = (np.asarray(labels) == ignore_index).astype(np.int32)
+    dx, dg = rmsnorm_bwd(out["dH"], X_bits, gamma_bits, rstd, skip)
+    out.update(dX=dx, dgamma=dg, rstd=rstd, H_bits=H_bits)
+    return out

@@ -429,3 +429,65 @@ void oracle_adamw_step(double *theta, const double *grad, double *m, double *v, 
         theta[i] = th - lr * (mh / (sqrt(vh) + eps));
     }
 }
+
+/*
+ * RMSNorm prologue ("the final-RMSNorm prologue, the step before
+ * the path: norm H on load, with rstd cached").  Def. Root Mean Square Layer
+ * Normalization:
+ *   r_n    = sqrt((1/D) sum_i x[n,i]^2 + eps),   rstd_n = 1 / r_n   (Alg. P:722-724)
+ *   y[n,i] = x[n,i] * rstd_n * gamma_i                                   (Alg. P:725)
+ * In place of nothing: y, rstd out; fp64.
+ */
+void oracle_rmsnorm_fwd(const double *x, const double *gamma, int64_t N, int64_t D, double eps, double *y,
+                        double *rstd) {
+    for (int64_t n = 0; n < N; ++n) {
+        const double *xr = x + n * D;
+        double ss = 0.0;
+        for (int64_t i = 0; i < D; ++i) ss += xr[i] * xr[i];
+        const double r = sqrt(ss / (double)D + eps);
+        rstd[n] = 1.0 / r;
+        for (int64_t i = 0; i < D; ++i) y[n * D + i] = xr[i] * rstd[n] * gamma[i];
+    }
+}
+
+/*
+ * RMSNorm backward: the exact gradient of Def. RMSNorm.  With
+ * xbar = x rstd and dy the upstream gradient of y:
+ *   dx[n,k]  = rstd_n (gamma_k dy[n,k] - xbar[n,k] (1/D) sum_i dy[n,i] gamma_i xbar[n,i])
+ *   dgamma_k = sum_n dy[n,k] xbar[n,k]                        (Alg. P:745, summed over rows)
+ * This is Prop. "RMSNorm Backward Pass" and the Alg. with two
+ * garbles corrected (reading R18): the Prop. drops the 1/D of the mean and
+ * both apply gamma_k to the second term as well.  Differentiating y_i = x_i gamma_i / r,
+ * r = sqrt(mean x^2 + eps): dy_i/dx_k = gamma_i delta_ik / r - x_i gamma_i x_k / (D r^3),
+ * which gives the line above.  Rows with skip[n] != 0 (ignored rows, never read by the
+ * CE path) get dx = 0 and add nothing to dgamma.  fp64, fixed order.
+ */
+void oracle_rmsnorm_bwd(const double *dy, const double *x, const double *gamma, const double *rstd,
+                        const int32_t *skip, int64_t N, int64_t D, double *dx, double *dgamma) {
+    for (int64_t i = 0; i < D; ++i) dgamma[i] = 0.0;
+    for (int64_t n = 0; n < N; ++n) {
+        double *dxr = dx + n * D;
+        if (skip && skip[n]) {
+            for (int64_t i = 0; i < D; ++i) dxr[i] = 0.0;
+            continue;
+        }
+        const double *xr = x + n * D, *dyr = dy + n * D;
+        const double rs = rstd[n];
+        double c1 = 0.0;
+        for (int64_t i = 0; i < D; ++i) c1 += dyr[i] * gamma[i] * (xr[i] * rs);
+        c1 /= (double)D;
+        for (int64_t k = 0; k < D; ++k) dxr[k] = rs * (gamma[k] * dyr[k] - (xr[k] * rs) * c1);
+        for (int64_t k = 0; k < D; ++k) dgamma[k] += dyr[k] * (xr[k] * rs);
+    }
+}
+
+/* fp64 -> bf16 bit pattern, round to nearest even (the CE path consumes bf16 H). */
+void oracle_to_bf16(const double *a, int64_t n, uint16_t *out) {
+    for (int64_t i = 0; i < n; ++i) {
+        const float f = (float)a[i];   /* fp64 -> fp32 (RNE), then fp32 -> bf16 (RNE) */
+        uint32_t u;
+        memcpy(&u, &f, 4);
+        u += 0x7FFFu + ((u >> 16) & 1u);
+        out[i] = (uint16_t)(u >> 16);
+    }
+}

@@ -29,6 +29,13 @@ muts+=(
  's/double vh = v\[i\] \/ bc2;/double vh = v[i];/'                                # dropped bias correction
  's/theta\[i\] = th - lr \* (mh \/ (sqrt(vh) + eps));/theta[i] = th - lr * (mh \/ sqrt(vh + eps));/'  # eps inside sqrt
 )
+# RMSNorm prologue (oracle_rmsnorm_fwd / _bwd)
+muts+=(
+ 's/const double r = sqrt(ss \/ (double)D + eps);/const double r = sqrt(ss + eps);/'          # dropped 1\/D (the Prop. garble)
+ 's/for (int64_t k = 0; k < D; ++k) dxr\[k\] = rs \* (gamma\[k\] \* dyr\[k\] - (xr\[k\] \* rs) \* c1);/for (int64_t k = 0; k < D; ++k) dxr[k] = rs * gamma[k] * (dyr[k] - (xr[k] * rs) * c1);/'  # gamma on both terms (the Alg. garble)
+ 's/c1 \/= (double)D;/c1 \/= 1.0;/'                                                       # dropped mean in c1
+ 's/dgamma\[k\] += dyr\[k\] \* (xr\[k\] \* rs);/dgamma[k] += dyr[k] * xr[k];/'           # dgamma without rstd
+)
 fail=0
 for m in "${muts[@]}"; do
   cp /tmp/oracle_orig.c oracle/cce_oracle.c

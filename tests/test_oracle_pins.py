@@ -496,3 +496,101 @@ def test_adamw_matches_torch_fp64(step, clip):
     # torch forms m with lerp (m + (1 - b1)(g - m)): same value, different rounding
     np.testing.assert_allclose(m, st["exp_avg"].numpy(), rtol=1e-12, atol=1e-30)
     np.testing.assert_allclose(v, st["exp_avg_sq"].numpy(), rtol=1e-12, atol=1e-30)
+
+
+# ---------------------------------------------------------------- RMSNorm prologue (NEXT #4)
+def test_rmsnorm_spec_worked_examples():
+    """S:118-120: x=[1,1,1,1], gamma=1, eps=0 -> y=x, rstd=1; x=[3,4] -> rstd=1/3.5355,
+    y=[0.8485, 1.1314] (mean square 12.5); scale invariance for eps=0."""
+    y, r = oracle.rmsnorm_fwd(np.ones((1, 4)), np.ones(4), 0.0)
+    assert np.all(y == 1.0) and r[0] == 1.0
+    y, r = oracle.rmsnorm_fwd(np.array([[3.0, 4.0]]), np.ones(2), 0.0)
+    assert abs(1.0 / r[0] - 3.5355) <= 5e-5 and abs(1.0 / r[0] - math.sqrt(12.5)) <= 1e-15
+    np.testing.assert_allclose(y[0], [0.8485, 1.1314], atol=5e-5)
+    x = np.random.default_rng(0).standard_normal((3, 16))
+    g = np.random.default_rng(1).standard_normal(16)
+    np.testing.assert_allclose(oracle.rmsnorm_fwd(7.5 * x, g, 0.0)[0], oracle.rmsnorm_fwd(x, g, 0.0)[0],
+                               rtol=1e-14, atol=1e-15)
+
+
+def test_rmsnorm_backward_special_cases():
+    """S:125-127: dy = 0 -> dx = 0, dgamma = 0; D = 1, eps = 0, gamma = 1: y = sign(x) is
+    constant, so dx = 0 exactly (up to rounding of x rstd = +-1)."""
+    x = np.array([[2.5], [-0.7]])
+    y, r = oracle.rmsnorm_fwd(x, np.ones(1), 0.0)
+    np.testing.assert_array_equal(y[:, 0], [1.0, -1.0])
+    dx, dg = oracle.rmsnorm_bwd(np.array([[0.3], [1.1]]), x, np.ones(1), r)
+    assert np.all(np.abs(dx) <= 1e-16)
+    dx, dg = oracle.rmsnorm_bwd(np.zeros((2, 1)), x, np.ones(1), r)
+    assert np.all(dx == 0) and np.all(dg == 0)
+
+
+@pytest.mark.parametrize("N,D,eps", [(5, 8, 1e-6), (3, 64, 1e-5), (4, 7, 0.3)])
+def test_rmsnorm_matches_torch_autograd_fp64(N, D, eps):
+    """Library routine: torch fp64 autograd of y = x rsqrt(mean(x^2) + eps) gamma, gamma != 1
+    (so a gamma applied to the wrong term, as in the paper's garbled Prop., fails)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(N * D)
+    x = rng.standard_normal((N, D)) * 3.0
+    g = 1.0 + rng.standard_normal(D)
+    dy = rng.standard_normal((N, D))
+    xt = torch.tensor(x, requires_grad=True)
+    gt = torch.tensor(g, requires_grad=True)
+    yt = xt * torch.rsqrt((xt * xt).mean(dim=1, keepdim=True) + eps) * gt
+    yt.backward(torch.tensor(dy))
+    y, r = oracle.rmsnorm_fwd(x, g, eps)
+    np.testing.assert_allclose(y, yt.detach().numpy(), rtol=1e-13, atol=1e-14)
+    dx, dg = oracle.rmsnorm_bwd(dy, x, g, r)
+    np.testing.assert_allclose(dx, xt.grad.numpy(), rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(dg, gt.grad.numpy(), rtol=1e-11, atol=1e-13)
+
+
+def test_rmsnorm_finite_differences():
+    """random (x, gamma, dy), D = 8: dx and dgamma match central finite differences
+    of <dy, rmsnorm(x)> within 1e-6 relative."""
+    rng = np.random.default_rng(3)
+    N, D, eps = 3, 8, 1e-3
+    x = rng.standard_normal((N, D))
+    g = rng.standard_normal(D)
+    dy = rng.standard_normal((N, D))
+    f = lambda xx, gg: float(np.sum(dy * oracle.rmsnorm_fwd(xx, gg, eps)[0]))  # noqa: E731
+    dx, dg = oracle.rmsnorm_bwd(dy, x, g, oracle.rmsnorm_fwd(x, g, eps)[1])
+    h = 1e-6
+    fx = np.zeros_like(x)
+    for i in range(N):
+        for j in range(D):
+            e = np.zeros_like(x)
+            e[i, j] = h
+            fx[i, j] = (f(x + e, g) - f(x - e, g)) / (2 * h)
+    fg = np.array([(f(x, g + h * np.eye(D)[j]) - f(x, g - h * np.eye(D)[j])) / (2 * h) for j in range(D)])
+    assert np.linalg.norm(dx - fx) / np.linalg.norm(fx) <= 1e-6
+    assert np.linalg.norm(dg - fg) / np.linalg.norm(fg) <= 1e-6
+
+
+def test_rmsnorm_skipped_rows_and_composite():
+    """Ignored rows (never read by the CE path) get dx = 0 and add nothing to dgamma; the
+    composite oracle (bf16 H = RMSNorm(X), CE, RMSNorm backward) equals torch fp64 autograd
+    through the same bf16 rounding of H (straight-through: rounding treated as identity in
+    the gradient, which is what consuming a bf16 activation means)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(7)
+    N, D, V = 12, 16, 40
+    X = workload.f32_to_bf16_bits((rng.standard_normal((N, D)) * 2.0).astype(np.float32))
+    G = workload.f32_to_bf16_bits((1.0 + 0.3 * rng.standard_normal(D)).astype(np.float32))
+    W = workload.f32_to_bf16_bits((rng.standard_normal((V, D)) / 4.0).astype(np.float32))
+    y = rng.integers(0, V, N).astype(np.int32)
+    y[[1, 5, 6]] = -100
+    r = oracle.cce_rmsnorm(X, G, W, y, eps=1e-6)
+    assert np.all(r["dX"][[1, 5, 6]] == 0.0)
+    f = lambda b: (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    xt = torch.tensor(f(X), requires_grad=True)
+    gt = torch.tensor(f(G), requires_grad=True)
+    Wt = torch.tensor(f(W))
+    yn = xt * torch.rsqrt((xt * xt).mean(dim=1, keepdim=True) + 1e-6) * gt
+    Hq = torch.tensor(f(r["H_bits"]))
+    Hst = yn + (Hq - yn).detach()          # forward value = bf16 H, gradient straight through
+    loss = torch.nn.functional.cross_entropy(Hst @ Wt.T, torch.tensor(y, dtype=torch.long), ignore_index=-100)
+    loss.backward()
+    assert abs(float(loss) - r["loss"]) <= 1e-12
+    np.testing.assert_allclose(r["dX"], xt.grad.numpy(), rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(r["dgamma"], gt.grad.numpy(), rtol=1e-10, atol=1e-14)
