@@ -176,6 +176,41 @@ cce_status cce_forward(cce_handle *h,
 cce_status cce_backward(cce_handle *h, const float *dloss, void *dH, void *dW, void *stream);
 
 /*
+ * RMSNorm prologue (the step before the path).  The forward takes
+ * the un-normalised final hidden states X [N, D] (bf16, row stride ldx) and the scale
+ * gamma [D] (bf16) and runs the path on H = bf16(RMSNorm(X)), Def. RMSNorm:
+ *   rstd_n = 1 / sqrt((1/D) sum_i X[n,i]^2 + eps),  H[n,i] = (X[n,i] rstd_n) gamma_i
+ * in fp32 (Alg. Fused RMSNorm Forward), fused into the gather of the valid
+ * rows (ignored rows are never read) with rstd cached in the workspace ("Cache rstd for
+ * backward").  eps >= 0; D <= 8192; gamma 16-byte aligned.  Other arguments and
+ * outputs as cce_forward.  X and gamma must stay alive and unmodified until the matching
+ * backward has been enqueued.
+ */
+cce_status cce_forward_rmsnorm(cce_handle *h,
+                               const void *X, int64_t N, int64_t D, int64_t ldx,
+                               const void *gamma, float eps,
+                               const void *W, int64_t V_local, int64_t ldw,
+                               const int32_t *labels,
+                               float *loss, float *lse, int32_t *n_valid,
+                               void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Backward through the loss AND the RMSNorm prologue, from the unrounded fp32 dH
+ * (never rounded to bf16 in between).  With xbar = X rstd and g = dL/dH (DESIGN.md
+ * reading R18: the exact gradient of Def. RMSNorm; the paper's Prop. P:227-233 and
+ * Alg. P:737-746 are garbled):
+ *   dX[n,k]   = rstd_n (gamma_k g[n,k] - xbar[n,k] (1/D) sum_i g[n,i] gamma_i xbar[n,i])
+ *   dgamma[k] = sum_{valid n} g[n,k] xbar[n,k]                        (Alg. P:745)
+ *   dX     [N, D] bf16 (float32 with CCE_FLAG_GRAD_FP32), dense; ignored rows 0
+ *   dgamma [D] bf16 (float32 with CCE_FLAG_GRAD_FP32)
+ *   dW     as cce_backward
+ * CCE_FLAG_ACCUMULATE adds into dX / dgamma / dW (ignored rows of dX untouched).
+ * Deterministic (fixed-order reductions).  Requires that the last forward on `h` was
+ * cce_forward_rmsnorm (else CCE_ERR_NO_FORWARD).
+ */
+cce_status cce_backward_rmsnorm(cce_handle *h, const float *dloss, void *dX, void *dgamma, void *dW, void *stream);
+
+/*
  * Fused AdamW.  The update is the paper's fused kernel,
  * Alg. "Fused AdamW Triton Kernel (Complete)", which is Def. AdamW
  * with a pre-computed clipping coefficient, per element:

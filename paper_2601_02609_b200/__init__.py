@@ -28,7 +28,8 @@ STATUS = {0: "CCE_OK", 1: "CCE_ERR_INVALID_VALUE", 2: "CCE_ERR_UNSUPPORTED", 3: 
 EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_bytes", "cce_forward", "cce_backward",
            "cce_get_error", "cce_host_staging_bytes", "cce_step_host", "cce_nccl_unique_id", "cce_nccl_comm_init",
            "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info",
-           "cce_profile_enable", "cce_profile_read", "cce_debug_trace", "cce_backward_adamw", "cce_adamw_step"]
+           "cce_profile_enable", "cce_profile_read", "cce_debug_trace", "cce_backward_adamw", "cce_adamw_step",
+           "cce_forward_rmsnorm", "cce_backward_rmsnorm"]
 PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 # "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
 # FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
@@ -89,6 +90,10 @@ def lib():
         L.cce_forward.restype = st
         L.cce_backward.argtypes = [p, p, p, p, p]
         L.cce_backward.restype = st
+        L.cce_forward_rmsnorm.argtypes = [p, p, i64, i64, i64, p, ctypes.c_float, p, i64, i64, p, p, p, p, p, sz, p]
+        L.cce_forward_rmsnorm.restype = st
+        L.cce_backward_rmsnorm.argtypes = [p, p, p, p, p, p]
+        L.cce_backward_rmsnorm.restype = st
         L.cce_backward_adamw.argtypes = [p, p, p, ctypes.POINTER(cce_adamw_params), p]
         L.cce_backward_adamw.restype = st
         L.cce_adamw_step.argtypes = [ctypes.POINTER(cce_adamw_params), p, i32, i64, p, p]
@@ -172,6 +177,20 @@ def cce_forward(h, H, W, labels, loss, lse, n_valid, workspace, stream=None):
     _check(lib().cce_forward(h, _ptr(H), N, D, H.stride(0), _ptr(W), V_local, W.stride(0), _ptr(labels), _ptr(loss),
                              _ptr(lse), _ptr(n_valid), _ptr(workspace), workspace.numel() * workspace.element_size(),
                              _stream(stream)), "cce_forward")
+
+
+def cce_forward_rmsnorm(h, X, gamma, eps, W, labels, loss, lse, n_valid, workspace, stream=None):
+    N, D = X.shape
+    V_local = W.shape[0]
+    _check(lib().cce_forward_rmsnorm(h, _ptr(X), N, D, X.stride(0), _ptr(gamma), float(eps), _ptr(W), V_local,
+                                     W.stride(0), _ptr(labels), _ptr(loss), _ptr(lse), _ptr(n_valid),
+                                     _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream)),
+           "cce_forward_rmsnorm")
+
+
+def cce_backward_rmsnorm(h, dloss, dX, dgamma, dW, stream=None):
+    _check(lib().cce_backward_rmsnorm(h, _ptr(dloss), _ptr(dX), _ptr(dgamma), _ptr(dW), _stream(stream)),
+           "cce_backward_rmsnorm")
 
 
 def cce_backward(h, dloss, dH, dW, stream=None):
@@ -305,6 +324,21 @@ class CCEHandle:
 
     def backward(self, dloss, dH, dW, stream=None):
         cce_backward(self.h, dloss, dH, dW, stream)
+
+    def forward_rmsnorm(self, X, gamma, eps, W, labels, want_lse=True, stream=None):
+        """The path on H = bf16(RMSNorm(X)) (gamma: [D] bf16); rstd cached for the backward."""
+        import torch
+        N, D = X.shape
+        ws = self.workspace(N, D, W.shape[0], X.device)
+        loss = (torch.empty(N, dtype=torch.float32, device=X.device) if self.reduction == REDUCTION_NONE
+                else torch.empty((), dtype=torch.float32, device=X.device))
+        lse = torch.empty(N, dtype=torch.float32, device=X.device) if want_lse else None
+        nv = torch.empty((), dtype=torch.int32, device=X.device)
+        cce_forward_rmsnorm(self.h, X, gamma, eps, W, labels, loss, lse, nv, ws, stream)
+        return loss, lse, nv
+
+    def backward_rmsnorm(self, dloss, dX, dgamma, dW, stream=None):
+        cce_backward_rmsnorm(self.h, dloss, dX, dgamma, dW, stream)
 
     def backward_adamw(self, dloss, dH, opt: cce_adamw_params, stream=None):
         """Backward with AdamW fused into the dW epilogue: the W given to the last forward

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -37,6 +38,12 @@ struct cce_handle {
   int64_t N = 0, D = 0, V_local = 0, ldw = 0;
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  // RMSNorm prologue (cce_forward_rmsnorm): the un-normalised rows and the scale, saved
+  // for cce_backward_rmsnorm
+  bool norm = false;
+  const void* nX = nullptr;
+  int64_t ldx = 0;
+  const void* gamma = nullptr;
   int64_t launches = 0;
   int quad_clusters = -1;           // co-resident 4-CTA clusters (queried once)
   cudaStream_t side = nullptr;      // forked stream for the NP = 1 co-launch
@@ -191,13 +198,15 @@ Nccl& nccl() {
 
 // ------------------------------------------------------------------ workspace layout
 namespace {
+constexpr int RMS_GP = 256;  // blocks of the RMSNorm backward (dgamma partials)
+
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
   int64_t Npad, Tv, C;
   int64_t n_chunks, sched_ints;
   size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, dloss_c, gbuf,
-      dH32, sched, total;
+      dH32, sched, rstd_c, gpart, total;
 };
 
 Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots) {
@@ -234,6 +243,8 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
   // backward work queue: head | g_done[n] | w_done[n] | dh_flag[tiles_d * ceil(Npad/BN)]
   L.sched_ints = 2 + 2 * L.n_chunks + ((D + BM - 1) / BM) * ((L.Npad + BN - 1) / BN);
   L.sched = take((size_t)L.sched_ints * 4);
+  L.rstd_c = take((size_t)L.Npad * 4);            // RMSNorm prologue: rstd per compact row
+  L.gpart = take((size_t)RMS_GP * D * 4);          // RMSNorm backward: per-block dgamma partials
   L.total = o;
   return L;
 }
@@ -511,9 +522,38 @@ cce_status cce_profile_read(cce_handle* h, double* ms_out, int64_t* launches_out
   return CCE_OK;
 }
 
+struct NormArgs {
+  const void* gamma;
+  float eps;
+};
+
+static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t D, int64_t ldh, const void* W,
+                               int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
+                               int32_t* n_valid, void* workspace, size_t workspace_bytes, void* stream,
+                               const NormArgs* norm);
+
 cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64_t ldh, const void* W,
                        int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
                        int32_t* n_valid, void* workspace, size_t workspace_bytes, void* stream) {
+  return forward_impl(h, H, N, D, ldh, W, V_local, ldw, labels, loss, lse, n_valid, workspace, workspace_bytes, stream,
+                      nullptr);
+}
+
+cce_status cce_forward_rmsnorm(cce_handle* h, const void* X, int64_t N, int64_t D, int64_t ldx, const void* gamma,
+                               float eps, const void* W, int64_t V_local, int64_t ldw, const int32_t* labels,
+                               float* loss, float* lse, int32_t* n_valid, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (!h || !gamma || !(eps >= 0.f) || !std::isfinite(eps)) return CCE_ERR_INVALID_VALUE;
+  if (!aligned16(gamma) || D > 8192) return CCE_ERR_UNSUPPORTED;
+  NormArgs na{gamma, eps};
+  return forward_impl(h, X, N, D, ldx, W, V_local, ldw, labels, loss, lse, n_valid, workspace, workspace_bytes, stream,
+                      &na);
+}
+
+static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t D, int64_t ldh, const void* W,
+                               int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
+                               int32_t* n_valid, void* workspace, size_t workspace_bytes, void* stream,
+                               const NormArgs* norm) {
   if (!h || !loss) return CCE_ERR_INVALID_VALUE;
   if (N < 0 || D <= 0 || V_local < 0 || ldh < D || ldw < D) return CCE_ERR_INVALID_VALUE;
   if (N > 0 && (!H || !labels)) return CCE_ERR_INVALID_VALUE;
@@ -539,9 +579,15 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
     k_label_scan<<<1, 1024, 0, s>>>(labels, (int)N, h->cfg.ignore_index, (long long)h->cfg.vocab_total,
                                     at<int>(ws, L.pos), at<int>(ws, L.idx), at<int>(ws, L.labels_c), nvp, errp); }
     { ProfScope ps(h, s, 4);
-    k_gather_rows<<<grid_for((long long)L.Npad * D / 8, 256, 4 * h->num_sms), 256, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(H), ldh, (int)D, (int)L.Npad, at<int>(ws, L.idx), nvp,
-        at<__nv_bfloat16>(ws, L.Hc)); }
+    if (norm)  // RMSNorm prologue: normalise the valid rows on the way into Hc, cache rstd
+      k_gather_rmsnorm<<<grid_for(L.Npad, 8, 8 * h->num_sms), 256, 0, s>>>(
+          static_cast<const __nv_bfloat16*>(H), ldh, (int)D, (int)L.Npad, at<int>(ws, L.idx), nvp,
+          static_cast<const __nv_bfloat16*>(norm->gamma), norm->eps, at<__nv_bfloat16>(ws, L.Hc),
+          at<float>(ws, L.rstd_c));
+    else
+      k_gather_rows<<<grid_for((long long)L.Npad * D / 8, 256, 4 * h->num_sms), 256, 0, s>>>(
+          static_cast<const __nv_bfloat16*>(H), ldh, (int)D, (int)L.Npad, at<int>(ws, L.idx), nvp,
+          at<__nv_bfloat16>(ws, L.Hc)); }
   }
 
   // a1 + a2: tcgen05 logit tiles with the online-softmax epilogue
@@ -629,6 +675,10 @@ cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64
   if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
 
   h->have_fwd = true;
+  h->norm = norm != nullptr;
+  h->nX = H;
+  h->ldx = ldh;
+  h->gamma = norm ? norm->gamma : nullptr;
   h->W = W;
   h->N = N;
   h->D = D;
@@ -665,7 +715,15 @@ static bool adamw_aligned(const cce_adamw_params* o) {
 }
 
 static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, void* dW, const cce_adamw_params* opt,
-                                void* stream);
+                                void* stream, void* dgamma = nullptr, bool norm = false);
+
+cce_status cce_backward_rmsnorm(cce_handle* h, const float* dloss, void* dX, void* dgamma, void* dW, void* stream) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  if (!h->have_fwd || !h->norm) return CCE_ERR_NO_FORWARD;
+  if (!dgamma) return CCE_ERR_INVALID_VALUE;
+  if (!aligned16(dgamma)) return CCE_ERR_UNSUPPORTED;
+  return backward_impl(h, dloss, dX, dW, nullptr, stream, dgamma, true);
+}
 
 cce_status cce_backward(cce_handle* h, const float* dloss, void* dH, void* dW, void* stream) {
   return backward_impl(h, dloss, dH, dW, nullptr, stream);
@@ -691,7 +749,7 @@ cce_status cce_adamw_step(const cce_adamw_params* opt, const void* grad, int32_t
 }
 
 static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, void* dW, const cce_adamw_params* opt,
-                                void* stream) {
+                                void* stream, void* dgamma, bool norm) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   if (!h->have_fwd) return CCE_ERR_NO_FORWARD;
   if (!dloss || (h->N > 0 && !dH) || (h->V_local > 0 && !dW)) return CCE_ERR_INVALID_VALUE;
@@ -854,11 +912,37 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       if (n.allreduce(dH32, dH32, (size_t)L.Npad * D, kNcclFloat32, kNcclSum, h->cfg.nccl_comm, s) != 0)
         return CCE_ERR_NCCL;
     }
+    if (norm) {
+      // RMSNorm backward from the unrounded fp32 dH: dX (valid rows), dgamma, zeros for ignored rows
+      const int gf = (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0, ac = (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0;
+      const size_t sm = (size_t)RMS_BWD_WARPS * D * 4;
+      if (sm > 48 * 1024 &&
+          cudaFuncSetAttribute(k_rmsnorm_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+        return CCE_ERR_CUDA;
+      { ProfScope ps(h, s, 4);
+      k_rmsnorm_bwd<<<RMS_GP, 32 * RMS_BWD_WARPS, sm, s>>>(
+          dH32, static_cast<const __nv_bfloat16*>(h->nX), h->ldx, at<int>(ws, L.idx), nvp,
+          static_cast<const __nv_bfloat16*>(h->gamma), at<float>(ws, L.rstd_c), (int)D, dH, gf, ac,
+          at<float>(ws, L.gpart)); }
+      { ProfScope ps(h, s, 4);
+      k_dgamma_reduce<<<grid_for(D, 256, 64), 256, 0, s>>>(at<float>(ws, L.gpart), RMS_GP, (int)D, dgamma, gf, ac); }
+      if (!ac) {
+        ProfScope ps(h, s, 4);
+        k_zero_ignored<<<grid_for((long long)N * D / 8, 256, 4 * h->num_sms), 256, 0, s>>>(at<int>(ws, L.pos), (int)N,
+                                                                                         (int)D, dH, gf);
+      }
+      if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
+      return CCE_OK;
+    }
     ProfScope ps(h, s, 4);
     k_scatter_dH<<<grid_for((long long)N * D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(dH32, at<int>(ws, L.pos), (int)N,
                                                                                      (int)D, dH,
                                                                                      (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0,
                                                                                      (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0);
+  } else if (norm && !(h->cfg.flags & CCE_FLAG_ACCUMULATE)) {
+    // no rows: dgamma = 0
+    if (cudaMemsetAsync(dgamma, 0, (size_t)D * ((h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 4 : 2), s) != cudaSuccess)
+      return CCE_ERR_CUDA;
   }
   if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
   return CCE_OK;

@@ -383,3 +383,187 @@ __global__ void k_adamw(const AdamwArgs a) {
 }
 
 }  // namespace cce
+
+namespace cce {
+
+// ------------------------------------------------------------------ RMSNorm prologue
+// (Def. RMSNorm, Alg. Fused RMSNorm Forward P:712-731):
+// the gather of the valid rows normalises them on the way, Hc[r] = bf16((x rstd) gamma)
+// with rstd = 1 / sqrt(mean(x^2) + eps) in fp32, and caches rstd per compact row for the
+// backward (Alg. "Cache rstd for backward").  One warp per row; 16-byte vectors; the
+// warp's sum of squares is reduced in a fixed butterfly order (deterministic).  Rows
+// [n_valid, round_up(n_valid, 128)) are zeroed like k_gather_rows; ignored rows are never read.
+__global__ void k_gather_rmsnorm(const __nv_bfloat16* __restrict__ X, long long ldx, int D, int Npad,
+                                 const int* __restrict__ idx, const int* __restrict__ n_valid,
+                                 const __nv_bfloat16* __restrict__ gamma, float eps, __nv_bfloat16* __restrict__ Hc,
+                                 float* __restrict__ rstd_c) {
+  const int nv = *n_valid;
+  const int rows = min(Npad, ((nv + 127) / 128) * 128);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int nvec = D / 8;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
+    uint4* dst = reinterpret_cast<uint4*>(Hc + (long long)r * D);
+    if (r >= nv) {
+      for (int c = lane; c < nvec; c += 32) dst[c] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(X + (long long)idx[r] * ldx);
+    float ss = 0.f;
+    for (int c = lane; c < nvec; c += 32) {
+      const uint4 v = src[c];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float a = __uint_as_float(w[k] << 16), b = __uint_as_float(w[k] & 0xffff0000u);
+        ss = fmaf(a, a, ss);
+        ss = fmaf(b, b, ss);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float rstd = 1.f / sqrtf(ss / (float)D + eps);
+    const uint4* g4 = reinterpret_cast<const uint4*>(gamma);
+    for (int c = lane; c < nvec; c += 32) {
+      const uint4 v = src[c], gv = g4[c];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w}, gw[4] = {gv.x, gv.y, gv.z, gv.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float y0 = (__uint_as_float(w[k] << 16) * rstd) * __uint_as_float(gw[k] << 16);
+        const float y1 = (__uint_as_float(w[k] & 0xffff0000u) * rstd) * __uint_as_float(gw[k] & 0xffff0000u);
+        __nv_bfloat162 p = __floats2bfloat162_rn(y0, y1);
+        o[k] = *reinterpret_cast<uint32_t*>(&p);
+      }
+      dst[c] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    if (lane == 0) rstd_c[r] = rstd;
+  }
+}
+
+// RMSNorm backward (reading R18: the exact gradient of Def. RMSNorm), fed by the
+// UNROUNDED fp32 dH of the CE path (dH32, compact rows):
+//   xbar = x rstd,  c1 = (1/D) sum_i g_i gamma_i xbar_i,  dx = rstd (gamma g - xbar c1)
+//   dgamma = sum_rows g xbar
+// Block = 4 warps; warp w of block b takes compact rows b*4 + w, + 4*gridDim, ... in
+// order and accumulates its dgamma contribution in its own shared-memory row [D];
+// the block sums its 4 rows in fixed order into gpart[b][D] (k_dgamma_reduce then sums
+// the blocks in fixed order): deterministic, no atomics.  dX rows of valid tokens are
+// written here (scattered to the original positions); ignored rows by k_zero_ignored.
+constexpr int RMS_BWD_WARPS = 4;
+__global__ void __launch_bounds__(32 * RMS_BWD_WARPS)
+    k_rmsnorm_bwd(const float* __restrict__ dH32, const __nv_bfloat16* __restrict__ X, long long ldx,
+                  const int* __restrict__ idx, const int* __restrict__ n_valid,
+                  const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ rstd_c, int D, void* dX,
+                  int grad_fp32, int accumulate, float* __restrict__ gpart) {
+  extern __shared__ float sp[];  // [RMS_BWD_WARPS][D]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* part = sp + (size_t)w * D;
+  for (int j = lane; j < D; j += 32) part[j] = 0.f;
+  const int nv = *n_valid;
+  const int nvec = D / 8;
+  const uint4* g4 = reinterpret_cast<const uint4*>(gamma);
+  for (int r = blockIdx.x * RMS_BWD_WARPS + w; r < nv; r += gridDim.x * RMS_BWD_WARPS) {
+    const long long n = idx[r];
+    const float rs = rstd_c[r];
+    const uint4* xs = reinterpret_cast<const uint4*>(X + n * ldx);
+    const float4* gs = reinterpret_cast<const float4*>(dH32 + (long long)r * D);
+    float c1 = 0.f;
+    for (int c = lane; c < nvec; c += 32) {
+      const uint4 xv = xs[c], gv = g4[c];
+      const float4 a = gs[2 * c], b = gs[2 * c + 1];
+      const float gg[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, gw[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        c1 = fmaf(gg[2 * k] * __uint_as_float(gw[k] << 16), __uint_as_float(xw[k] << 16) * rs, c1);
+        c1 = fmaf(gg[2 * k + 1] * __uint_as_float(gw[k] & 0xffff0000u), __uint_as_float(xw[k] & 0xffff0000u) * rs, c1);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    c1 /= (float)D;
+    for (int c = lane; c < nvec; c += 32) {
+      const uint4 xv = xs[c], gv = g4[c];
+      const float4 a = gs[2 * c], b = gs[2 * c + 1];
+      const float gg[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, gw[4] = {gv.x, gv.y, gv.z, gv.w};
+      float dx[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float xb0 = __uint_as_float(xw[k] << 16) * rs, xb1 = __uint_as_float(xw[k] & 0xffff0000u) * rs;
+        dx[2 * k] = rs * (__uint_as_float(gw[k] << 16) * gg[2 * k] - xb0 * c1);
+        dx[2 * k + 1] = rs * (__uint_as_float(gw[k] & 0xffff0000u) * gg[2 * k + 1] - xb1 * c1);
+        part[c * 8 + 2 * k] = fmaf(gg[2 * k], xb0, part[c * 8 + 2 * k]);
+        part[c * 8 + 2 * k + 1] = fmaf(gg[2 * k + 1], xb1, part[c * 8 + 2 * k + 1]);
+      }
+      if (grad_fp32) {
+        float4* o = reinterpret_cast<float4*>(static_cast<float*>(dX) + n * D) + 2 * c;
+        if (accumulate) {
+          const float4 p0 = o[0], p1 = o[1];
+          dx[0] += p0.x; dx[1] += p0.y; dx[2] += p0.z; dx[3] += p0.w;
+          dx[4] += p1.x; dx[5] += p1.y; dx[6] += p1.z; dx[7] += p1.w;
+        }
+        o[0] = make_float4(dx[0], dx[1], dx[2], dx[3]);
+        o[1] = make_float4(dx[4], dx[5], dx[6], dx[7]);
+      } else {
+        uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(dX) + n * D) + c;
+        if (accumulate) {
+          const uint4 p = *o;
+          const uint32_t pw[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            dx[2 * k] += __uint_as_float(pw[k] << 16);
+            dx[2 * k + 1] += __uint_as_float(pw[k] & 0xffff0000u);
+          }
+        }
+        __nv_bfloat162 q0 = __floats2bfloat162_rn(dx[0], dx[1]), q1 = __floats2bfloat162_rn(dx[2], dx[3]);
+        __nv_bfloat162 q2 = __floats2bfloat162_rn(dx[4], dx[5]), q3 = __floats2bfloat162_rn(dx[6], dx[7]);
+        *o = make_uint4(*reinterpret_cast<uint32_t*>(&q0), *reinterpret_cast<uint32_t*>(&q1),
+                        *reinterpret_cast<uint32_t*>(&q2), *reinterpret_cast<uint32_t*>(&q3));
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < RMS_BWD_WARPS; ++k) s += sp[(size_t)k * D + j];
+    gpart[(size_t)blockIdx.x * D + j] = s;
+  }
+}
+
+// dgamma = sum of the per-block partials in block order (deterministic).
+__global__ void k_dgamma_reduce(const float* __restrict__ gpart, int nb, int D, void* dgamma, int grad_fp32,
+                                int accumulate) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < D; j += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < nb; ++b) s += gpart[(size_t)b * D + j];
+    if (grad_fp32) {
+      float* o = static_cast<float*>(dgamma) + j;
+      *o = accumulate ? *o + s : s;
+    } else {
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(dgamma) + j;
+      *o = __float2bfloat16_rn(accumulate ? __bfloat162float(*o) + s : s);
+    }
+  }
+}
+
+// dX rows of ignored tokens: 0 (overwrite mode only; they receive no gradient).
+__global__ void k_zero_ignored(const int* __restrict__ pos, int N, int D, void* dX, int grad_fp32) {
+  const int nvec = D / 8;
+  const long long total = (long long)N * nvec;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(i / nvec), c = (int)(i % nvec);
+    if (pos[n] >= 0) continue;
+    if (grad_fp32) {
+      float4* o = reinterpret_cast<float4*>(static_cast<float*>(dX) + (long long)n * D) + 2 * c;
+      o[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(dX) + (long long)n * D)[c] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+}  // namespace cce

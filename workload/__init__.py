@@ -264,3 +264,15 @@ def make_adamw_state(seed: int, shape, g_scale: float):
     m = (0.5 * g_scale * normal_f64(seed, S_ADAM_M, 0, n)).astype(np.float32).reshape(shape)
     v = ((g_scale * g_scale) * (0.5 + 1.5 * uniform01(seed, S_ADAM_V, 0, n))).astype(np.float32).reshape(shape)
     return m, v
+
+
+S_NORM_X, S_NORM_G = 103, 104
+
+
+def make_rmsnorm_inputs(seed: int, N: int, D: int, x_std: float = 2.0, g_std: float = 0.1):
+    """Inputs of the RMSNorm prologue: the un-normalised final hidden
+    states X ~ x_std N(0,1) and a learned-looking scale gamma ~ 1 + g_std N(0,1), both bf16
+    bit patterns (RNE)."""
+    X = normal_bf16(seed, S_NORM_X, N, D, x_std)
+    g = f32_to_bf16_bits((1.0 + g_std * normal_f64(seed, S_NORM_G, 0, D)).astype(np.float32))
+    return X, g
