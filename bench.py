@@ -104,9 +104,18 @@ class ClockSampler:
                 pw.append(float(r[3]))
             except (ValueError, IndexError):
                 pass
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows),
-                "power_w_max": max(pw) if pw else None}
+        # "under load": the samples drawing at least half the peak power seen (the sampler
+        # also covers the idle lead-in before the timed region)
+        load = []
+        for r in self.rows:
+            try:
+                if pw and float(r[3]) >= 0.5 * max(pw):
+                    load.append(float(r[1]))
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(load) if load else (statistics.median(sm) if sm else None),
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(self.rows),
+                "samples_under_load": len(load), "power_w_max": max(pw) if pw else None}
 
 
 def cpu_baseline(p, n_tokens_target_s=15.0):
@@ -255,7 +264,7 @@ def main():
     cce.cce_profile_read(h.h, reset=True)
     l0 = cce.cce_kernel_launches(h.h)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, period_ms=10)  # the timed region is ~0.1 s: sample every 10 ms
     sampler.start()
     time.sleep(0.3)
     if world > 1:
