@@ -260,6 +260,27 @@ def main():
     assert math.isfinite(loss.item()) and int(nvt.item()) == n_valid
     assert torch.isfinite(dW.float()).all() and dW.float().abs().sum().item() > 0
 
+    # memory report: one step between cudaMemGetInfo / torch peak readings.  The
+    # library never allocates (caller-owned workspace), so the device's free memory and the
+    # torch allocator peak must not move; the largest buffer is compared with one bf16 copy
+    # of the logits, N x V x 2 bytes (the paper's 4.97 GB fp32 figure).
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info(dev)[0]
+    torch.cuda.reset_peak_memory_stats(dev)
+    alloc0 = torch.cuda.memory_allocated(dev)
+    step()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info(dev)[0]
+    nv_bf16 = c.N * c.V * 2
+    buffers = {"workspace": ws.numel(), "W": W.numel() * 2, "dW": dW.numel() * 2, "H": H.numel() * 2,
+               "dH": dH.numel() * 2}
+    memory = {"workspace_bytes": int(ws.numel()), "largest_buffer": max(buffers, key=buffers.get),
+              "largest_buffer_bytes": int(max(buffers.values())), "logits_NxV_bf16_bytes": nv_bf16,
+              "logits_NxV_fp32_bytes": 2 * nv_bf16,
+              "torch_peak_delta_bytes_during_step": int(torch.cuda.max_memory_allocated(dev) - alloc0),
+              "device_free_delta_bytes_during_step": int(free0 - free1),
+              "no_NxV_buffer": bool(max(buffers.values()) < nv_bf16)}
+
     cce.cce_profile_enable(h.h, True)
     cce.cce_profile_read(h.h, reset=True)
     l0 = cce.cce_kernel_launches(h.h)
@@ -366,6 +387,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "memory": memory,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
             "wall_s_timed_region": wall,
             "clocks": clocks,

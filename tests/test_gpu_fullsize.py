@@ -105,3 +105,79 @@ def test_full_size_invariants(full):
     assert np.linalg.norm(dW.sum(0)) <= 1e-2 * np.linalg.norm(dW)
     dH = (outs[0]["dH"].astype(np.uint16).astype(np.uint32) << 16).view(np.float32)
     assert np.isfinite(dH).all()
+
+
+def test_memory_no_nxv_buffer():
+    """SURVEY 8(d) memory report at the bench configuration: the library allocates nothing
+    (caller-owned workspace: device free memory and the torch allocator peak do not move
+    during a forward + backward) and no buffer is N x V sized (the workspace, the largest
+    buffer, is compared with one bf16 copy of the logits, N V 2 bytes = 2.49 GB)."""
+    import torch
+    import __graft_entry__
+    import paper_2601_02609_b200 as cce
+    __graft_entry__.build()
+    dev = torch.device("cuda:0")
+    c = workload.CONFIGS["qwen05b"]
+    p = workload.make_config("qwen05b", seed=42)
+    H, W, y = to_dev(p, dev)
+    h = cce.CCEHandle(vocab_total=c.V)
+    ws = h.workspace(c.N, c.D, c.V, dev)
+    assert ws.numel() < c.N * c.V * 2 // 4
+    dH = torch.empty_like(H)
+    dW = torch.empty_like(W)
+    one = torch.ones((), dtype=torch.float32, device=dev)
+    h.forward(H, W, y)          # warm: the handle's small outputs are allocated here
+    h.backward(one, dH, dW)
+    loss = torch.empty((), dtype=torch.float32, device=dev)
+    lse = torch.empty(c.N, dtype=torch.float32, device=dev)
+    nvt = torch.empty((), dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info(dev)[0]
+    torch.cuda.reset_peak_memory_stats(dev)
+    a0 = torch.cuda.memory_allocated(dev)
+    cce.cce_forward(h.h, H, W, y, loss, lse, nvt, ws)
+    cce.cce_backward(h.h, one, dH, dW)
+    torch.cuda.synchronize()
+    assert torch.cuda.max_memory_allocated(dev) == a0
+    assert torch.cuda.mem_get_info(dev)[0] == free0
+    assert np.isfinite(loss.item())
+    h.close()
+
+
+def test_rmsnorm_prologue_full_size_sampled_rows():
+    """The RMSNorm prologue at the bench configuration: per-row LSE
+    and dX of sampled valid rows against the oracle (H = bf16(RMSNorm(X)) for all rows,
+    then the row-local CE and RMSNorm backward of the picked rows), plus the whole-output
+    properties (ignored rows of dX bit-zero, finite gradients)."""
+    import torch
+    import __graft_entry__
+    import paper_2601_02609_b200 as cce
+    __graft_entry__.build()
+    dev = torch.device("cuda:0")
+    c = workload.CONFIGS["qwen05b"]
+    p = workload.make_config("qwen05b", seed=42)
+    X, g = workload.make_rmsnorm_inputs(42, c.N, c.D)
+    t = lambda b: torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).view(torch.bfloat16).to(dev)  # noqa: E731
+    Xt, gt, Wt = t(X), t(g), t(p["W"])
+    y = torch.from_numpy(p["labels"]).to(dev)
+    h = cce.CCEHandle(vocab_total=c.V)
+    loss, lse, nv = h.forward_rmsnorm(Xt, gt, 1e-6, Wt, y)
+    dX = torch.empty_like(Xt)
+    dg = torch.empty_like(gt)
+    dW = torch.empty_like(Wt)
+    h.backward_rmsnorm(torch.ones((), dtype=torch.float32, device=dev), dX, dg, dW)
+    torch.cuda.synchronize()
+    h.close()
+    valid = p["labels"] != -100
+    rows = np.nonzero(valid)[0]
+    pick = np.unique(np.concatenate([rows[:3], rows[-3:], rows[np.linspace(0, len(rows) - 1, 10).astype(int)]]))
+    y_ref, rstd = oracle.rmsnorm_fwd(X, g, 1e-6)
+    H_bits = oracle.to_bf16(y_ref)
+    lse_ref, _, dH_ref = oracle.rows(H_bits, p["W"], p["labels"], pick, scale=1.0 / len(rows))
+    got_lse = lse.cpu().numpy().astype(np.float64)[pick]
+    assert np.max(np.abs(got_lse - lse_ref) / np.maximum(np.abs(lse_ref), 1.0)) <= TOL_LSE
+    dX_ref, _ = oracle.rmsnorm_bwd(dH_ref, X[pick], g, rstd[pick])
+    got = bf16_to_f64(dX)
+    assert rel_fro(got[pick], dX_ref) <= TOL_GRAD
+    assert np.all(dX.view(torch.int16).cpu().numpy()[~valid] == 0)
+    assert np.isfinite(got).all() and np.isfinite(bf16_to_f64(dg)).all() and np.isfinite(loss.item())
