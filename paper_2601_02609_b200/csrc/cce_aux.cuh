@@ -105,14 +105,28 @@ __global__ void __launch_bounds__(1024) k_merge_tiles(const float2* __restrict__
   const int i = blockIdx.x * 32 + lane;
   float m = -INFINITY, d = 0.f, zs = 0.f;
   if (i < nv) {
-    for (int t = w; t < Tv; t += 32) {
-      const float2 pd = part[(size_t)t * Npad + i];
-      if (pd.y > 0.f) {
-        const float mn = fmaxf(m, pd.x);
-        d = d * expf(m - mn) + pd.y * expf(pd.x - mn);
-        m = mn;
+    // four tiles' partials in flight per thread (the loop is latency-bound otherwise);
+    // merged in the same tile order as one at a time
+    for (int t0 = w; t0 < Tv; t0 += 4 * 32) {
+      float2 pd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + 32 * u;
+        pd[u] = t < Tv ? part[(size_t)t * Npad + i] : make_float2(-INFINITY, 0.f);
       }
-      if (zs_part) zs += zs_part[(size_t)t * Npad + i];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (pd[u].y > 0.f) {
+          const float mn = fmaxf(m, pd[u].x);
+          d = d * expf(m - mn) + pd[u].y * expf(pd[u].x - mn);
+          m = mn;
+        }
+      }
+      if (zs_part) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (t0 + 32 * u < Tv) zs += zs_part[(size_t)(t0 + 32 * u) * Npad + i];
+      }
     }
   }
   red[w][lane] = make_float2(m, d);
