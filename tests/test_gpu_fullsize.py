@@ -181,3 +181,52 @@ def test_rmsnorm_prologue_full_size_sampled_rows():
     assert rel_fro(got[pick], dX_ref) <= TOL_GRAD
     assert np.all(dX.view(torch.int16).cpu().numpy()[~valid] == 0)
     assert np.isfinite(got).all() and np.isfinite(bf16_to_f64(dg)).all() and np.isfinite(loss.item())
+
+
+def test_fused_adamw_full_size_sampled_rows():
+    """The fused optimizer step at the bench configuration, in the
+    default launch (pair kernel, W_out double buffer): sampled vocabulary rows of the new
+    master weights / moments against oracle.dW_rows (golden LSE) fed to oracle.adamw_step,
+    with warm moments (step 10)."""
+    import torch
+    import __graft_entry__
+    import paper_2601_02609_b200 as cce
+    __graft_entry__.build()
+    if not os.path.exists(GOLD):
+        pytest.skip("golden file missing (scripts/make_golden.py)")
+    g = np.load(GOLD)
+    dev = torch.device("cuda:0")
+    p = workload.make_config("qwen05b", seed=42)
+    H, W, y = to_dev(p, dev)
+    V, D = W.shape
+    lab = p["labels"][p["labels"] != -100]
+    common = np.bincount(lab, minlength=V).argsort()[-4:]
+    pick = np.unique(np.concatenate([[0, 8191, 8192, V - 1], common,
+                                     np.random.default_rng(1).choice(V, 8, replace=False)]))
+    lse_all = np.zeros(len(p["labels"]))
+    lse_all[g["valid_rows"]] = g["lse"]
+    dW_ref = oracle.dW_rows(p["H"], p["W"], p["labels"], lse_all, 1.0 / len(g["valid_rows"]), pick)
+    gs = float(np.sqrt(np.mean(dW_ref * dW_ref)))
+    m0, v0 = workload.make_adamw_state(5, (V, D), gs)
+    master = W.float()
+    m, v = torch.from_numpy(m0).to(dev), torch.from_numpy(v0).to(dev)
+    Wo = torch.empty_like(W)
+    h = cce.CCEHandle(vocab_total=V)
+    h.forward(H, W, y)
+    opt = cce.adamw_params(m, v, lr=1e-3, step=10, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1,
+                           master=master, W_out=Wo)
+    h.backward_adamw(torch.ones((), dtype=torch.float32, device=dev), torch.empty_like(H), opt)
+    torch.cuda.synchronize()
+    h.close()
+    th0 = workload.bf16_bits_to_f32(p["W"][pick]).astype(np.float64)
+    rth, rm, rv = oracle.adamw_step(th0, dW_ref, m0[pick], v0[pick], lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8,
+                                    weight_decay=0.1, step=10)
+    got_m = m.cpu().numpy()[pick].astype(np.float64)
+    got_v = v.cpu().numpy()[pick].astype(np.float64)
+    got_t = master.cpu().numpy()[pick].astype(np.float64)
+    assert rel_fro(got_m, rm) <= TOL_GRAD
+    assert rel_fro(got_v, rv) <= TOL_GRAD
+    dec = th0 * (1 - 1e-3 * 0.1)
+    assert rel_fro(got_t - dec, rth - dec) <= TOL_GRAD
+    assert np.array_equal(Wo.view(torch.int16).cpu().numpy()[pick].view(np.uint16),
+                          workload.f32_to_bf16_bits(master.cpu().numpy()[pick]))
