@@ -95,6 +95,11 @@ typedef enum {
  * left untouched. */
 #define CCE_FLAG_GRAD_FP32 64u
 #define CCE_FLAG_ACCUMULATE 128u
+/* Split-phase combine for vocabulary sharding with the caller's own collectives (world > 1
+ * without an NCCL communicator, e.g. torch.distributed or a single process driving several
+ * shards): see cce_combine_offsets / cce_forward_finish / cce_backward_finish.  Not with
+ * cce_backward_rmsnorm, cce_backward_adamw or cce_step_host (CCE_ERR_UNSUPPORTED). */
+#define CCE_FLAG_EXTERNAL_COMBINE 256u
 
 /* Reduction of the per-token losses (cce_config.reduction). */
 #define CCE_REDUCTION_MEAN 0  /* loss = sum_valid l_n / n_valid (default) */
@@ -269,6 +274,25 @@ cce_status cce_backward_adamw(cce_handle *h, const float *dloss, void *dH, const
  */
 cce_status cce_adamw_step(const cce_adamw_params *opt, const void *grad, int32_t grad_fp32, int64_t n,
                           void *W_bf16, void *stream);
+
+/*
+ * Split-phase combine (CCE_FLAG_EXTERNAL_COMBINE; SURVEY 8(e) rows a9 / a10 done by the
+ * caller).  cce_forward then stops after this rank's per-row partial statistics; the
+ * caller gathers them from every rank into the all-ranks array (rank-major) and calls
+ * cce_forward_finish, which merges them in rank order into the global LSE / loss exactly
+ * like the NCCL path.  cce_backward stops with this rank's partial dH (fp32, compact valid
+ * rows); the caller replaces it with the sum over ranks and calls cce_backward_finish,
+ * which writes dH.  dW is complete after cce_backward.
+ * cce_combine_offsets: byte offsets inside the workspace for a problem (N, D, V_local):
+ *   out4[0] this rank's stats   float [Npad][4]          (m, d, z_y, sum of logits)
+ *   out4[1] all ranks' stats    float [world][Npad][4]
+ *   out4[2] partial dH          float [Npad][D]
+ *   out4[3] Npad (rows of those arrays; rows >= n_valid are ignored)
+ * The finish calls return CCE_ERR_NO_FORWARD without a pending phase.
+ */
+cce_status cce_combine_offsets(const cce_handle *h, int64_t N, int64_t D, int64_t V_local, int64_t *out4);
+cce_status cce_forward_finish(cce_handle *h, void *stream);
+cce_status cce_backward_finish(cce_handle *h, void *stream);
 
 /* Synchronises `stream` and returns CCE_ERR_LABEL_RANGE if the most recent
  * cce_forward on this handle saw an out-of-range label (the offending rows are

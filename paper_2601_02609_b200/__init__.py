@@ -29,7 +29,8 @@ EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_byt
            "cce_get_error", "cce_host_staging_bytes", "cce_step_host", "cce_nccl_unique_id", "cce_nccl_comm_init",
            "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info",
            "cce_profile_enable", "cce_profile_read", "cce_debug_trace", "cce_backward_adamw", "cce_adamw_step",
-           "cce_forward_rmsnorm", "cce_backward_rmsnorm"]
+           "cce_forward_rmsnorm", "cce_backward_rmsnorm", "cce_combine_offsets", "cce_forward_finish",
+           "cce_backward_finish"]
 PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 # "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
 # FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
@@ -40,6 +41,7 @@ FLAG_QUAD_ONLY = 16
 FLAG_QUAD = 32
 FLAG_GRAD_FP32 = 64
 FLAG_ACCUMULATE = 128
+FLAG_EXTERNAL_COMBINE = 256
 REDUCTION_MEAN, REDUCTION_SUM, REDUCTION_NONE = 0, 1, 2
 _REDUCTIONS = {"mean": REDUCTION_MEAN, "sum": REDUCTION_SUM, "none": REDUCTION_NONE}
 
@@ -90,6 +92,12 @@ def lib():
         L.cce_forward.restype = st
         L.cce_backward.argtypes = [p, p, p, p, p]
         L.cce_backward.restype = st
+        L.cce_combine_offsets.argtypes = [p, i64, i64, i64, p]
+        L.cce_combine_offsets.restype = st
+        L.cce_forward_finish.argtypes = [p, p]
+        L.cce_forward_finish.restype = st
+        L.cce_backward_finish.argtypes = [p, p]
+        L.cce_backward_finish.restype = st
         L.cce_forward_rmsnorm.argtypes = [p, p, i64, i64, i64, p, ctypes.c_float, p, i64, i64, p, p, p, p, p, sz, p]
         L.cce_forward_rmsnorm.restype = st
         L.cce_backward_rmsnorm.argtypes = [p, p, p, p, p, p]
@@ -223,6 +231,22 @@ def cce_adamw_step(opt: cce_adamw_params, grad, n: int, W_bf16=None, stream=None
     g32 = 1 if (grad is not None and grad.dtype == torch.float32) else 0
     _check(lib().cce_adamw_step(ctypes.byref(opt), _ptr(grad), g32, n, _ptr(W_bf16), _stream(stream)),
            "cce_adamw_step")
+
+
+def cce_combine_offsets(h, N: int, D: int, V_local: int):
+    """(stats_off, stats_all_off, dH32_off, Npad): byte offsets into the workspace for the
+    split-phase combine (FLAG_EXTERNAL_COMBINE)."""
+    out = (ctypes.c_int64 * 4)()
+    _check(lib().cce_combine_offsets(h, N, D, V_local, out), "cce_combine_offsets")
+    return tuple(int(x) for x in out)
+
+
+def cce_forward_finish(h, stream=None):
+    _check(lib().cce_forward_finish(h, _stream(stream)), "cce_forward_finish")
+
+
+def cce_backward_finish(h, stream=None):
+    _check(lib().cce_backward_finish(h, _stream(stream)), "cce_backward_finish")
 
 
 def cce_get_error(h, stream=None) -> int:

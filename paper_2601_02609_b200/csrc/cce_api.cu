@@ -41,6 +41,12 @@ struct cce_handle {
   // RMSNorm prologue (cce_forward_rmsnorm): the un-normalised rows and the scale, saved
   // for cce_backward_rmsnorm
   bool norm = false;
+  // split-phase combine (CCE_FLAG_EXTERNAL_COMBINE): outputs of the pending finish calls
+  bool fwd_pending = false, bwd_pending = false;
+  float* p_loss = nullptr;
+  float* p_lse = nullptr;
+  int32_t* p_nv = nullptr;
+  void* p_dH = nullptr;
   const void* nX = nullptr;
   int64_t ldx = 0;
   const void* gamma = nullptr;
@@ -432,7 +438,8 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
     return CCE_ERR_INVALID_VALUE;
   // world > 1 needs a communicator; world == 1 may carry one (a 1-rank comm runs the
   // same NCCL collectives -- identities -- which lets one GPU exercise that path)
-  if (cfg->world > 1 && cfg->nccl_comm == nullptr) return CCE_ERR_INVALID_VALUE;
+  if (cfg->world > 1 && cfg->nccl_comm == nullptr && !(cfg->flags & CCE_FLAG_EXTERNAL_COMBINE))
+    return CCE_ERR_INVALID_VALUE;
   if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
   if (!(cfg->label_smoothing >= 0.f && cfg->label_smoothing < 1.f) || !(cfg->z_loss >= 0.f && cfg->z_loss < 1e30f))
     return CCE_ERR_INVALID_VALUE;
@@ -531,6 +538,8 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
                                int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
                                int32_t* n_valid, void* workspace, size_t workspace_bytes, void* stream,
                                const NormArgs* norm);
+static cce_status forward_tail(cce_handle* h, const float4* stats_all, float* loss, float* lse, int32_t* n_valid,
+                               cudaStream_t s);
 
 cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64_t ldh, const void* W,
                        int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
@@ -649,6 +658,28 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
         at<float2>(ws, L.part), V_local > 0 ? (int)L.Tv : 0, (int)L.Npad, at<float>(ws, L.zy_c), nvp,
         (h->cfg.label_smoothing > 0.f && V_local > 0) ? at<float>(ws, L.zs_part) : nullptr, stats);
   }
+  h->have_fwd = false;
+  h->norm = norm != nullptr;
+  h->nX = H;
+  h->ldx = ldh;
+  h->gamma = norm ? norm->gamma : nullptr;
+  h->W = W;
+  h->N = N;
+  h->D = D;
+  h->V_local = V_local;
+  h->ldw = ldw;
+  h->ws = workspace;
+  h->ws_bytes = workspace_bytes;
+  if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) {
+    // a9 done by the caller: it gathers every rank's `stats` into `stats_all`, then calls
+    // cce_forward_finish (cce_combine_offsets locates both in the workspace)
+    if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
+    h->fwd_pending = true;
+    h->p_loss = loss;
+    h->p_lse = lse;
+    h->p_nv = n_valid;
+    return CCE_OK;
+  }
   const float4* stats_all = stats;
   if (h->cfg.nccl_comm) {
     Nccl& n = nccl();
@@ -657,6 +688,17 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
       return CCE_ERR_NCCL;
     stats_all = at<float4>(ws, L.stats_all);
   }
+  return forward_tail(h, stats_all, loss, lse, n_valid, s);
+}
+
+// a4 (global) + loss: per-row LSE / loss from the (gathered) per-rank stats.
+static cce_status forward_tail(cce_handle* h, const float4* stats_all, float* loss, float* lse, int32_t* n_valid,
+                               cudaStream_t s) {
+  const int64_t N = h->N;
+  const Layout L = layout(N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots);
+  void* ws = h->ws;
+  int* nvp = at<int>(ws, L.scal);
+  int* errp = nvp + 1;
   if (N > 0) {
     ProfScope ps(h, s, 4);
     k_finalize<<<grid_for(N, 256, 8 * h->num_sms), 256, 0, s>>>(stats_all, h->cfg.world, (int)L.Npad,
@@ -673,19 +715,26 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
                               h->cfg.reduction == CCE_REDUCTION_SUM ? 1 : 0);
   }
   if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
-
   h->have_fwd = true;
-  h->norm = norm != nullptr;
-  h->nX = H;
-  h->ldx = ldh;
-  h->gamma = norm ? norm->gamma : nullptr;
-  h->W = W;
-  h->N = N;
-  h->D = D;
-  h->V_local = V_local;
-  h->ldw = ldw;
-  h->ws = workspace;
-  h->ws_bytes = workspace_bytes;
+  return CCE_OK;
+}
+
+cce_status cce_forward_finish(cce_handle* h, void* stream) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  if (!h->fwd_pending) return CCE_ERR_NO_FORWARD;
+  h->fwd_pending = false;
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots);
+  return forward_tail(h, at<float4>(h->ws, L.stats_all), h->p_loss, h->p_lse, h->p_nv,
+                      static_cast<cudaStream_t>(stream));
+}
+
+cce_status cce_combine_offsets(const cce_handle* h, int64_t N, int64_t D, int64_t V_local, int64_t* out4) {
+  if (!h || !out4 || N < 0 || D <= 0 || V_local < 0) return CCE_ERR_INVALID_VALUE;
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots);
+  out4[0] = (int64_t)L.stats;      // this rank's stats: float [Npad][4] (m, d, z_y, sum z)
+  out4[1] = (int64_t)L.stats_all;  // all ranks' stats: float [world][Npad][4], rank-major
+  out4[2] = (int64_t)L.dH32;       // this rank's partial dH: float [Npad][D], compact valid rows
+  out4[3] = L.Npad;
   return CCE_OK;
 }
 
@@ -719,6 +768,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
 
 cce_status cce_backward_rmsnorm(cce_handle* h, const float* dloss, void* dX, void* dgamma, void* dW, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
+  if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) return CCE_ERR_UNSUPPORTED;
   if (!h->have_fwd || !h->norm) return CCE_ERR_NO_FORWARD;
   if (!dgamma) return CCE_ERR_INVALID_VALUE;
   if (!aligned16(dgamma)) return CCE_ERR_UNSUPPORTED;
@@ -734,6 +784,7 @@ cce_status cce_backward_adamw(cce_handle* h, const float* dloss, void* dH, const
   if (!h) return CCE_ERR_INVALID_VALUE;
   if (!h->have_fwd) return CCE_ERR_NO_FORWARD;
   if (!adamw_params_ok(opt)) return CCE_ERR_INVALID_VALUE;
+  if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) return CCE_ERR_UNSUPPORTED;
   if (h->cfg.flags & (CCE_FLAG_ONE_CTA | CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY | CCE_FLAG_ACCUMULATE))
     return CCE_ERR_UNSUPPORTED;
   if (!adamw_aligned(opt) || (h->D % 8) != 0 || (opt->W_out && !aligned16(opt->W_out))) return CCE_ERR_UNSUPPORTED;
@@ -905,6 +956,14 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
   }
   if (N > 0) {
     if (V_local == 0 && cudaMemsetAsync(dH32, 0, (size_t)L.Npad * D * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+    if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) {
+      // a10 done by the caller: it sums every rank's partial dH32 in place, then calls
+      // cce_backward_finish (the scatter to dH)
+      if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
+      h->bwd_pending = true;
+      h->p_dH = dH;
+      return CCE_OK;
+    }
     if (h->cfg.nccl_comm) {
       // a10: dH partials summed over the vocabulary shards
       Nccl& n = nccl();
@@ -948,6 +1007,19 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
   return CCE_OK;
 }
 
+cce_status cce_backward_finish(cce_handle* h, void* stream) {
+  if (!h) return CCE_ERR_INVALID_VALUE;
+  if (!h->bwd_pending) return CCE_ERR_NO_FORWARD;
+  h->bwd_pending = false;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots);
+  ProfScope ps(h, s, 4);
+  k_scatter_dH<<<grid_for((long long)h->N * h->D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(
+      at<float>(h->ws, L.dH32), at<int>(h->ws, L.pos), (int)h->N, (int)h->D, h->p_dH,
+      (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0, (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0);
+  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+}
+
 cce_status cce_get_error(cce_handle* h, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -975,6 +1047,7 @@ cce_status cce_step_host(cce_handle* h, const void* H_host, int64_t N, int64_t D
                          void* stream) {
   if (!h || !loss_host || (N > 0 && (!H_host || !labels_host))) return CCE_ERR_INVALID_VALUE;
   if (N < 0 || D <= 0) return CCE_ERR_INVALID_VALUE;
+  if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) return CCE_ERR_UNSUPPORTED;
   if (!dev_inputs || dev_inputs_bytes < cce_host_staging_bytes(N, D) || !aligned16(dev_inputs))
     return CCE_ERR_WORKSPACE;
   if (h->cfg.reduction == CCE_REDUCTION_NONE) return CCE_ERR_UNSUPPORTED;

@@ -137,7 +137,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
     // (Def. "Online Softmax"), target logit captured when y falls here.
     const int row = mt * BM + e.row_in_tile;
     const bool rv = row < nv;
-    const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+    // the target only counts on the rank that owns it: a label of the NEXT shard can fall in
+    // this shard's padded tail tile (local id in [V_local, 256-aligned)), where the logits are masked
+    const int yl = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+    const int y = ((unsigned)yl < (unsigned)p.V_local) ? yl : -1;
     float m = -INFINITY, d = 0.f;
 #pragma unroll 1
     for (int j = 0; j < JCH; ++j) {
@@ -189,7 +192,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
     // n_valid use an exponent offset of +inf (-> 0); the vocab tail is masked per chunk.
     const int row = mt * BM + e.row_in_tile;
     const bool rv = row < nv;
-    const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+    // the target only counts on the rank that owns it: a label of the NEXT shard can fall in
+    // this shard's padded tail tile (local id in [V_local, 256-aligned)), where the logits are masked
+    const int yl = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+    const int y = ((unsigned)yl < (unsigned)p.V_local) ? yl : -1;
     const float off2 = rv ? (p.lse_c[row] * LOG2E - __log2f(fabsf(scale))) : INFINITY;
     __nv_bfloat16* out = p.gbuf + (size_t)row * p.C + nt * BN + cbase;
 #pragma unroll 1

@@ -161,7 +161,10 @@ struct PEpi {
 __device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv) {
   const int row = it.m0 + e.rank * HM + e.rit;
   const bool rv = row < nv;
-  const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+  // the target only counts on the rank that owns it: a label of the NEXT shard can fall in
+  // this shard's padded tail tile (local id in [V_local, 256-aligned)), where the logits are masked
+  const int yl = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+  const int y = ((unsigned)yl < (unsigned)p.V_local) ? yl : -1;
   const int cb = e.half * (PN / 2);
   float m = -INFINITY, d = 0.f;
   float zs = 0.f;  // sum of the logits (label smoothing's mean z)
@@ -233,7 +236,10 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
   // fully coalesced 512-byte runs of the column-blocked G ring.
   const int row = it.m0 + e.rank * HM + e.rit;
   const bool rv = row < nv;
-  const int y = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+  // the target only counts on the rank that owns it: a label of the NEXT shard can fall in
+  // this shard's padded tail tile (local id in [V_local, 256-aligned)), where the logits are masked
+  const int yl = rv ? (p.labels_c[row] - p.vocab_offset) : -1;
+  const int y = ((unsigned)yl < (unsigned)p.V_local) ? yl : -1;
   const float lse = rv ? p.lse_c[row] : 0.f;
   if (p.dloss_c) scale = rv ? p.dloss_c[row] : 0.f;       // reduction "none": per-row upstream gradient
   const float sa = scale * (1.f + 2.f * p.z_loss * lse);  // scale of the softmax term
