@@ -654,7 +654,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   if (N > 0) {
     // an empty shard (V_local == 0) merges zero tiles: (m=-inf, d=0, z_y=0) for every row
     ProfScope ps(h, s, 4);
-    k_merge_tiles<<<(unsigned)((L.Npad + 31) / 32), 1024, 0, s>>>(
+    k_merge_tiles<<<(unsigned)((L.Npad + 31) / 32), 32 * MERGE_SL, 0, s>>>(
         at<float2>(ws, L.part), V_local > 0 ? (int)L.Tv : 0, (int)L.Npad, at<float>(ws, L.zy_c), nvp,
         (h->cfg.label_smoothing > 0.f && V_local > 0) ? at<float>(ws, L.zs_part) : nullptr, stats);
   }

@@ -11,60 +11,65 @@ namespace cce {
 
 // a0: range check + stable compaction of the non-ignored rows (P:2076-2079:
 // rows with y == ignore_index are skipped; the mean divides by their count,
-// P:899).  One block of 1024 threads, each owning a contiguous segment of the
-// labels, so the compact order equals the original row order.
+// P:899).  One block of 1024 threads walks the labels in tiles of 1024 (thread t owns
+// label n0 + t: coalesced), ranks the valid ones with a warp ballot + block scan and
+// carries the running count, so the compact order equals the original row order.
 // Out-of-range labels set err and are treated as ignored.
 __global__ void __launch_bounds__(1024) k_label_scan(const int32_t* __restrict__ labels, int N, int ignore_index,
                                                      long long vocab_total, int* __restrict__ pos,
                                                      int* __restrict__ idx, int* __restrict__ labels_c,
                                                      int* __restrict__ n_valid_out, int* __restrict__ err_out) {
   __shared__ int warp_tot[32];
-  const int t = threadIdx.x;
-  const int per = (N + 1023) / 1024;
-  const int b = min(N, t * per), e = min(N, b + per);
-  int cnt = 0, bad = 0;
-  for (int n = b; n < e; ++n) {
-    const int y = labels[n];
-    if (y == ignore_index) continue;
-    if (y < 0 || (long long)y >= vocab_total) { bad = 1; continue; }
-    ++cnt;
-  }
-  // block exclusive scan of cnt
-  const int lane = t & 31, w = t >> 5;
-  int incl = cnt;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  int base = 0, bad = 0;
+  constexpr int ST = 8;  // tiles per super-tile: all its labels are loaded before the scans
+  for (int s0 = 0; s0 < N; s0 += ST * 1024) {
+    int ys[ST];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) warp_tot[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    int s = warp_tot[lane];
+    for (int k = 0; k < ST; ++k) {
+      const int n = s0 + k * 1024 + t;
+      ys[k] = n < N ? labels[n] : ignore_index;
+    }
+#pragma unroll 1
+  for (int k = 0; k < ST; ++k) {
+    const int n = s0 + k * 1024 + t;
+    const int y = ys[k];
+    bool v = false;
+    if (n < N && y != ignore_index) {
+      if (y < 0 || (long long)y >= vocab_total) bad = 1;
+      else v = true;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, v);
+    const int wpre = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) warp_tot[w] = __popc(m);
+    __syncthreads();
+    if (w == 0) {
+      int s = warp_tot[lane];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += u;
+      }
+      warp_tot[lane] = s;  // inclusive over warps
     }
-    warp_tot[lane] = s;  // inclusive over warps
+    __syncthreads();
+    if (n < N) {
+      if (v) {
+        const int off = base + (w > 0 ? warp_tot[w - 1] : 0) + wpre;
+        pos[n] = off;
+        idx[off] = n;
+        labels_c[off] = y;
+      } else {
+        pos[n] = -1;
+      }
+    }
+    base += warp_tot[31];
+    __syncthreads();  // warp_tot is rewritten by the next tile
   }
-  __syncthreads();
-  int off = incl - cnt + (w > 0 ? warp_tot[w - 1] : 0);
-  for (int n = b; n < e; ++n) {
-    const int y = labels[n];
-    const bool v = (y != ignore_index) && y >= 0 && (long long)y < vocab_total;
-    if (v) {
-      pos[n] = off;
-      idx[off] = n;
-      labels_c[off] = y;
-      ++off;
-    } else {
-      pos[n] = -1;
-    }
   }
   const int any_bad = __syncthreads_or(bad);
   if (t == 0) {
-    *n_valid_out = warp_tot[31];
+    *n_valid_out = base;
     if (any_bad) atomicOr(err_out, 1);
   }
 }
@@ -87,46 +92,55 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ H, long long ldh
   }
 }
 
+constexpr int MERGE_SL = 16;  // tile slices per merge block (512 threads: two blocks per SM, one wave)
 // a4 (local part): merge the per-vocabulary-tile (m, d) partials of each valid
 // row with the online-softmax merge:
-// m = max_t m_t, d = sum_t d_t exp(m_t - m).  Block = 32 rows x 32 tile-slices:
-// thread (lane, w) folds tiles t = w, w+32, ... of row i0+lane in a single pass
-// (coalesced: part is [tile][row]), then warp 0 folds the 32 slices in order.
+// m = max_t m_t, d = sum_t d_t exp(m_t - m).  Block = 32 rows x MERGE_SL tile-slices
+// (512 threads): thread (lane, w) folds tiles t = w, w+16,
+// ... of row i0+lane (coalesced: part is [tile][row]), then warp 0 folds the slices in order.
 // Fixed order -> deterministic.  Out: (m, d, z_y) per compact row.
 // With label smoothing the per-tile logit sums (zs_part, may be nullptr) are summed in
 // the same fixed order into the 4th stat (sum_v z_v of the row over this shard).
-__global__ void __launch_bounds__(1024) k_merge_tiles(const float2* __restrict__ part, int Tv, int Npad,
+__global__ void __launch_bounds__(32 * MERGE_SL) k_merge_tiles(const float2* __restrict__ part, int Tv, int Npad,
                                                       const float* __restrict__ zy_c, const int* __restrict__ n_valid,
                                                       const float* __restrict__ zs_part, float4* __restrict__ stats) {
-  __shared__ float2 red[32][33];
-  __shared__ float redz[32][33];
+  __shared__ float2 red[MERGE_SL][33];
+  __shared__ float redz[MERGE_SL][33];
   const int nv = *n_valid;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
   float m = -INFINITY, d = 0.f, zs = 0.f;
   if (i < nv) {
-    // four tiles' partials in flight per thread (the loop is latency-bound otherwise);
-    // merged in the same tile order as one at a time
-    for (int t0 = w; t0 < Tv; t0 += 4 * 32) {
-      float2 pd[4];
+    // batches of eight tiles' partials per thread, the next batch loaded before the current
+    // one is merged (the loop is load-latency-bound otherwise); merged in tile order
+    constexpr int NB = 8;
+    float2 cur[NB], nxt[NB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int t = t0 + 32 * u;
-        pd[u] = t < Tv ? part[(size_t)t * Npad + i] : make_float2(-INFINITY, 0.f);
+    for (int u = 0; u < NB; ++u) {
+      const int t = w + MERGE_SL * u;
+      cur[u] = t < Tv ? part[(size_t)t * Npad + i] : make_float2(-INFINITY, 0.f);
+    }
+    for (int t0 = w; t0 < Tv; t0 += NB * MERGE_SL) {
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const int t = t0 + NB * MERGE_SL + MERGE_SL * u;
+        nxt[u] = t < Tv ? part[(size_t)t * Npad + i] : make_float2(-INFINITY, 0.f);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (pd[u].y > 0.f) {
-          const float mn = fmaxf(m, pd[u].x);
-          d = d * expf(m - mn) + pd[u].y * expf(pd[u].x - mn);
+      for (int u = 0; u < NB; ++u) {
+        if (cur[u].y > 0.f) {
+          const float mn = fmaxf(m, cur[u].x);
+          d = d * expf(m - mn) + cur[u].y * expf(cur[u].x - mn);
           m = mn;
         }
       }
       if (zs_part) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (t0 + 32 * u < Tv) zs += zs_part[(size_t)(t0 + 32 * u) * Npad + i];
+        for (int u = 0; u < NB; ++u)
+          if (t0 + MERGE_SL * u < Tv) zs += zs_part[(size_t)(t0 + MERGE_SL * u) * Npad + i];
       }
+#pragma unroll
+      for (int u = 0; u < NB; ++u) cur[u] = nxt[u];
     }
   }
   red[w][lane] = make_float2(m, d);
@@ -134,7 +148,7 @@ __global__ void __launch_bounds__(1024) k_merge_tiles(const float2* __restrict__
   __syncthreads();
   if (w == 0 && i < nv) {
     float M = -INFINITY, S = 0.f, Z = 0.f;
-    for (int k = 0; k < 32; ++k) {
+    for (int k = 0; k < MERGE_SL; ++k) {
       const float2 pd = red[k][lane];
       if (pd.y > 0.f) {
         const float mn = fmaxf(M, pd.x);
