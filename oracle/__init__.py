@@ -253,13 +253,13 @@ def to_bf16(a):
     return out
 
 
-def cce_rmsnorm(X_bits, gamma_bits, W_bits, labels, eps=1e-6, ignore_index=-100, dloss=1.0):
+def cce_rmsnorm(X_bits, gamma_bits, W_bits, labels, eps=1e-6, ignore_index=-100, dloss=1.0, **cce_kwargs):
     """The path with the RMSNorm prologue: H = bf16(RMSNorm(X)) (the CE path consumes bf16
     H), the plain CE oracle on H, then the RMSNorm backward of its dH.  Returns
     oracle.cce's dict plus dX [N,D], dgamma [D], rstd [N] and H_bits."""
     y, rstd = rmsnorm_fwd(X_bits, gamma_bits, eps)
     H_bits = to_bf16(y)
-    out = cce(H_bits, W_bits, labels, ignore_index=ignore_index, dloss=dloss)
+    out = cce(H_bits, W_bits, labels, ignore_index=ignore_index, dloss=dloss, **cce_kwargs)
     skip = (np.asarray(labels) == ignore_index).astype(np.int32)
     dx, dg = rmsnorm_bwd(out["dH"], X_bits, gamma_bits, rstd, skip)
     out.update(dX=dx, dgamma=dg, rstd=rstd, H_bits=H_bits)

@@ -256,3 +256,30 @@ def test_standalone_adamw(dev, n, grad_dtype, use_master):
         # theta read from and rounded back to bf16: within one bf16 rounding of the exact result
         got = bf16_to_f64(W)
         assert np.all(np.abs(got - rth) <= np.abs(rth) * 2.0 ** -8 + 1e-12)
+
+
+def test_fused_adamw_with_regularised_loss(dev):
+    """The fused step consumes the regularised dW (label smoothing + z-loss, NEXT #1)."""
+    import torch
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(1000, 128, 41000, seed=23, ignore="bern40")
+    ref = oracle.cce(p["H"], p["W"], p["labels"], label_smoothing=0.1, z_loss=1e-4)
+    g = ref["dW"]
+    gs = float(np.sqrt(np.mean(g * g)))
+    m0, v0 = workload.make_adamw_state(23, g.shape, gs)
+    th0 = _theta0(p)
+    rth, rm, rv = oracle.adamw_step(th0, g, m0, v0, lr=LR, beta1=B1, beta2=B2, eps=EPS, weight_decay=WD, step=6)
+    H, W, y = to_dev(p, dev)
+    master = W.float()
+    m, v = torch.from_numpy(m0).to(dev), torch.from_numpy(v0).to(dev)
+    Wo = torch.empty_like(W)
+    h = cce.CCEHandle(vocab_total=W.shape[0], label_smoothing=0.1, z_loss=1e-4)
+    loss, _, _ = h.forward(H, W, y)
+    opt = cce.adamw_params(m, v, lr=LR, step=6, beta1=B1, beta2=B2, eps=EPS, weight_decay=WD, master=master, W_out=Wo)
+    h.backward_adamw(torch.ones((), dtype=torch.float32, device=dev), torch.empty_like(H), opt)
+    torch.cuda.synchronize()
+    h.close()
+    assert abs(float(loss.item()) - ref["loss"]) <= 2e-3
+    assert rel_fro(m.cpu().numpy().astype(np.float64), rm) <= TOL_GRAD
+    assert rel_fro(v.cpu().numpy().astype(np.float64), rv) <= TOL_GRAD
+    _check_update(master.cpu().numpy().astype(np.float64), rth, th0)

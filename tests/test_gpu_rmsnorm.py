@@ -126,3 +126,27 @@ def test_rmsnorm_prologue_deterministic(dev):
     b = _run(dev, X, g, p["W"], p["labels"])
     for k in ("dX", "dgamma", "dW", "lse"):
         assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("eps_ls,lam,reduction", [(0.1, 1e-4, "mean"), (0.0, 1e-4, "sum")])
+def test_rmsnorm_prologue_with_regularised_loss(dev, eps_ls, lam, reduction):
+    """The prologue composes with label smoothing / z-loss and the sum reduction (the
+    RMSNorm backward consumes whatever dH the CE path produced)."""
+    import torch
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(700, 128, 3000, seed=17, ignore="bern40")
+    X, g = workload.make_rmsnorm_inputs(17, 700, 128)
+    ref = oracle.cce_rmsnorm(X, g, p["W"], p["labels"], eps=EPS, label_smoothing=eps_ls, z_loss=lam,
+                             reduction=reduction)
+    Xt, gt, Wt = _t(X, dev), _t(g, dev), _t(p["W"], dev)
+    yt = torch.from_numpy(p["labels"]).to(dev)
+    h = cce.CCEHandle(vocab_total=3000, label_smoothing=eps_ls, z_loss=lam, reduction=reduction)
+    loss, lse, nv = h.forward_rmsnorm(Xt, gt, EPS, Wt, yt)
+    dX, dg, dW = torch.empty_like(Xt), torch.empty_like(gt), torch.empty_like(Wt)
+    h.backward_rmsnorm(torch.ones((), dtype=torch.float32, device=dev), dX, dg, dW)
+    torch.cuda.synchronize()
+    h.close()
+    assert abs(float(loss.item()) - float(ref["loss"])) <= TOL_LOSS * max(1.0, abs(float(ref["loss"])) * 1e-3)
+    assert rel_fro(bf16_to_f64(dX), ref["dX"]) <= TOL_GRAD
+    assert rel_fro(bf16_to_f64(dg), ref["dgamma"]) <= TOL_GRAD
+    assert rel_fro(bf16_to_f64(dW), ref["dW"]) <= TOL_GRAD
