@@ -255,8 +255,9 @@ def to_bf16(a):
 
 def cce_rmsnorm(X_bits, gamma_bits, W_bits, labels, eps=1e-6, ignore_index=-100, dloss=1.0, **cce_kwargs):
     """The path with the RMSNorm prologue: H = bf16(RMSNorm(X)) (the CE path consumes bf16
-    H), the plain CE oracle on H, then the RMSNorm backward of its dH.  Returns
-    oracle.cce's dict plus dX [N,D], dgamma [D], rstd [N] and H_bits."""
+    H), the CE oracle on H (cce_kwargs: label_smoothing, z_loss, reduction), then
+    the RMSNorm backward of its dH.  Returns oracle.cce's dict plus dX [N,D], dgamma [D],
+    rstd [N] and H_bits."""
     y, rstd = rmsnorm_fwd(X_bits, gamma_bits, eps)
     H_bits = to_bf16(y)
     out = cce(H_bits, W_bits, labels, ignore_index=ignore_index, dloss=dloss, **cce_kwargs)
