@@ -579,14 +579,14 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   int* nvp = at<int>(ws, L.scal);
   int* errp = nvp + 1;
 
-  // a0: label scan + compaction
-  // clear n_valid and the label-error word (reported for this forward by cce_get_error)
-  if (cudaMemsetAsync(nvp, 0, 8, s) != cudaSuccess) return CCE_ERR_CUDA;
-  if (cudaMemsetAsync(at<float>(ws, L.zy_c), 0, (size_t)L.Npad * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+  // a0: label scan + compaction (it also writes n_valid and the label-error word of this
+  // forward, and resets zy_c, the forward queue counters and the finalize counter)
+  if (N == 0 && cudaMemsetAsync(nvp, 0, 16, s) != cudaSuccess) return CCE_ERR_CUDA;
   if (N > 0) {
     { ProfScope ps(h, s, 4);
     k_label_scan<<<1, 1024, 0, s>>>(labels, (int)N, h->cfg.ignore_index, (long long)h->cfg.vocab_total,
-                                    at<int>(ws, L.pos), at<int>(ws, L.idx), at<int>(ws, L.labels_c), nvp, errp); }
+                                    at<int>(ws, L.pos), at<int>(ws, L.idx), at<int>(ws, L.labels_c), nvp, errp,
+                                    at<float>(ws, L.zy_c), (int)L.Npad, at<int>(ws, L.sched), nvp + 2); }
     { ProfScope ps(h, s, 4);
     if (norm)  // RMSNorm prologue: normalise the valid rows on the way into Hc, cache rstd
       k_gather_rmsnorm<<<grid_for(L.Npad, 8, 8 * h->num_sms), 256, 0, s>>>(
@@ -631,7 +631,6 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
       CUtensorMap tA, tB;
       if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM)) return CCE_ERR_CUDA;
       if (!make_map(&tB, W, D, V_local, ldw, quad ? 64 : pairk::PN / 2)) return CCE_ERR_CUDA;
-      if (cudaMemsetAsync(at<int>(ws, L.sched), 0, 8, s) != cudaSuccess) return CCE_ERR_CUDA;
       pairk::PairParams pp{};
       pp.g = p;
       pp.mode = 0;
@@ -700,15 +699,15 @@ static cce_status forward_tail(cce_handle* h, const float4* stats_all, float* lo
   int* nvp = at<int>(ws, L.scal);
   int* errp = nvp + 1;
   if (N > 0) {
+    // per-row LSE / loss and, in the last block, the deterministic loss reduction
     ProfScope ps(h, s, 4);
-    k_finalize<<<grid_for(N, 256, 8 * h->num_sms), 256, 0, s>>>(stats_all, h->cfg.world, (int)L.Npad,
-                                                                at<int>(ws, L.pos), (int)N, lse, at<float>(ws, L.lse_c),
-                                                                at<float>(ws, L.loss_rows), h->cfg.label_smoothing,
-                                                                h->cfg.z_loss,
-                                                                (float)(1.0 / (double)h->cfg.vocab_total),
-                                                                h->cfg.reduction == CCE_REDUCTION_NONE ? loss : nullptr);
-  }
-  {
+    k_finalize_loss<<<grid_for(N, 256, 8 * h->num_sms), 256, 0, s>>>(
+        stats_all, h->cfg.world, (int)L.Npad, at<int>(ws, L.pos), (int)N, lse, at<float>(ws, L.lse_c),
+        at<float>(ws, L.loss_rows), h->cfg.label_smoothing, h->cfg.z_loss, (float)(1.0 / (double)h->cfg.vocab_total),
+        h->cfg.reduction == CCE_REDUCTION_NONE ? loss : nullptr, nvp, errp,
+        h->cfg.reduction == CCE_REDUCTION_NONE ? nullptr : loss, n_valid, h->cfg.reduction == CCE_REDUCTION_SUM ? 1 : 0,
+        nvp + 2);
+  } else {
     ProfScope ps(h, s, 4);
     k_loss<<<1, 1024, 0, s>>>(at<float>(ws, L.loss_rows), nvp, errp,
                               h->cfg.reduction == CCE_REDUCTION_NONE ? nullptr : loss, n_valid,

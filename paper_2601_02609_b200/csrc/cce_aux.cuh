@@ -15,12 +15,23 @@ namespace cce {
 // label n0 + t: coalesced), ranks the valid ones with a warp ballot + block scan and
 // carries the running count, so the compact order equals the original row order.
 // Out-of-range labels set err and are treated as ignored.
+// The same launch also resets the per-forward state the later kernels accumulate into
+// (saves three memsets): the target logits zy_c [Npad] (written only by the tile that owns
+// the label), the forward work-queue head / done counters and the finalize block counter.
 __global__ void __launch_bounds__(1024) k_label_scan(const int32_t* __restrict__ labels, int N, int ignore_index,
                                                      long long vocab_total, int* __restrict__ pos,
                                                      int* __restrict__ idx, int* __restrict__ labels_c,
-                                                     int* __restrict__ n_valid_out, int* __restrict__ err_out) {
+                                                     int* __restrict__ n_valid_out, int* __restrict__ err_out,
+                                                     float* __restrict__ zy_c, int Npad, int* __restrict__ sched2,
+                                                     int* __restrict__ fin_counter) {
   __shared__ int warp_tot[32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int i = t; i < Npad; i += 1024) zy_c[i] = 0.f;
+  if (t == 0) {
+    sched2[0] = 0;
+    sched2[1] = 0;
+    *fin_counter = 0;
+  }
   int base = 0, bad = 0;
   constexpr int ST = 8;  // tiles per super-tile: all its labels are loaded before the scans
   for (int s0 = 0; s0 < N; s0 += ST * 1024) {
@@ -70,7 +81,7 @@ __global__ void __launch_bounds__(1024) k_label_scan(const int32_t* __restrict__
   const int any_bad = __syncthreads_or(bad);
   if (t == 0) {
     *n_valid_out = base;
-    if (any_bad) atomicOr(err_out, 1);
+    *err_out = any_bad ? 1 : 0;  // the flag of THIS forward (cce_get_error)
   }
 }
 
@@ -128,10 +139,15 @@ __global__ void __launch_bounds__(32 * MERGE_SL) k_merge_tiles(const float2* __r
       }
 #pragma unroll
       for (int u = 0; u < NB; ++u) {
+        // one exponential per merge (the larger max keeps its partial unscaled); fast exp
+        // (ex2.approx, reading R16): the kernel is instruction-bound, not memory-bound
         if (cur[u].y > 0.f) {
-          const float mn = fmaxf(m, cur[u].x);
-          d = d * expf(m - mn) + cur[u].y * expf(cur[u].x - mn);
-          m = mn;
+          if (cur[u].x > m) {
+            d = d * __expf(m - cur[u].x) + cur[u].y;
+            m = cur[u].x;
+          } else {
+            d += cur[u].y * __expf(cur[u].x - m);
+          }
         }
       }
       if (zs_part) {
@@ -161,16 +177,22 @@ __global__ void __launch_bounds__(32 * MERGE_SL) k_merge_tiles(const float2* __r
   }
 }
 
+
 // a4 (global part) + a9 combine: merge the per-rank stats in rank order (empty
 // shards contribute m=-inf, d=0), lse = m + log d (Theorem), per-row loss
 // lse - z_y.  Ignored rows get lse = 0 (reading R4).
 // With label smoothing eps / z-loss lambda the row loss is
 //   (1 - eps)(lse - z_y) + eps (lse - sum_v z_v / V_total) + lambda lse^2.
-__global__ void k_finalize(const float4* __restrict__ stats_all, int world, int Npad, const int* __restrict__ pos,
-                           int N, float* __restrict__ lse_out, float* __restrict__ lse_c,
-                           float* __restrict__ loss_rows, float ls_eps, float z_loss, float inv_vtotal,
-                           float* __restrict__ loss_tok) {
-  // loss_tok (reduction "none"): the per-token loss at the original positions, 0 for ignored rows
+// The same launch then reduces the loss: every block publishes
+// its rows (threadfence + counter), and the last block to finish sums loss_rows[0, nv)
+// in a fixed order (thread-strided, then a fixed shuffle tree and warp order), so the
+// result is deterministic; it resets the counter for the next forward.
+__global__ void __launch_bounds__(256) k_finalize_loss(
+    const float4* __restrict__ stats_all, int world, int Npad, const int* __restrict__ pos, int N,
+    float* __restrict__ lse_out, float* __restrict__ lse_c, float* __restrict__ loss_rows, float ls_eps,
+    float z_loss, float inv_vtotal, float* __restrict__ loss_tok, const int* __restrict__ n_valid,
+    const int* __restrict__ err, float* __restrict__ loss, int32_t* __restrict__ n_valid_out, int sum,
+    int* __restrict__ counter) {
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     const int i = pos[n];
     if (i < 0) {
@@ -180,15 +202,15 @@ __global__ void k_finalize(const float4* __restrict__ stats_all, int world, int 
     }
     float m = -INFINITY, zy = 0.f, zs = 0.f;
     for (int r = 0; r < world; ++r) {
-      const float4 s = stats_all[(size_t)r * Npad + i];
-      m = fmaxf(m, s.x);
-      zy += s.z;
-      zs += s.w;
+      const float4 st = stats_all[(size_t)r * Npad + i];
+      m = fmaxf(m, st.x);
+      zy += st.z;
+      zs += st.w;
     }
     float d = 0.f;
     for (int r = 0; r < world; ++r) {
-      const float4 s = stats_all[(size_t)r * Npad + i];
-      if (s.y > 0.f) d += s.y * expf(s.x - m);
+      const float4 st = stats_all[(size_t)r * Npad + i];
+      if (st.y > 0.f) d += st.y * expf(st.x - m);
     }
     const float lse = m + logf(d);
     lse_c[i] = lse;
@@ -198,6 +220,38 @@ __global__ void k_finalize(const float4* __restrict__ stats_all, int world, int 
     loss_rows[i] = l;
     if (loss_tok) loss_tok[n] = l;
     if (lse_out) lse_out[n] = lse;
+  }
+  __shared__ int am_last;
+  __shared__ float red[8];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) am_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  const int nv = *n_valid;
+  // eight independent partial sums per thread (loads in flight), combined in a fixed order
+  float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i0 = threadIdx.x; i0 < nv; i0 += 8 * blockDim.x) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < nv) a8[u] += __ldcg(loss_rows + i);
+    }
+  }
+  float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+    float l = sum ? t : (nv > 0 ? t / (float)nv : 0.f);
+    if (*err) l = __int_as_float(0x7fc00000);
+    if (loss) *loss = l;
+    if (n_valid_out) *n_valid_out = nv;
+    *counter = 0;
   }
 }
 
