@@ -315,6 +315,23 @@ cce_status cce_step_host(cce_handle *h,
                          void *dev_inputs, size_t dev_inputs_bytes,
                          void *workspace, size_t workspace_bytes, void *stream);
 
+/*
+ * cce_step_host without the final synchronisation, for a training loop that keeps the
+ * next batch's upload in flight (the paper's zero-sync principle): the
+ * H2D copies run on `copy_stream` (NULL or equal to `stream`: no overlap) after the
+ * previous step that used the same `dev_inputs` buffer has finished with it, the compute
+ * waits for them on `stream`, and the loss is copied to `loss_host` (pinned memory) at
+ * the end of the step on `stream`.  Rotate two (at most four) staging buffers so step i+1's
+ * copy overlaps step i's compute; synchronise `stream` before reading loss_host.
+ */
+cce_status cce_step_host_async(cce_handle *h,
+                               const void *H_host, int64_t N, int64_t D,
+                               const int32_t *labels_host,
+                               const void *W, int64_t V_local, int64_t ldw,
+                               float *loss_host, void *dH, void *dW,
+                               void *dev_inputs, size_t dev_inputs_bytes,
+                               void *workspace, size_t workspace_bytes, void *stream, void *copy_stream);
+
 /* NCCL plumbing for world > 1 (NCCL is resolved at run time with dlopen; the
  * library does not link it).  The 128-byte unique id is produced on rank 0 and
  * broadcast by the caller (e.g. over torch.distributed). */

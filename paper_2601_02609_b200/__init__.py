@@ -30,7 +30,7 @@ EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_byt
            "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info",
            "cce_profile_enable", "cce_profile_read", "cce_debug_trace", "cce_backward_adamw", "cce_adamw_step",
            "cce_forward_rmsnorm", "cce_backward_rmsnorm", "cce_combine_offsets", "cce_forward_finish",
-           "cce_backward_finish"]
+           "cce_backward_finish", "cce_step_host_async"]
 PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 # "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
 # FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
@@ -112,6 +112,8 @@ def lib():
         L.cce_host_staging_bytes.restype = sz
         L.cce_step_host.argtypes = [p, p, i64, i64, p, p, i64, i64, p, p, p, p, sz, p, sz, p]
         L.cce_step_host.restype = st
+        L.cce_step_host_async.argtypes = [p, p, i64, i64, p, p, i64, i64, p, p, p, p, sz, p, sz, p, p]
+        L.cce_step_host_async.restype = st
         L.cce_nccl_unique_id.argtypes = [p]
         L.cce_nccl_unique_id.restype = st
         L.cce_nccl_comm_init.argtypes = [ctypes.POINTER(p), i32, p, i32]
@@ -265,6 +267,20 @@ def cce_step_host(h, H_host, labels_host, W, dH, dW, staging, workspace, stream=
                                _ptr(staging), staging.numel() * staging.element_size(), _ptr(workspace),
                                workspace.numel() * workspace.element_size(), _stream(stream)), "cce_step_host")
     return out.value
+
+
+def cce_step_host_async(h, H_host, labels_host, W, dH, dW, staging, workspace, loss_host, stream=None,
+                        copy_stream=None):
+    """Enqueue one end-to-end step (host H / labels in, loss out to loss_host, a pinned float32
+    tensor element or array) without synchronising; see cce.h."""
+    N, D = H_host.shape
+    _check(lib().cce_step_host_async(h, ctypes.c_void_p(H_host.data_ptr()), N, D,
+                                     ctypes.c_void_p(labels_host.data_ptr()), _ptr(W), W.shape[0], W.stride(0),
+                                     ctypes.c_void_p(loss_host.data_ptr()), _ptr(dH), _ptr(dW), _ptr(staging),
+                                     staging.numel() * staging.element_size(), _ptr(workspace),
+                                     workspace.numel() * workspace.element_size(), _stream(stream),
+                                     None if copy_stream is None else ctypes.c_void_p(copy_stream.cuda_stream)),
+           "cce_step_host_async")
 
 
 def cce_kernel_launches(h) -> int:

@@ -47,6 +47,10 @@ struct cce_handle {
   float* p_lse = nullptr;
   int32_t* p_nv = nullptr;
   void* p_dH = nullptr;
+  // cce_step_host_async: per staging buffer, the event after which its inputs are consumed
+  struct Stage { const void* buf; cudaEvent_t consumed; };
+  Stage stages[4] = {};
+  cudaEvent_t ev_copied = nullptr;
   const void* nX = nullptr;
   int64_t ldx = 0;
   const void* gamma = nullptr;
@@ -476,6 +480,9 @@ cce_status cce_destroy(cce_handle* h) {
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  for (auto& e : h->stages)
+    if (e.consumed) cudaEventDestroy(e.consumed);
+  if (h->ev_copied) cudaEventDestroy(h->ev_copied);
   delete h;
   return CCE_OK;
 }
@@ -1040,10 +1047,10 @@ size_t cce_host_staging_bytes(int64_t N, int64_t D) {
   return align_up((size_t)N * D * 2, 256) + align_up((size_t)(N > 0 ? N : 1) * 4, 256) + 256;
 }
 
-cce_status cce_step_host(cce_handle* h, const void* H_host, int64_t N, int64_t D, const int32_t* labels_host,
-                         const void* W, int64_t V_local, int64_t ldw, float* loss_host, void* dH, void* dW,
-                         void* dev_inputs, size_t dev_inputs_bytes, void* workspace, size_t workspace_bytes,
-                         void* stream) {
+static cce_status step_host_impl(cce_handle* h, const void* H_host, int64_t N, int64_t D, const int32_t* labels_host,
+                                 const void* W, int64_t V_local, int64_t ldw, float* loss_host, void* dH, void* dW,
+                                 void* dev_inputs, size_t dev_inputs_bytes, void* workspace, size_t workspace_bytes,
+                                 void* stream, void* copy_stream, bool sync) {
   if (!h || !loss_host || (N > 0 && (!H_host || !labels_host))) return CCE_ERR_INVALID_VALUE;
   if (N < 0 || D <= 0) return CCE_ERR_INVALID_VALUE;
   if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) return CCE_ERR_UNSUPPORTED;
@@ -1051,15 +1058,37 @@ cce_status cce_step_host(cce_handle* h, const void* H_host, int64_t N, int64_t D
     return CCE_ERR_WORKSPACE;
   if (h->cfg.reduction == CCE_REDUCTION_NONE) return CCE_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t cs = copy_stream ? static_cast<cudaStream_t>(copy_stream) : s;
   char* base = static_cast<char*>(dev_inputs);
   void* Hd = base;
   int32_t* yd = reinterpret_cast<int32_t*>(base + align_up((size_t)N * D * 2, 256));
   float* scal = reinterpret_cast<float*>(base + align_up((size_t)N * D * 2, 256) + align_up((size_t)(N > 0 ? N : 1) * 4, 256));
   float* loss_d = scal;
   float* dloss_d = scal + 1;
+  cce_handle::Stage* stg = nullptr;
+  if (cs != s) {
+    // the staging buffer's previous step must be done with it before the copy overwrites it
+    for (auto& e : h->stages)
+      if (e.buf == dev_inputs) { stg = &e; break; }
+    if (!stg) {
+      for (auto& e : h->stages)
+        if (!e.buf) { stg = &e; break; }
+      if (!stg) return CCE_ERR_INVALID_VALUE;  // more than four staging buffers in rotation
+      stg->buf = dev_inputs;
+      if (cudaEventCreateWithFlags(&stg->consumed, cudaEventDisableTiming) != cudaSuccess) return CCE_ERR_CUDA;
+      if (cudaEventRecord(stg->consumed, s) != cudaSuccess) return CCE_ERR_CUDA;
+    }
+    if (!h->ev_copied && cudaEventCreateWithFlags(&h->ev_copied, cudaEventDisableTiming) != cudaSuccess)
+      return CCE_ERR_CUDA;
+    if (cudaStreamWaitEvent(cs, stg->consumed, 0) != cudaSuccess) return CCE_ERR_CUDA;
+  }
   if (N > 0) {
-    if (cudaMemcpyAsync(Hd, H_host, (size_t)N * D * 2, cudaMemcpyHostToDevice, s) != cudaSuccess) return CCE_ERR_CUDA;
-    if (cudaMemcpyAsync(yd, labels_host, (size_t)N * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return CCE_ERR_CUDA;
+    if (cudaMemcpyAsync(Hd, H_host, (size_t)N * D * 2, cudaMemcpyHostToDevice, cs) != cudaSuccess) return CCE_ERR_CUDA;
+    if (cudaMemcpyAsync(yd, labels_host, (size_t)N * 4, cudaMemcpyHostToDevice, cs) != cudaSuccess) return CCE_ERR_CUDA;
+  }
+  if (cs != s) {
+    if (cudaEventRecord(h->ev_copied, cs) != cudaSuccess || cudaStreamWaitEvent(s, h->ev_copied, 0) != cudaSuccess)
+      return CCE_ERR_CUDA;
   }
   cce_status st = cce_forward(h, N > 0 ? Hd : nullptr, N, D, D, W, V_local, ldw, N > 0 ? yd : nullptr, loss_d, nullptr,
                               nullptr, workspace, workspace_bytes, stream);
@@ -1071,8 +1100,25 @@ cce_status cce_step_host(cce_handle* h, const void* H_host, int64_t N, int64_t D
   st = cce_backward(h, dloss_d, dH, dW, stream);
   if (st != CCE_OK) return st;
   if (cudaMemcpyAsync(loss_host, loss_d, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CCE_ERR_CUDA;
-  if (cudaStreamSynchronize(s) != cudaSuccess) return CCE_ERR_CUDA;
+  if (stg && cudaEventRecord(stg->consumed, s) != cudaSuccess) return CCE_ERR_CUDA;
+  if (sync && cudaStreamSynchronize(s) != cudaSuccess) return CCE_ERR_CUDA;
   return CCE_OK;
+}
+
+cce_status cce_step_host(cce_handle* h, const void* H_host, int64_t N, int64_t D, const int32_t* labels_host,
+                         const void* W, int64_t V_local, int64_t ldw, float* loss_host, void* dH, void* dW,
+                         void* dev_inputs, size_t dev_inputs_bytes, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  return step_host_impl(h, H_host, N, D, labels_host, W, V_local, ldw, loss_host, dH, dW, dev_inputs, dev_inputs_bytes,
+                        workspace, workspace_bytes, stream, nullptr, true);
+}
+
+cce_status cce_step_host_async(cce_handle* h, const void* H_host, int64_t N, int64_t D, const int32_t* labels_host,
+                               const void* W, int64_t V_local, int64_t ldw, float* loss_host, void* dH, void* dW,
+                               void* dev_inputs, size_t dev_inputs_bytes, void* workspace, size_t workspace_bytes,
+                               void* stream, void* copy_stream) {
+  return step_host_impl(h, H_host, N, D, labels_host, W, V_local, ldw, loss_host, dH, dW, dev_inputs, dev_inputs_bytes,
+                        workspace, workspace_bytes, stream, copy_stream, false);
 }
 
 cce_status cce_nccl_unique_id(void* id_out) {

@@ -273,6 +273,38 @@ def test_step_host_matches_device_path(dev):
     h.close()
 
 
+def test_step_host_async_pipeline(dev):
+    """cce_step_host_async with two staging buffers rotated on a copy stream: different
+    batches per step, each step's loss / gradients equal the synchronous path's bits."""
+    import torch
+    import paper_2601_02609_b200 as cce
+    probs = [workload.make_problem(300, 128, 4000, seed=40 + i, ignore="bern40") for i in range(4)]
+    _, W, _ = to_dev(probs[0], dev)
+    Hs = [torch.from_numpy(p["H"].view(np.int16)).view(torch.bfloat16).pin_memory() for p in probs]
+    ys = [torch.from_numpy(p["labels"]).pin_memory() for p in probs]
+    h = cce.CCEHandle(vocab_total=4000)
+    ws = h.workspace(300, 128, 4000, dev)
+    nb = cce.cce_host_staging_bytes(300, 128)
+    stages = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    dHs = [torch.empty((300, 128), dtype=torch.bfloat16, device=dev) for _ in range(4)]
+    dWs = [torch.empty((4000, 128), dtype=torch.bfloat16, device=dev) for _ in range(4)]
+    losses = torch.empty(4, dtype=torch.float32).pin_memory()
+    copy = torch.cuda.Stream()
+    for i in range(4):
+        cce.cce_step_host_async(h.h, Hs[i], ys[i], W, dHs[i], dWs[i], stages[i % 2], ws, losses[i], None, copy)
+    torch.cuda.synchronize()
+    for i in range(4):
+        dH = torch.empty_like(dHs[i])
+        dW = torch.empty_like(dWs[i])
+        l_sync = cce.cce_step_host(h.h, Hs[i], ys[i], W, dH, dW, stages[0], ws)
+        assert losses[i].item() == l_sync
+        assert torch.equal(dH.view(torch.int16), dHs[i].view(torch.int16))
+        assert torch.equal(dW.view(torch.int16), dWs[i].view(torch.int16))
+        ref = oracle.cce(probs[i]["H"], probs[0]["W"], probs[i]["labels"])   # W is shared by the steps
+        assert abs(l_sync - ref["loss"]) <= 2e-3
+    h.close()
+
+
 def test_nccl_path_on_one_rank(dev):
     """The vocabulary-sharded combine (a9 stats allgather, a10 dH all-reduce) through a
     real 1-rank NCCL communicator: the collectives are identities, so every output must
