@@ -57,6 +57,8 @@ def test_multi_tile_shapes(dev, N, D, V, ign, flags, monkeypatch):
     (520, 2048, 9000, "none"),     # configs[2] hidden size (paper memory example), 0% ignored
     (300, 4096, 5000, "bern40"),   # configs[3] hidden size (Llama-3-8B head), ragged rows / vocabulary
     (700, 3584, 6100, "bern40"),   # configs[4] hidden size (Qwen2.5-7B head), 14 x 256 hidden tiles
+    (260, 8192, 2300, "bern40"),   # Llama-3-70B-class hidden size: 128 k-blocks per logit tile, 32 hidden tiles
+    (333, 5120, 4100, "none"),     # 5120 = 20 hidden tiles, ragged rows / vocabulary
 ])
 def test_large_hidden_sizes(dev, N, D, V, ign):
     """The wide-hidden configurations: D = 2048 / 3584 / 4096 (8 / 14 / 16 hidden tiles
