@@ -100,6 +100,13 @@ typedef enum {
  * shards): see cce_combine_offsets / cce_forward_finish / cce_backward_finish.  Not with
  * cce_backward_rmsnorm, cce_backward_adamw or cce_step_host (CCE_ERR_UNSUPPORTED). */
 #define CCE_FLAG_EXTERNAL_COMBINE 256u
+/* Sequence-sharded dH (for sequence-parallel callers): with world P,
+ * cce_backward writes only this rank's slice of dH, the original rows
+ * [rank S, min(N, (rank + 1) S)) with S = ceil(N / P), as a dense [n_r, D] array; the
+ * partial dH of the ranks is reduce-scattered (ncclReduceScatter, half the bytes of the
+ * all-reduce) instead of all-reduced.  World 1: the full dH.  Not with
+ * cce_backward_rmsnorm (CCE_ERR_UNSUPPORTED). */
+#define CCE_FLAG_DH_SEQ_SHARD 512u
 
 /* Reduction of the per-token losses (cce_config.reduction). */
 #define CCE_REDUCTION_MEAN 0  /* loss = sum_valid l_n / n_valid (default) */
@@ -286,7 +293,10 @@ cce_status cce_adamw_step(const cce_adamw_params *opt, const void *grad, int32_t
  * cce_combine_offsets: byte offsets inside the workspace for a problem (N, D, V_local):
  *   out4[0] this rank's stats   float [Npad][4]          (m, d, z_y, sum of logits)
  *   out4[1] all ranks' stats    float [world][Npad][4]
- *   out4[2] partial dH          float [Npad][D]
+ *   out4[2] partial dH          float [Npad][D] compact valid rows; with
+ *                               CCE_FLAG_DH_SEQ_SHARD float [P S][D] in original row order,
+ *                               to be reduce-scattered: rank r's summed slice (S rows) goes
+ *                               at row r S of its own array before cce_backward_finish
  *   out4[3] Npad (rows of those arrays; rows >= n_valid are ignored)
  * The finish calls return CCE_ERR_NO_FORWARD without a pending phase.
  */

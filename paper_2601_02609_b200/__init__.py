@@ -42,6 +42,7 @@ FLAG_QUAD = 32
 FLAG_GRAD_FP32 = 64
 FLAG_ACCUMULATE = 128
 FLAG_EXTERNAL_COMBINE = 256
+FLAG_DH_SEQ_SHARD = 512
 REDUCTION_MEAN, REDUCTION_SUM, REDUCTION_NONE = 0, 1, 2
 _REDUCTIONS = {"mean": REDUCTION_MEAN, "sum": REDUCTION_SUM, "none": REDUCTION_NONE}
 

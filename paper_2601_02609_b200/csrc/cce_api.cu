@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -177,6 +178,7 @@ typedef int (*nccl_init_t)(void**, int, NcclId, int);
 typedef int (*nccl_destroy_t)(void*);
 typedef int (*nccl_allgather_t)(const void*, void*, size_t, int, void*, cudaStream_t);
 typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_reducescatter_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 struct Nccl {
   bool ok = false;
   nccl_get_id_t get_id;
@@ -184,6 +186,7 @@ struct Nccl {
   nccl_destroy_t destroy;
   nccl_allgather_t allgather;
   nccl_allreduce_t allreduce;
+  nccl_reducescatter_t reducescatter;
 };
 const int kNcclFloat32 = 7, kNcclSum = 0;
 
@@ -200,7 +203,8 @@ Nccl& nccl() {
     n.destroy = (nccl_destroy_t)dlsym(h, "ncclCommDestroy");
     n.allgather = (nccl_allgather_t)dlsym(h, "ncclAllGather");
     n.allreduce = (nccl_allreduce_t)dlsym(h, "ncclAllReduce");
-    n.ok = n.get_id && n.init && n.destroy && n.allgather && n.allreduce;
+    n.reducescatter = (nccl_reducescatter_t)dlsym(h, "ncclReduceScatter");
+    n.ok = n.get_id && n.init && n.destroy && n.allgather && n.allreduce && n.reducescatter;
   });
   return n;
 }
@@ -216,10 +220,11 @@ struct Layout {
   int64_t Npad, Tv, C;
   int64_t n_chunks, sched_ints;
   size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, dloss_c, gbuf,
-      dH32, sched, rstd_c, gpart, total;
+      dH32, sched, rstd_c, gpart, dHo, total;
+  int64_t seq_slice;  // CCE_FLAG_DH_SEQ_SHARD: rows per rank of the original-order dH (0 otherwise)
 };
 
-Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots) {
+Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots, bool seq = false) {
   Layout L;
   L.Npad = align_up((size_t)(N > 0 ? N : 1), 256);  // pair tiles are 256 rows
   L.Tv = (V_local + BN - 1) / BN;
@@ -255,6 +260,9 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
   L.sched = take((size_t)L.sched_ints * 4);
   L.rstd_c = take((size_t)L.Npad * 4);            // RMSNorm prologue: rstd per compact row
   L.gpart = take((size_t)RMS_GP * D * 4);          // RMSNorm backward: per-block dgamma partials
+  // CCE_FLAG_DH_SEQ_SHARD: this rank's partial dH in original row order, world x slice rows
+  L.seq_slice = seq ? (N + world - 1) / world : 0;
+  L.dHo = take(seq ? (size_t)world * L.seq_slice * D * 4 : 0);
   L.total = o;
   return L;
 }
@@ -489,7 +497,7 @@ cce_status cce_destroy(cce_handle* h) {
 
 size_t cce_workspace_bytes(const cce_handle* h, int64_t N, int64_t D, int64_t V_local) {
   if (!h || N < 0 || D <= 0 || V_local < 0) return 0;
-  return layout(N, D, V_local, h->cfg.world, h->chunk, h->slots).total;
+  return layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0).total;
 }
 
 int64_t cce_kernel_launches(const cce_handle* h) { return h ? h->launches : 0; }
@@ -578,7 +586,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   if (D % 64 != 0 || N > (1LL << 30) || V_local > (1LL << 30)) return CCE_ERR_UNSUPPORTED;
   if ((N > 0 && !aligned16(H)) || (V_local > 0 && !aligned16(W)) || (ldh * 2) % 16 || (ldw * 2) % 16)
     return CCE_ERR_UNSUPPORTED;
-  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
   if (!workspace || workspace_bytes < L.total || !aligned16(workspace)) return CCE_ERR_WORKSPACE;
   if (!get_encode()) return CCE_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -701,7 +709,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
 static cce_status forward_tail(cce_handle* h, const float4* stats_all, float* loss, float* lse, int32_t* n_valid,
                                cudaStream_t s) {
   const int64_t N = h->N;
-  const Layout L = layout(N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots);
+  const Layout L = layout(N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
   void* ws = h->ws;
   int* nvp = at<int>(ws, L.scal);
   int* errp = nvp + 1;
@@ -729,17 +737,19 @@ cce_status cce_forward_finish(cce_handle* h, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   if (!h->fwd_pending) return CCE_ERR_NO_FORWARD;
   h->fwd_pending = false;
-  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
   return forward_tail(h, at<float4>(h->ws, L.stats_all), h->p_loss, h->p_lse, h->p_nv,
                       static_cast<cudaStream_t>(stream));
 }
 
 cce_status cce_combine_offsets(const cce_handle* h, int64_t N, int64_t D, int64_t V_local, int64_t* out4) {
   if (!h || !out4 || N < 0 || D <= 0 || V_local < 0) return CCE_ERR_INVALID_VALUE;
-  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
   out4[0] = (int64_t)L.stats;      // this rank's stats: float [Npad][4] (m, d, z_y, sum z)
   out4[1] = (int64_t)L.stats_all;  // all ranks' stats: float [world][Npad][4], rank-major
-  out4[2] = (int64_t)L.dH32;       // this rank's partial dH: float [Npad][D], compact valid rows
+  // this rank's partial dH: float [Npad][D] compact valid rows, or with CCE_FLAG_DH_SEQ_SHARD
+  // float [world x slice][D] in original row order (rank r's slice at r x slice rows)
+  out4[2] = (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) ? (int64_t)L.dHo : (int64_t)L.dH32;
   out4[3] = L.Npad;
   return CCE_OK;
 }
@@ -774,7 +784,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
 
 cce_status cce_backward_rmsnorm(cce_handle* h, const float* dloss, void* dX, void* dgamma, void* dW, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
-  if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) return CCE_ERR_UNSUPPORTED;
+  if (h->cfg.flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD)) return CCE_ERR_UNSUPPORTED;
   if (!h->have_fwd || !h->norm) return CCE_ERR_NO_FORWARD;
   if (!dgamma) return CCE_ERR_INVALID_VALUE;
   if (!aligned16(dgamma)) return CCE_ERR_UNSUPPORTED;
@@ -805,6 +815,18 @@ cce_status cce_adamw_step(const cce_adamw_params* opt, const void* grad, int32_t
   return launch_adamw(opt, grad, grad_fp32 ? 1 : 0, n, W_bf16, static_cast<cudaStream_t>(stream));
 }
 
+// CCE_FLAG_DH_SEQ_SHARD: this rank's reduced slice of the original-order dH -> dH [n_r, D]
+static cce_status seq_rows_out(cce_handle* h, const Layout& L, void* dH, cudaStream_t s) {
+  const int64_t slice = L.seq_slice, r = h->cfg.rank;
+  const int64_t n_r = std::max<int64_t>(0, std::min<int64_t>(slice, h->N - r * slice));
+  if (n_r == 0) return CCE_OK;
+  ProfScope ps(h, s, 4);
+  k_rows_out<<<grid_for(n_r * h->D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(
+      at<float>(h->ws, L.dHo) + r * slice * h->D, (int)n_r, (int)h->D, dH,
+      (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0, (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0);
+  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+}
+
 static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, void* dW, const cce_adamw_params* opt,
                                 void* stream, void* dgamma, bool norm) {
   if (!h) return CCE_ERR_INVALID_VALUE;
@@ -813,7 +835,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
   if ((dH && !aligned16(dH)) || (dW && !aligned16(dW))) return CCE_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t N = h->N, D = h->D, V_local = h->V_local;
-  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
   void* ws = h->ws;
   int* nvp = at<int>(ws, L.scal);
   float* dH32 = at<float>(ws, L.dH32);
@@ -960,8 +982,19 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
         cudaMemsetAsync(dW, 0, (size_t)V_local * D * ((h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 4 : 2), s) != cudaSuccess)
       return CCE_ERR_CUDA;
   }
+  const bool seq = (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0;
+  float* dHo = seq ? at<float>(ws, L.dHo) : nullptr;
   if (N > 0) {
     if (V_local == 0 && cudaMemsetAsync(dH32, 0, (size_t)L.Npad * D * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+    if (seq) {
+      // sequence-sharded dH: this rank's partial in ORIGINAL row order (ignored rows 0, pad
+      // rows up to world x slice zeroed), the array the reduce-scatter splits by rank
+      ProfScope ps(h, s, 4);
+      k_scatter_dH<<<grid_for((long long)N * D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(dH32, at<int>(ws, L.pos),
+                                                                                       (int)N, (int)D, dHo, 1, 0);
+      const int64_t pad = h->cfg.world * L.seq_slice - N;
+      if (pad > 0 && cudaMemsetAsync(dHo + N * D, 0, (size_t)pad * D * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+    }
     if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) {
       // a10 done by the caller: it sums every rank's partial dH32 in place, then calls
       // cce_backward_finish (the scatter to dH)
@@ -971,12 +1004,19 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       return CCE_OK;
     }
     if (h->cfg.nccl_comm) {
-      // a10: dH partials summed over the vocabulary shards
+      // a10: dH partials summed over the vocabulary shards (all-reduce), or reduce-scattered
+      // by sequence slice (CCE_FLAG_DH_SEQ_SHARD; in place: rank r's slice at r x slice rows)
       Nccl& n = nccl();
       if (!n.ok) return CCE_ERR_NCCL;
-      if (n.allreduce(dH32, dH32, (size_t)L.Npad * D, kNcclFloat32, kNcclSum, h->cfg.nccl_comm, s) != 0)
+      if (seq) {
+        const size_t cnt = (size_t)L.seq_slice * D;
+        if (n.reducescatter(dHo, dHo + (size_t)h->cfg.rank * cnt, cnt, kNcclFloat32, kNcclSum, h->cfg.nccl_comm, s) != 0)
+          return CCE_ERR_NCCL;
+      } else if (n.allreduce(dH32, dH32, (size_t)L.Npad * D, kNcclFloat32, kNcclSum, h->cfg.nccl_comm, s) != 0) {
         return CCE_ERR_NCCL;
+      }
     }
+    if (seq) return seq_rows_out(h, L, dH, s);
     if (norm) {
       // RMSNorm backward from the unrounded fp32 dH: dX (valid rows), dgamma, zeros for ignored rows
       const int gf = (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0, ac = (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0;
@@ -1018,7 +1058,8 @@ cce_status cce_backward_finish(cce_handle* h, void* stream) {
   if (!h->bwd_pending) return CCE_ERR_NO_FORWARD;
   h->bwd_pending = false;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
+  if (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) return seq_rows_out(h, L, h->p_dH, s);
   ProfScope ps(h, s, 4);
   k_scatter_dH<<<grid_for((long long)h->N * h->D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(
       at<float>(h->ws, L.dH32), at<int>(h->ws, L.pos), (int)h->N, (int)h->D, h->p_dH,
@@ -1030,7 +1071,7 @@ cce_status cce_get_error(cce_handle* h, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!h->ws) return CCE_OK;
-  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
   int* errp = at<int>(h->ws, L.scal) + 1;
   int err = 0;
   if (cudaMemcpyAsync(&err, errp, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CCE_ERR_CUDA;

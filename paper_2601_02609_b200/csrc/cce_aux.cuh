@@ -342,6 +342,41 @@ __global__ void k_scatter_dH(const float* __restrict__ dH32, const int* __restri
 
 __global__ void k_set_scalar(float* p, float v) { *p = v; }
 
+// CCE_FLAG_DH_SEQ_SHARD: rows of an fp32 dH slice -> the caller's dH (bf16 or fp32, overwrite or add).
+__global__ void k_rows_out(const float* __restrict__ src, int rows, int D, void* __restrict__ dst, int fp32,
+                           int accumulate) {
+  const long long total = (long long)rows * D / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    float4 a = reinterpret_cast<const float4*>(src)[2 * i], b = reinterpret_cast<const float4*>(src)[2 * i + 1];
+    if (fp32) {
+      float4* d = reinterpret_cast<float4*>(dst) + 2 * i;
+      if (accumulate) {
+        const float4 o0 = d[0], o1 = d[1];
+        a.x += o0.x; a.y += o0.y; a.z += o0.z; a.w += o0.w;
+        b.x += o1.x; b.y += o1.y; b.z += o1.z; b.w += o1.w;
+      }
+      d[0] = a;
+      d[1] = b;
+    } else {
+      uint4* d = reinterpret_cast<uint4*>(dst) + i;
+      float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      if (accumulate) {
+        const uint4 o = *d;
+        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          f[2 * k] += __uint_as_float(w[k] << 16);
+          f[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
+        }
+      }
+      __nv_bfloat162 q0 = __floats2bfloat162_rn(f[0], f[1]), q1 = __floats2bfloat162_rn(f[2], f[3]);
+      __nv_bfloat162 q2 = __floats2bfloat162_rn(f[4], f[5]), q3 = __floats2bfloat162_rn(f[6], f[7]);
+      *d = make_uint4(*reinterpret_cast<uint32_t*>(&q0), *reinterpret_cast<uint32_t*>(&q1),
+                      *reinterpret_cast<uint32_t*>(&q2), *reinterpret_cast<uint32_t*>(&q3));
+    }
+  }
+}
+
 // reduction "none": the per-token upstream gradients of the valid rows in compact order.
 __global__ void k_gather_dloss(const float* __restrict__ dloss, const int* __restrict__ idx,
                                const int* __restrict__ n_valid, int Npad, float* __restrict__ dloss_c) {

@@ -128,3 +128,90 @@ def test_labels_in_a_shards_padded_tail(dev, world):
     assert np.isfinite(res[0]["loss"]) and abs(res[0]["loss"] - ref["loss"]) <= TOL_LOSS
     assert rel_fro(res[0]["dH"], ref["dH"]) <= TOL_GRAD
     assert rel_fro(dW, ref["dW"]) <= TOL_GRAD
+
+
+def _sharded_seq(dev, p, world):
+    """CCE_FLAG_DH_SEQ_SHARD with the split-phase combine: the stats allgather as above,
+    then each rank's partial dH in original row order is reduce-scattered (torch sum in rank
+    order; rank r's slice placed at row r*S of its own array) and cce_backward_finish writes
+    that rank's [n_r, D] rows."""
+    import torch
+    import paper_2601_02609_b200 as cce
+    H, W, y = to_dev(p, dev)
+    N, D = H.shape
+    V = W.shape[0]
+    S = (N + world - 1) // world
+    hs = []
+    for r in range(world):
+        lo, hi = cce.shard_range(V, r, world)
+        Wr = W[lo:hi].contiguous()
+        h = cce.CCEHandle(vocab_total=V, vocab_offset=lo, rank=r, world=world,
+                          flags=cce.FLAG_EXTERNAL_COMBINE | cce.FLAG_DH_SEQ_SHARD)
+        loss, lse, nv = h.forward(H, Wr, y)
+        hs.append((h, Wr, loss, cce.cce_combine_offsets(h.h, N, D, hi - lo)))
+    allstats = torch.cat([h._ws[so:so + npad * 16].view(torch.float32).clone()
+                          for h, _, _, (so, sao, dho, npad) in hs])
+    for h, _, _, (so, sao, dho, npad) in hs:
+        h._ws[sao:sao + world * npad * 16].view(torch.float32).copy_(allstats)
+        cce.cce_forward_finish(h.h)
+    one = torch.ones((), dtype=torch.float32, device=dev)
+    dHs, dWs = [], []
+    for r, (h, Wr, _, _) in enumerate(hs):
+        n_r = max(0, min(S, N - r * S))
+        dH = torch.full((max(n_r, 1), D), float("nan"), dtype=torch.bfloat16, device=dev)
+        dW = torch.empty_like(Wr)
+        h.backward(one, dH, dW)
+        dHs.append((dH, n_r))
+        dWs.append(dW)
+    tot = None
+    for h, _, _, (so, sao, dho, npad) in hs:
+        part = h._ws[dho:dho + world * S * D * 4].view(torch.float32)
+        tot = part.clone() if tot is None else tot + part
+    for r, (h, _, _, (so, sao, dho, npad)) in enumerate(hs):
+        h._ws[dho + r * S * D * 4:dho + (r + 1) * S * D * 4].view(torch.float32).copy_(tot[r * S * D:(r + 1) * S * D])
+        cce.cce_backward_finish(h.h)
+    torch.cuda.synchronize()
+    dH = np.concatenate([bf16_to_f64(d)[:n] for d, n in dHs])
+    loss = hs[0][2].item()
+    for h, *_ in hs:
+        h.close()
+    return loss, dH, np.concatenate([bf16_to_f64(d) for d in dWs])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_sequence_sharded_dH(dev, world):
+    """CCE_FLAG_DH_SEQ_SHARD (NEXT #4): every rank gets its own ceil(N/P) original rows of dH
+    (N = 700 is not a multiple of 3: ragged last slice)."""
+    p = workload.make_problem(700, 128, 3000, seed=91 + world, ignore="bern40")
+    loss, dH, dW = _sharded_seq(dev, p, world)
+    ref = oracle.cce(p["H"], p["W"], p["labels"])
+    assert abs(loss - ref["loss"]) <= TOL_LOSS
+    assert dH.shape == ref["dH"].shape
+    assert np.all(dH[p["labels"] == -100] == 0)
+    assert rel_fro(dH, ref["dH"]) <= TOL_GRAD
+    assert rel_fro(dW, ref["dW"]) <= TOL_GRAD
+
+
+def test_sequence_sharded_dH_nccl_one_rank(dev):
+    """The NCCL reduce-scatter on a 1-rank communicator is the identity: dH bit-identical to
+    the plain path."""
+    import torch
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(700, 256, 9000, seed=29, ignore="bern40")
+    H, W, y = to_dev(p, dev)
+    one = torch.ones((), dtype=torch.float32, device=dev)
+    outs = []
+    comm = cce.cce_nccl_comm_init(1, cce.cce_nccl_unique_id(), 0)
+    try:
+        for flags, c in ((0, None), (cce.FLAG_DH_SEQ_SHARD, comm)):
+            h = cce.CCEHandle(vocab_total=9000, nccl_comm=c, flags=flags)
+            h.forward(H, W, y)
+            dH = torch.empty_like(H)
+            dW = torch.empty_like(W)
+            h.backward(one, dH, dW)
+            torch.cuda.synchronize()
+            outs.append((dH.view(torch.int16).cpu(), dW.view(torch.int16).cpu()))
+            h.close()
+    finally:
+        cce.cce_nccl_comm_destroy(comm)
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
