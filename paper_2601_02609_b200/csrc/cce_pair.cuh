@@ -436,25 +436,6 @@ __device__ __forceinline__ void epi_dw_adamw(const GemmParams& p, uint32_t taddr
   __syncwarp();
 }
 
-// Fused AdamW: before waiting for a DW item's accumulator, each epilogue thread pulls its
-// row segment of the optimizer state (m, v, master or the bf16 theta) into L2, so the
-// epilogue's loads hit L2 instead of HBM and the HBM reads overlap the item's MMAs.
-__device__ __forceinline__ void prefetch_dw_adamw(const GemmParams& p, const PEpi& e, const PItem& it) {
-  const int c0 = it.c * p.C;
-  const int width = min(p.C, p.V_local - c0);
-  const int vrow = it.m0 + e.rank * HM + e.rit;
-  const int hw = it.N / 2;
-  const int d0 = it.n0 + e.half * hw;
-  if (vrow >= width || d0 >= p.D) return;
-  const int cols = min(hw, p.D - d0);
-  const size_t off = (size_t)(c0 + vrow) * p.D + d0;
-  bulk_prefetch_l2(p.am + off, cols * 4);
-  bulk_prefetch_l2(p.av + off, cols * 4);
-  if (p.master) bulk_prefetch_l2(p.master + off, cols * 4);
-  else bulk_prefetch_l2(p.Win + (size_t)(c0 + vrow) * p.ldw + d0, cols * 2);
-  if (p.grad_in) bulk_prefetch_l2(p.grad_in + off, cols * 4);
-}
-
 __device__ __forceinline__ void epi_dh(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv) {
   const int t = it.m0 + e.rank * HM + e.rit;  // compact row
   const int hw = it.N / 2;
@@ -817,7 +798,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       if (++rs == PRING) { rs = 0; rph ^= 1; }
       if (it.type == PT_END) break;
       const bool have_acc = it.num_kb > 0;
-      if (ADAMW && it.type == PT_DW && !(P.strict & 8192)) prefetch_dw_adamw(g, e, it);
       uint32_t acc = 0;
       if (have_acc) {
         acc = acc_it & 1;

@@ -297,13 +297,6 @@ __device__ __forceinline__ void umma_commit_mask(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
-// Bulk (non-tensor) prefetch of a contiguous global range into L2 (16-B aligned, size a
-// multiple of 16); fire-and-forget.
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
-               : "memory");
-}
-
 // TMA prefetch of a tensor box into L2 only (no shared memory, no barrier).
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
