@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="cce_config.flags (2 = per-chunk backward schedule)")
+    ap.add_argument("--combine", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: the sharded exchange through NCCL or over peer memory (CCE_FLAG_P2P_COMBINE)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -232,14 +234,21 @@ def main():
     y = torch.from_numpy(p["labels"]).to(dev)
 
     comm = None
-    if world > 1:
+    p2p = world > 1 and args.combine == "p2p"
+    if world > 1 and not p2p:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(cce.cce_nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         comm = cce.cce_nccl_comm_init(world, bytes(uid.cpu().numpy().tobytes()), rank)
-    h = cce.CCEHandle(vocab_total=c.V, vocab_offset=lo, rank=rank, world=world, nccl_comm=comm, flags=args.flags)
+    h = cce.CCEHandle(vocab_total=c.V, vocab_offset=lo, rank=rank, world=world, nccl_comm=comm,
+                      flags=args.flags | (cce.FLAG_P2P_COMBINE if p2p else 0))
     ws = h.workspace(c.N, c.D, hi - lo, dev)
+    if p2p:  # map every rank's workspace into every other rank (CUDA IPC), then a barrier
+        allh = [None] * world
+        dist.all_gather_object(allh, cce.cce_p2p_export(ws))
+        cce.cce_p2p_attach(h.h, ws, [a[0] for a in allh], [a[1] for a in allh])
+        dist.barrier()
     loss = torch.empty((), dtype=torch.float32, device=dev)
     lse = torch.empty(c.N, dtype=torch.float32, device=dev)
     nvt = torch.empty((), dtype=torch.int32, device=dev)
@@ -399,7 +408,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOAD_DESC[args.config], "N": c.N, "D": c.D, "V": c.V, "n_valid": n_valid,
-                       "seed": args.seed, "parallelism": f"vocab-sharded x{world}" if world > 1 else "single GPU",
+                       "seed": args.seed, "parallelism": (f"vocab-sharded x{world} ({args.combine} exchange)" if world > 1 else "single GPU"),
                        "l2": "256 MB L2 flush between timed steps" if not args.no_flush else "no flush"},
             "frac_of_peak_credited": frac_credited,
             "frac_of_sustained_peak_credited": frac_credited * pk["bf16_tflops"] / pk["bf16_tflops_sustained"],

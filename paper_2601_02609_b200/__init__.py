@@ -30,7 +30,7 @@ EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_byt
            "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info",
            "cce_profile_enable", "cce_profile_read", "cce_debug_trace", "cce_backward_adamw", "cce_adamw_step",
            "cce_forward_rmsnorm", "cce_backward_rmsnorm", "cce_combine_offsets", "cce_forward_finish",
-           "cce_backward_finish", "cce_step_host_async"]
+           "cce_backward_finish", "cce_step_host_async", "cce_p2p_export", "cce_p2p_attach"]
 PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 # "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
 # FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
@@ -43,6 +43,7 @@ FLAG_GRAD_FP32 = 64
 FLAG_ACCUMULATE = 128
 FLAG_EXTERNAL_COMBINE = 256
 FLAG_DH_SEQ_SHARD = 512
+FLAG_P2P_COMBINE = 1024
 REDUCTION_MEAN, REDUCTION_SUM, REDUCTION_NONE = 0, 1, 2
 _REDUCTIONS = {"mean": REDUCTION_MEAN, "sum": REDUCTION_SUM, "none": REDUCTION_NONE}
 
@@ -113,6 +114,10 @@ def lib():
         L.cce_host_staging_bytes.restype = sz
         L.cce_step_host.argtypes = [p, p, i64, i64, p, p, i64, i64, p, p, p, p, sz, p, sz, p]
         L.cce_step_host.restype = st
+        L.cce_p2p_export.argtypes = [p, p, p]
+        L.cce_p2p_export.restype = st
+        L.cce_p2p_attach.argtypes = [p, p, p, p]
+        L.cce_p2p_attach.restype = st
         L.cce_step_host_async.argtypes = [p, p, i64, i64, p, p, i64, i64, p, p, p, p, sz, p, sz, p, p]
         L.cce_step_host_async.restype = st
         L.cce_nccl_unique_id.argtypes = [p]
@@ -282,6 +287,21 @@ def cce_step_host_async(h, H_host, labels_host, W, dH, dW, staging, workspace, l
                                      workspace.numel() * workspace.element_size(), _stream(stream),
                                      None if copy_stream is None else ctypes.c_void_p(copy_stream.cuda_stream)),
            "cce_step_host_async")
+
+
+def cce_p2p_export(t):
+    """(64-byte CUDA IPC handle, byte offset) of the allocation holding tensor t."""
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _check(lib().cce_p2p_export(ctypes.c_void_p(t.data_ptr()), buf, ctypes.byref(off)), "cce_p2p_export")
+    return buf.raw, off.value
+
+
+def cce_p2p_attach(h, workspace, handles, offsets):
+    """handles / offsets: per rank (lists indexed by rank), from every rank's cce_p2p_export."""
+    blob = ctypes.create_string_buffer(b"".join(bytes(x) for x in handles), 64 * len(handles))
+    offs = (ctypes.c_int64 * len(offsets))(*offsets)
+    _check(lib().cce_p2p_attach(h, _ptr(workspace), blob, offs), "cce_p2p_attach")
 
 
 def cce_kernel_launches(h) -> int:

@@ -17,6 +17,7 @@
 #include "cce_aux.cuh"
 #include "cce_bwd.cuh"
 #include "cce_gemm.cuh"
+#include "cce_p2p.cuh"
 #include "cce_pair.cuh"
 #include "cce_quad.cuh"
 
@@ -52,6 +53,12 @@ struct cce_handle {
   struct Stage { const void* buf; cudaEvent_t consumed; };
   Stage stages[4] = {};
   cudaEvent_t ev_copied = nullptr;
+  // CCE_FLAG_P2P_COMBINE: peers' workspaces (CUDA IPC), the attached local workspace, step epoch
+  PeerPtrs peers = {};
+  void* opened[P2P_MAX] = {};
+  void* p2p_ws = nullptr;
+  bool p2p_attached = false;
+  int epoch = 0;
   const void* nX = nullptr;
   int64_t ldx = 0;
   const void* gamma = nullptr;
@@ -220,11 +227,13 @@ struct Layout {
   int64_t Npad, Tv, C;
   int64_t n_chunks, sched_ints;
   size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, dloss_c, gbuf,
-      dH32, sched, rstd_c, gpart, dHo, total;
+      dH32, sched, rstd_c, gpart, dHo, p2p_flags, dHred, total;
   int64_t seq_slice;  // CCE_FLAG_DH_SEQ_SHARD: rows per rank of the original-order dH (0 otherwise)
 };
 
-Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots, bool seq = false) {
+Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots, uint32_t flags = 0) {
+  const bool seq = (flags & CCE_FLAG_DH_SEQ_SHARD) != 0;
+  const bool p2p = (flags & CCE_FLAG_P2P_COMBINE) != 0;
   Layout L;
   L.Npad = align_up((size_t)(N > 0 ? N : 1), 256);  // pair tiles are 256 rows
   L.Tv = (V_local + BN - 1) / BN;
@@ -239,6 +248,15 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
     o = align_up(o + bytes, 256);
     return at;
   };
+  L.p2p_flags = L.dHred = 0;
+  if (p2p) {
+    // the regions peers read or write come first, at offsets that depend only on (N, D, world)
+    // (shard sizes V_local differ between ranks): flags, all-ranks stats, reduced dH, partial dH
+    L.p2p_flags = take(3 * P2P_MAX * 4);
+    L.stats_all = take((size_t)world * L.Npad * 16);
+    L.dHred = take((size_t)L.Npad * D * 4);
+    L.dH32 = take((size_t)L.Npad * D * 4);
+  }
   L.scal = take(64);
   L.pos = take((size_t)(N > 0 ? N : 1) * 4);
   L.idx = take((size_t)L.Npad * 4);
@@ -248,12 +266,12 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
   L.zs_part = take((size_t)L.Tv * L.Npad * 4);  // label smoothing only: per-tile logit sums
   L.zy_c = take((size_t)L.Npad * 4);
   L.stats = take((size_t)L.Npad * 16);
-  L.stats_all = take((size_t)world * L.Npad * 16);
+  if (!p2p) L.stats_all = take((size_t)world * L.Npad * 16);
   L.lse_c = take((size_t)L.Npad * 4);
   L.loss_rows = take((size_t)L.Npad * 4);
   L.dloss_c = take((size_t)L.Npad * 4);  // reduction "none": upstream gradients of the valid rows
   L.gbuf = take((size_t)slots * L.Npad * L.C * 2);  // ring of N x chunk dlogits (never N x V)
-  L.dH32 = take((size_t)L.Npad * D * 4);
+  if (!p2p) L.dH32 = take((size_t)L.Npad * D * 4);
   L.n_chunks = (V_local + L.C - 1) / L.C;
   // backward work queue: head | g_done[n] | w_done[n] | dh_flag[tiles_d * ceil(Npad/BN)]
   L.sched_ints = 2 + 2 * L.n_chunks + ((D + BM - 1) / BM) * ((L.Npad + BN - 1) / BN);
@@ -450,8 +468,11 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
     return CCE_ERR_INVALID_VALUE;
   // world > 1 needs a communicator; world == 1 may carry one (a 1-rank comm runs the
   // same NCCL collectives -- identities -- which lets one GPU exercise that path)
-  if (cfg->world > 1 && cfg->nccl_comm == nullptr && !(cfg->flags & CCE_FLAG_EXTERNAL_COMBINE))
+  if (cfg->world > 1 && cfg->nccl_comm == nullptr && !(cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_P2P_COMBINE)))
     return CCE_ERR_INVALID_VALUE;
+  if ((cfg->flags & CCE_FLAG_P2P_COMBINE) &&
+      (cfg->nccl_comm || (cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD)) || cfg->world > P2P_MAX))
+    return CCE_ERR_UNSUPPORTED;
   if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
   if (!(cfg->label_smoothing >= 0.f && cfg->label_smoothing < 1.f) || !(cfg->z_loss >= 0.f && cfg->z_loss < 1e30f))
     return CCE_ERR_INVALID_VALUE;
@@ -491,13 +512,15 @@ cce_status cce_destroy(cce_handle* h) {
   for (auto& e : h->stages)
     if (e.consumed) cudaEventDestroy(e.consumed);
   if (h->ev_copied) cudaEventDestroy(h->ev_copied);
+  for (auto p : h->opened)
+    if (p) cudaIpcCloseMemHandle(p);
   delete h;
   return CCE_OK;
 }
 
 size_t cce_workspace_bytes(const cce_handle* h, int64_t N, int64_t D, int64_t V_local) {
   if (!h || N < 0 || D <= 0 || V_local < 0) return 0;
-  return layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0).total;
+  return layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags).total;
 }
 
 int64_t cce_kernel_launches(const cce_handle* h) { return h ? h->launches : 0; }
@@ -586,8 +609,10 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   if (D % 64 != 0 || N > (1LL << 30) || V_local > (1LL << 30)) return CCE_ERR_UNSUPPORTED;
   if ((N > 0 && !aligned16(H)) || (V_local > 0 && !aligned16(W)) || (ldh * 2) % 16 || (ldw * 2) % 16)
     return CCE_ERR_UNSUPPORTED;
-  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   if (!workspace || workspace_bytes < L.total || !aligned16(workspace)) return CCE_ERR_WORKSPACE;
+  if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) && (!h->p2p_attached || workspace != h->p2p_ws))
+    return CCE_ERR_INVALID_VALUE;  // peers address this workspace: it must be the attached one
   if (!get_encode()) return CCE_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void* ws = workspace;
@@ -684,6 +709,20 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   h->ldw = ldw;
   h->ws = workspace;
   h->ws_bytes = workspace_bytes;
+  if (h->cfg.flags & CCE_FLAG_P2P_COMBINE) {
+    // a9 over peer memory: push this rank's stats into every rank's all-ranks array, raise
+    // the flag, wait for every rank's
+    const int epoch = ++h->epoch;
+    if (N > 0) {
+      ProfScope ps(h, s, 4);
+      k_p2p_push_stats<<<grid_for(L.Npad, 256, 2 * h->num_sms), 256, 0, s>>>(
+          stats, (int)L.Npad, nvp, h->peers, (unsigned long long)L.stats_all, h->cfg.rank, h->cfg.world);
+    }
+    k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_STATS, h->cfg.rank, h->cfg.world,
+                                  epoch);
+    k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_STATS, h->cfg.world, epoch, errp);
+    return forward_tail(h, at<float4>(ws, L.stats_all), loss, lse, n_valid, s);
+  }
   if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) {
     // a9 done by the caller: it gathers every rank's `stats` into `stats_all`, then calls
     // cce_forward_finish (cce_combine_offsets locates both in the workspace)
@@ -709,7 +748,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
 static cce_status forward_tail(cce_handle* h, const float4* stats_all, float* loss, float* lse, int32_t* n_valid,
                                cudaStream_t s) {
   const int64_t N = h->N;
-  const Layout L = layout(N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
+  const Layout L = layout(N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   void* ws = h->ws;
   int* nvp = at<int>(ws, L.scal);
   int* errp = nvp + 1;
@@ -737,14 +776,14 @@ cce_status cce_forward_finish(cce_handle* h, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   if (!h->fwd_pending) return CCE_ERR_NO_FORWARD;
   h->fwd_pending = false;
-  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   return forward_tail(h, at<float4>(h->ws, L.stats_all), h->p_loss, h->p_lse, h->p_nv,
                       static_cast<cudaStream_t>(stream));
 }
 
 cce_status cce_combine_offsets(const cce_handle* h, int64_t N, int64_t D, int64_t V_local, int64_t* out4) {
   if (!h || !out4 || N < 0 || D <= 0 || V_local < 0) return CCE_ERR_INVALID_VALUE;
-  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   out4[0] = (int64_t)L.stats;      // this rank's stats: float [Npad][4] (m, d, z_y, sum z)
   out4[1] = (int64_t)L.stats_all;  // all ranks' stats: float [world][Npad][4], rank-major
   // this rank's partial dH: float [Npad][D] compact valid rows, or with CCE_FLAG_DH_SEQ_SHARD
@@ -835,7 +874,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
   if ((dH && !aligned16(dH)) || (dW && !aligned16(dW))) return CCE_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t N = h->N, D = h->D, V_local = h->V_local;
-  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   void* ws = h->ws;
   int* nvp = at<int>(ws, L.scal);
   float* dH32 = at<float>(ws, L.dH32);
@@ -1003,6 +1042,24 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       h->p_dH = dH;
       return CCE_OK;
     }
+    if (h->cfg.flags & CCE_FLAG_P2P_COMBINE) {
+      // a10 over peer memory: all partials complete -> each rank sums its row slice over the
+      // ranks and stores it into every rank's reduced array -> all slices complete
+      const int epoch = h->epoch;
+      k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_READY, h->cfg.rank,
+                                    h->cfg.world, epoch);
+      k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_READY, h->cfg.world, epoch, nvp + 1);
+      {
+        ProfScope ps(h, s, 4);
+        k_p2p_reduce_dH<<<grid_for(L.Npad * D / 4 / h->cfg.world, 256, 4 * h->num_sms), 256, 0, s>>>(
+            h->peers, (unsigned long long)L.dH32, (unsigned long long)L.dHred, (int)D, nvp, h->cfg.rank,
+            h->cfg.world);
+      }
+      k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_DONE, h->cfg.rank, h->cfg.world,
+                                    epoch);
+      k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_DONE, h->cfg.world, epoch, nvp + 1);
+      dH32 = at<float>(ws, L.dHred);
+    }
     if (h->cfg.nccl_comm) {
       // a10: dH partials summed over the vocabulary shards (all-reduce), or reduce-scattered
       // by sequence slice (CCE_FLAG_DH_SEQ_SHARD; in place: rank r's slice at r x slice rows)
@@ -1058,7 +1115,7 @@ cce_status cce_backward_finish(cce_handle* h, void* stream) {
   if (!h->bwd_pending) return CCE_ERR_NO_FORWARD;
   h->bwd_pending = false;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   if (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) return seq_rows_out(h, L, h->p_dH, s);
   ProfScope ps(h, s, 4);
   k_scatter_dH<<<grid_for((long long)h->N * h->D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(
@@ -1067,18 +1124,67 @@ cce_status cce_backward_finish(cce_handle* h, void* stream) {
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
 
+typedef CUresult (*PFN_addrRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+cce_status cce_p2p_export(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return CCE_ERR_INVALID_VALUE;
+  static PFN_addrRange range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return CCE_ERR_CUDA;
+    range = reinterpret_cast<PFN_addrRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) return CCE_ERR_CUDA;
+  cudaIpcMemHandle_t mh;
+  if (cudaIpcGetMemHandle(&mh, reinterpret_cast<void*>(base)) != cudaSuccess) return CCE_ERR_CUDA;
+  std::memcpy(handle_out, &mh, sizeof(mh));
+  *offset_out = (int64_t)(reinterpret_cast<uintptr_t>(dev_ptr) - (uintptr_t)base);
+  return CCE_OK;
+}
+
+cce_status cce_p2p_attach(cce_handle* h, void* workspace, const void* handles, const int64_t* offsets) {
+  if (!h || !workspace || !handles || !offsets) return CCE_ERR_INVALID_VALUE;
+  if (!(h->cfg.flags & CCE_FLAG_P2P_COMBINE) || h->p2p_attached) return CCE_ERR_INVALID_VALUE;
+  if (!aligned16(workspace)) return CCE_ERR_UNSUPPORTED;
+  const int world = h->cfg.world, rank = h->cfg.rank;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      h->peers.ws[r] = static_cast<char*>(workspace);
+      continue;
+    }
+    cudaIpcMemHandle_t mh;
+    std::memcpy(&mh, static_cast<const char*>(handles) + (size_t)r * CCE_P2P_HANDLE_BYTES, sizeof(mh));
+    void* base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return CCE_ERR_CUDA;
+    h->opened[r] = base;
+    h->peers.ws[r] = static_cast<char*>(base) + offsets[r];
+  }
+  // this rank's flags start at 0 (every rank attaches before any rank's first step)
+  if (cudaMemset(workspace, 0, 3 * P2P_MAX * 4) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return CCE_ERR_CUDA;
+  h->p2p_ws = workspace;
+  h->p2p_attached = true;
+  h->epoch = 0;
+  return CCE_OK;
+}
+
 cce_status cce_get_error(cce_handle* h, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!h->ws) return CCE_OK;
-  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0);
+  const Layout L = layout(h->N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   int* errp = at<int>(h->ws, L.scal) + 1;
   int err = 0;
   if (cudaMemcpyAsync(&err, errp, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CCE_ERR_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return CCE_ERR_CUDA;
   if (err) {
     if (cudaMemsetAsync(errp, 0, 4, s) != cudaSuccess) return CCE_ERR_CUDA;
-    return CCE_ERR_LABEL_RANGE;
+    return (err & 4) ? CCE_ERR_NCCL : CCE_ERR_LABEL_RANGE;  // bit 2: a peer never signalled (P2P)
   }
   return CCE_OK;
 }
