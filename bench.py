@@ -215,10 +215,19 @@ def main():
         if world == 1 and args.gpus > 1:
             print(json.dumps({"error": "--gpus N > 1 must be launched with torchrun"}), flush=True)
             return 2
+    # CCE_BENCH_ONE_GPU=1 (testing the N > 1 plumbing on a one-GPU box): every rank on cuda:0,
+    # gloo for the host-side process group, --combine p2p for the exchange (NCCL refuses two
+    # ranks on one GPU).  The timings of such a run are time-sliced, not a scaling result.
+    one_gpu = os.environ.get("CCE_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     if rank == 0:
         cce_build.build()
     if world > 1:
