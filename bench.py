@@ -256,7 +256,7 @@ def main():
     if p2p:  # map every rank's workspace into every other rank (CUDA IPC), then a barrier
         allh = [None] * world
         dist.all_gather_object(allh, cce.cce_p2p_export(ws))
-        cce.cce_p2p_attach(h.h, ws, [a[0] for a in allh], [a[1] for a in allh])
+        cce.cce_p2p_attach(h.h, ws, c.N, c.D, [a[0] for a in allh], [a[1] for a in allh])
         dist.barrier()
     loss = torch.empty((), dtype=torch.float32, device=dev)
     lse = torch.empty(c.N, dtype=torch.float32, device=dev)

@@ -107,11 +107,12 @@ typedef enum {
  * all-reduce) instead of all-reduced.  World 1: the full dH.  Not with
  * cce_backward_rmsnorm (CCE_ERR_UNSUPPORTED). */
 #define CCE_FLAG_DH_SEQ_SHARD 512u
-/* The sharded exchange over peer memory instead of NCCL: the kernel
- * that merges this rank's per-row stats pushes them into every rank's all-ranks array
- * (stores over NVLink / to peer memory), and after the backward each rank sums its row
- * slice of the partial dH over all ranks (loads from peer memory, rank order) and stores
- * the sum into every rank's reduced array; release / acquire flags per step, waits bounded
+/* The sharded exchange over peer memory instead of NCCL: this rank's
+ * per-row stats are pushed into every rank's all-ranks array right after the merge (stores
+ * over NVLink / to peer memory), and inside the backward kernel, as soon as every rank's
+ * dH tile is final, the tile's owner sums it over the ranks (loads from peer memory, rank
+ * order) and stores the sum into every rank's reduced array, overlapping the remaining
+ * tensor-core work tile by tile; release / acquire flags per step, waits bounded
  * (a peer that never signals makes cce_get_error return CCE_ERR_NCCL and loss NaN instead
  * of hanging).  Needs cce_p2p_attach; world <= 8; not with a communicator,
  * CCE_FLAG_EXTERNAL_COMBINE or CCE_FLAG_DH_SEQ_SHARD.  One backward per forward. */
@@ -356,15 +357,17 @@ cce_status cce_step_host_async(cce_handle *h,
  * (CCE_P2P_HANDLE_BYTES bytes, written to host memory) of the allocation holding
  * `dev_ptr`, and dev_ptr's byte offset inside it.  Each rank exports its workspace, the
  * caller all-gathers (handle, offset) (e.g. torch.distributed), and every rank calls
- * cce_p2p_attach with the arrays indexed by rank (its own entry is ignored) and the
- * workspace it will pass to cce_forward; attach zeroes this rank's flags, so all ranks
+ * cce_p2p_attach with the arrays indexed by rank (its own entry is ignored), the
+ * workspace it will pass to cce_forward and the problem's N, D (later steps must use the
+ * same N, D: the flag arrays are laid out for them); attach zeroes this rank's flags, so all ranks
  * must attach before any rank's first step (a barrier).  The workspace must stay the same
  * buffer afterwards (cce_forward returns CCE_ERR_INVALID_VALUE otherwise); the mappings
  * are closed by cce_destroy.
  */
 #define CCE_P2P_HANDLE_BYTES 64
 cce_status cce_p2p_export(const void *dev_ptr, void *handle_out, int64_t *offset_out);
-cce_status cce_p2p_attach(cce_handle *h, void *workspace, const void *handles, const int64_t *offsets);
+cce_status cce_p2p_attach(cce_handle *h, void *workspace, int64_t N, int64_t D, const void *handles,
+                          const int64_t *offsets);
 
 /* NCCL plumbing for world > 1 (NCCL is resolved at run time with dlopen; the
  * library does not link it).  The 128-byte unique id is produced on rank 0 and

@@ -116,7 +116,7 @@ def lib():
         L.cce_step_host.restype = st
         L.cce_p2p_export.argtypes = [p, p, p]
         L.cce_p2p_export.restype = st
-        L.cce_p2p_attach.argtypes = [p, p, p, p]
+        L.cce_p2p_attach.argtypes = [p, p, i64, i64, p, p]
         L.cce_p2p_attach.restype = st
         L.cce_step_host_async.argtypes = [p, p, i64, i64, p, p, i64, i64, p, p, p, p, sz, p, sz, p, p]
         L.cce_step_host_async.restype = st
@@ -297,11 +297,12 @@ def cce_p2p_export(t):
     return buf.raw, off.value
 
 
-def cce_p2p_attach(h, workspace, handles, offsets):
-    """handles / offsets: per rank (lists indexed by rank), from every rank's cce_p2p_export."""
+def cce_p2p_attach(h, workspace, N: int, D: int, handles, offsets):
+    """handles / offsets: per rank (lists indexed by rank), from every rank's cce_p2p_export;
+    N, D: the problem size of the steps that follow."""
     blob = ctypes.create_string_buffer(b"".join(bytes(x) for x in handles), 64 * len(handles))
     offs = (ctypes.c_int64 * len(offsets))(*offsets)
-    _check(lib().cce_p2p_attach(h, _ptr(workspace), blob, offs), "cce_p2p_attach")
+    _check(lib().cce_p2p_attach(h, _ptr(workspace), N, D, blob, offs), "cce_p2p_attach")
 
 
 def cce_kernel_launches(h) -> int:

@@ -59,6 +59,7 @@ struct cce_handle {
   void* p2p_ws = nullptr;
   bool p2p_attached = false;
   int epoch = 0;
+  int64_t p2p_N = 0, p2p_D = 0;  // the problem size the P2P flag arrays were laid out for
   const void* nX = nullptr;
   int64_t ldx = 0;
   const void* gamma = nullptr;
@@ -227,7 +228,8 @@ struct Layout {
   int64_t Npad, Tv, C;
   int64_t n_chunks, sched_ints;
   size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, dloss_c, gbuf,
-      dH32, sched, rstd_c, gpart, dHo, p2p_flags, dHred, total;
+      dH32, sched, rstd_c, gpart, dHo, p2p_flags, p2p_ready, p2p_done, dHred, total;
+  int64_t p2p_tmax;  // dH tiles the P2P flag arrays hold: ceil(D/256) x Npad/256
   int64_t seq_slice;  // CCE_FLAG_DH_SEQ_SHARD: rows per rank of the original-order dH (0 otherwise)
 };
 
@@ -248,11 +250,14 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
     o = align_up(o + bytes, 256);
     return at;
   };
-  L.p2p_flags = L.dHred = 0;
+  L.p2p_flags = L.p2p_ready = L.p2p_done = L.dHred = 0;
+  L.p2p_tmax = ((D + 255) / 256) * (L.Npad / 256);
   if (p2p) {
     // the regions peers read or write come first, at offsets that depend only on (N, D, world)
     // (shard sizes V_local differ between ranks): flags, all-ranks stats, reduced dH, partial dH
     L.p2p_flags = take(3 * P2P_MAX * 4);
+    L.p2p_ready = take((size_t)P2P_MAX * L.p2p_tmax * 4);  // ready[rank][tile]
+    L.p2p_done = take((size_t)2 * L.p2p_tmax * 4);         // done[tile][cta of the pair]
     L.stats_all = take((size_t)world * L.Npad * 16);
     L.dHred = take((size_t)L.Npad * D * 4);
     L.dH32 = take((size_t)L.Npad * D * 4);
@@ -320,10 +325,10 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
                        const pairk::PairParams& pp, cudaStream_t s, int prof_class) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(pairk::cce_pair_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pairk::PSMEM) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(pairk::cce_pair_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pairk::PSMEM) !=
-            cudaSuccess)
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if (cudaFuncSetAttribute(pairk::cce_pair_kernel<0, 0>, a, pairk::PSMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(pairk::cce_pair_kernel<1, 0>, a, pairk::PSMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(pairk::cce_pair_kernel<0, 1>, a, pairk::PSMEM) != cudaSuccess)
       return CCE_ERR_CUDA;
     attr = true;
   }
@@ -331,9 +336,11 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
   {
     ProfScope ps(h, s, prof_class);
     if (pp.g.adamw)
-      pairk::cce_pair_kernel<1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
+      pairk::cce_pair_kernel<1, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
+    else if (pp.world > 1)
+      pairk::cce_pair_kernel<0, 1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
     else
-      pairk::cce_pair_kernel<0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
+      pairk::cce_pair_kernel<0, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
@@ -471,7 +478,9 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
   if (cfg->world > 1 && cfg->nccl_comm == nullptr && !(cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_P2P_COMBINE)))
     return CCE_ERR_INVALID_VALUE;
   if ((cfg->flags & CCE_FLAG_P2P_COMBINE) &&
-      (cfg->nccl_comm || (cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD)) || cfg->world > P2P_MAX))
+      (cfg->nccl_comm || cfg->world > P2P_MAX ||
+       (cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD | CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY |
+                      CCE_FLAG_ONE_CTA))))
     return CCE_ERR_UNSUPPORTED;
   if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
   if (!(cfg->label_smoothing >= 0.f && cfg->label_smoothing < 1.f) || !(cfg->z_loss >= 0.f && cfg->z_loss < 1e30f))
@@ -611,8 +620,9 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     return CCE_ERR_UNSUPPORTED;
   const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   if (!workspace || workspace_bytes < L.total || !aligned16(workspace)) return CCE_ERR_WORKSPACE;
-  if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) && (!h->p2p_attached || workspace != h->p2p_ws))
-    return CCE_ERR_INVALID_VALUE;  // peers address this workspace: it must be the attached one
+  if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) &&
+      (!h->p2p_attached || workspace != h->p2p_ws || N != h->p2p_N || D != h->p2p_D))
+    return CCE_ERR_INVALID_VALUE;  // peers address this workspace (layout of the attached N, D)
   if (!get_encode()) return CCE_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void* ws = workspace;
@@ -839,7 +849,7 @@ cce_status cce_backward_adamw(cce_handle* h, const float* dloss, void* dH, const
   if (!h) return CCE_ERR_INVALID_VALUE;
   if (!h->have_fwd) return CCE_ERR_NO_FORWARD;
   if (!adamw_params_ok(opt)) return CCE_ERR_INVALID_VALUE;
-  if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) return CCE_ERR_UNSUPPORTED;
+  if (h->cfg.flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_P2P_COMBINE)) return CCE_ERR_UNSUPPORTED;
   if (h->cfg.flags & (CCE_FLAG_ONE_CTA | CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY | CCE_FLAG_ACCUMULATE))
     return CCE_ERR_UNSUPPORTED;
   if (!adamw_aligned(opt) || (h->D % 8) != 0 || (opt->W_out && !aligned16(opt->W_out))) return CCE_ERR_UNSUPPORTED;
@@ -956,6 +966,18 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       pp.sched = at<int>(ws, L.sched);
       pp.trace = static_cast<TraceRec*>(h->trace);
       pp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
+      if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) && h->cfg.world > 1) {
+        pp.peers = h->peers;
+        pp.world = h->cfg.world;
+        pp.prank = h->cfg.rank;
+        pp.epoch = h->epoch;
+        pp.tmax = (int)L.p2p_tmax;
+        pp.ready_off = L.p2p_ready;
+        pp.done_off = L.p2p_done;
+        pp.dH32_off = L.dH32;
+        pp.dHred_off = L.dHred;
+        pp.err = nvp + 1;
+      }
       CUtensorMap mDH;
       if (!make_map_f32(&mDH, dH32, D, L.Npad, D, 32, 32)) return CCE_ERR_CUDA;
       cce_status st = quad ? launch_quad(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1)
@@ -1042,22 +1064,10 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       h->p_dH = dH;
       return CCE_OK;
     }
-    if (h->cfg.flags & CCE_FLAG_P2P_COMBINE) {
-      // a10 over peer memory: all partials complete -> each rank sums its row slice over the
-      // ranks and stores it into every rank's reduced array -> all slices complete
-      const int epoch = h->epoch;
-      k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_READY, h->cfg.rank,
-                                    h->cfg.world, epoch);
-      k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_READY, h->cfg.world, epoch, nvp + 1);
-      {
-        ProfScope ps(h, s, 4);
-        k_p2p_reduce_dH<<<grid_for(L.Npad * D / 4 / h->cfg.world, 256, 4 * h->num_sms), 256, 0, s>>>(
-            h->peers, (unsigned long long)L.dH32, (unsigned long long)L.dHred, (int)D, nvp, h->cfg.rank,
-            h->cfg.world);
-      }
-      k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_DONE, h->cfg.rank, h->cfg.world,
-                                    epoch);
-      k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_DONE, h->cfg.world, epoch, nvp + 1);
+    if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) && h->cfg.world > 1) {
+      // a10 over peer memory, fused into the backward kernel (RED items, tile by tile): here
+      // only wait until every tile's reduced dH has arrived in this rank's reduced array
+      k_p2p_wait_tiles<<<1, 256, 0, s>>>(at<int>(ws, L.p2p_done), nvp, (int)D, h->epoch, nvp + 1);
       dH32 = at<float>(ws, L.dHred);
     }
     if (h->cfg.nccl_comm) {
@@ -1147,8 +1157,9 @@ cce_status cce_p2p_export(const void* dev_ptr, void* handle_out, int64_t* offset
   return CCE_OK;
 }
 
-cce_status cce_p2p_attach(cce_handle* h, void* workspace, const void* handles, const int64_t* offsets) {
-  if (!h || !workspace || !handles || !offsets) return CCE_ERR_INVALID_VALUE;
+cce_status cce_p2p_attach(cce_handle* h, void* workspace, int64_t N, int64_t D, const void* handles,
+                          const int64_t* offsets) {
+  if (!h || !workspace || !handles || !offsets || N < 0 || D <= 0) return CCE_ERR_INVALID_VALUE;
   if (!(h->cfg.flags & CCE_FLAG_P2P_COMBINE) || h->p2p_attached) return CCE_ERR_INVALID_VALUE;
   if (!aligned16(workspace)) return CCE_ERR_UNSUPPORTED;
   const int world = h->cfg.world, rank = h->cfg.rank;
@@ -1165,8 +1176,11 @@ cce_status cce_p2p_attach(cce_handle* h, void* workspace, const void* handles, c
     h->peers.ws[r] = static_cast<char*>(base) + offsets[r];
   }
   // this rank's flags start at 0 (every rank attaches before any rank's first step)
-  if (cudaMemset(workspace, 0, 3 * P2P_MAX * 4) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+  const Layout L = layout(N, D, 0, world, h->chunk, h->slots, h->cfg.flags);
+  if (cudaMemset(workspace, 0, L.stats_all) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
     return CCE_ERR_CUDA;
+  h->p2p_N = N;
+  h->p2p_D = D;
   h->p2p_ws = workspace;
   h->p2p_attached = true;
   h->epoch = 0;

@@ -4,9 +4,11 @@
 //   a9  the merged per-row stats are PUSHED into each rank's all-ranks array by the
 //       kernel that produced them (k_p2p_push_stats, stores over NVLink), then a release
 //       flag per (kind, source rank) is raised in every peer and waited for;
-//   a10 each rank sums ITS row slice of the partial dH over all ranks in rank order (loads
-//       over NVLink, deterministic) and stores the sum into every rank's reduced-dH array
-//       (a reduce-scatter and an all-gather fused into one kernel).
+//   a10 inside the backward kernel (cce_pair.cuh, RED items): as soon as every rank's
+//       last-chunk dH tile is final, the tile's owner (tile % world) sums it over the ranks
+//       in rank order (loads over NVLink, deterministic) and stores the sum into every
+//       rank's reduced-dH array (a reduce-scatter and an all-gather fused, overlapping the
+//       remaining MMA items tile by tile); k_p2p_wait_tiles gates the scatter on it.
 // Flags are epoch counters (one step = one epoch) in each rank's workspace; waits are
 // bounded (a missing peer sets the error word instead of hanging the GPU).
 #pragma once
@@ -16,7 +18,7 @@
 namespace cce {
 
 constexpr int P2P_MAX = 8;                // ranks
-constexpr int P2P_STATS = 0, P2P_READY = 1, P2P_DONE = 2;  // flag kinds
+constexpr int P2P_STATS = 0;  // flag kind: per-row stats pushed (the other kinds are per tile)
 constexpr unsigned long long P2P_TIMEOUT_NS = 5000000000ull;
 
 struct PeerPtrs {
@@ -74,26 +76,22 @@ __global__ void k_p2p_wait(const int* __restrict__ flags, int kind, int world, i
   }
 }
 
-// a10: rows [rank S, (rank + 1) S) of the compact dH (S = ceil(n_valid / world)): the sum of
-// all ranks' partials in rank order, stored into every rank's reduced array.
-__global__ void k_p2p_reduce_dH(PeerPtrs peers, unsigned long long dH32_off, unsigned long long dHred_off, int D,
-                                const int* __restrict__ n_valid, int rank, int world) {
-  const int nv = *n_valid;
-  const int S = (nv + world - 1) / world;
-  const int r0 = rank * S, r1 = min(nv, r0 + S);
-  if (r1 <= r0) return;
-  const int vec = D / 4;
-  const long long total = (long long)(r1 - r0) * vec;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long e = (long long)r0 * vec + i;  // float4 index into [Npad][D]
-    float4 acc = reinterpret_cast<const float4*>(peers.ws[0] + dH32_off)[e];
-    for (int q = 1; q < world; ++q) {
-      const float4 v = reinterpret_cast<const float4*>(peers.ws[q] + dH32_off)[e];
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+// Wait until every tile's RED item raised done[tile][cta] for this epoch (tiles from the
+// device-side n_valid); bounded like k_p2p_wait.
+__global__ void k_p2p_wait_tiles(const int* __restrict__ done, const int* __restrict__ n_valid, int D, int epoch,
+                                 int* err) {
+  const int t256 = (*n_valid + 255) / 256, n_dt = (D + 255) / 256;
+  const int n = 2 * t256 * n_dt;
+  const unsigned long long t0 = p2p_now();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    while (ld_acquire_sys(done + i) < epoch) {
+      if (p2p_now() - t0 > P2P_TIMEOUT_NS) {
+        atomicOr(err, 4);
+        return;
+      }
+      __nanosleep(1000);
     }
-    for (int q = 0; q < world; ++q) reinterpret_cast<float4*>(peers.ws[q] + dHred_off)[e] = acc;
   }
-  __threadfence_system();
 }
 
 }  // namespace cce

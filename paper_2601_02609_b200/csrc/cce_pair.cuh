@@ -36,6 +36,7 @@
 #pragma once
 #include "cce_bwd.cuh"
 #include "cce_gemm.cuh"
+#include "cce_p2p.cuh"
 
 namespace cce {
 namespace pairk {
@@ -55,7 +56,8 @@ constexpr int PSMEM = PSTAGES * PSTAGE_BYTES + 1024 /*align*/ + 1024 /*barriers+
                       PEPI_WARPS * 4096 /*epilogue store staging*/;
 static_assert(PSMEM <= 232448, "pair kernel shared memory");
 
-enum PType : int { PT_FWD = 0, PT_G = 1, PT_DW = 2, PT_DH = 3, PT_END = 4 };
+// PT_RED (P2P backward): the cross-rank sum of one dH tile, queued after every MMA item
+enum PType : int { PT_FWD = 0, PT_G = 1, PT_DW = 2, PT_DH = 3, PT_END = 4, PT_RED = 5 };
 
 struct PItem {
   int type, c, m0, n0, N, num_kb, tile_id, q;
@@ -73,6 +75,17 @@ struct PairParams {
   int prefetch;    // k-blocks of L2 prefetch (TMA prefetch.tensor) beyond the SMEM ring
   int strict;      // debug bit 0: serialise every item behind all earlier ones;
                    // debug bit 1: skip operand loads (measures raw MMA throughput; garbage results)
+  // CCE_FLAG_P2P_COMBINE, fused into this kernel (P2P instantiation): when rank r's last-chunk
+  // DH(tile) is complete it raises ready[r][tile] in every rank; RED(tile) items (tiles
+  // tile % world == rank, queued last) wait for every rank's ready flag, sum the tile's partial
+  // dH over the ranks in rank order (loads from peer memory), store the sum into every rank's
+  // reduced array and raise done[tile][cta] in every rank -- the exchange overlaps the
+  // remaining MMA items tile by tile.
+  PeerPtrs peers;
+  int world, prank, epoch, tmax;             // tmax: tile capacity of the flag arrays
+  unsigned long long ready_off, done_off;    // int flag arrays in every workspace
+  unsigned long long dH32_off, dHred_off;    // partial / reduced dH in every workspace
+  int* err;                                  // error word (bit 2: a peer never signalled)
   int* sched;      // zeroed: [0] head [1] done | g_done[n] | w_done[n] | dh_flag[n_dt * t256]
   TraceRec* trace;
   int trace_cap;
@@ -143,6 +156,14 @@ __device__ PItem decode(const PairParams& P, const PCounts& k, int q) {
         return make_item(PT_DW, c, (r / k.n_dt) * PM, dt * PN, dtile_N(g.D, dt), (k.nv + BK - 1) / BK, 0, q);
       }
       r -= cnt;
+    }
+  }
+  // P2P: this rank's share of the cross-rank dH reduction, after every MMA item
+  if (P.world > 1 && P.peers.ws[0] != nullptr) {
+    const int tile = P.prank + r * P.world;
+    if (tile < k.n_dh) {
+      const int dt = tile % k.n_dt;
+      return make_item(PT_RED, n - 1, (tile / k.n_dt) * PM, dt * PN, dtile_N(g.D, dt), 0, tile, q);
     }
   }
   return make_item(PT_END, 0, 0, 0, 0, 0, 0, q);
@@ -436,6 +457,46 @@ __device__ __forceinline__ void epi_dw_adamw(const GemmParams& p, uint32_t taddr
   __syncwarp();
 }
 
+// RED(tile): rows of this CTA's half of the tile, warp = 32 rows x its column half; lane =
+// four consecutive columns (512-byte runs per row).  Sum over ranks in rank order (the
+// same order on every rank: identical reduced dH everywhere), broadcast to every rank.
+__device__ __forceinline__ void epi_reduce(const PairParams& P, const PEpi& e, const PItem& it, int nv, bool leader) {
+  const GemmParams& g = P.g;
+  if (leader) {
+    const int* rf = reinterpret_cast<const int*>(P.peers.ws[P.prank] + P.ready_off);
+    const unsigned long long t0 = p2p_now();
+    for (int q = 0; q < P.world; ++q) {
+      while (ld_acquire_sys(rf + q * P.tmax + it.tile_id) < P.epoch) {
+        if (p2p_now() - t0 > P2P_TIMEOUT_NS) { atomicOr(P.err, 4); break; }
+        __nanosleep(500);
+      }
+    }
+  }
+  named_bar_sync(2, PEPI_THREADS);
+  const int hw = it.N / 2;
+  const int lane = e.rit & 31;
+  const int row0 = it.m0 + e.rank * HM + e.q * 32;
+  const int col = it.n0 + e.half * hw + lane * 4;
+  if (lane * 4 < hw && col < g.D) {
+    for (int rr = 0; rr < 32; ++rr) {
+      const int row = row0 + rr;
+      if (row >= nv) break;
+      const size_t idx = (size_t)row * g.D + col;
+      float4 acc = *reinterpret_cast<const float4*>(P.peers.ws[0] + P.dH32_off + idx * 4);
+      for (int qr = 1; qr < P.world; ++qr) {
+        const float4 v = *reinterpret_cast<const float4*>(P.peers.ws[qr] + P.dH32_off + idx * 4);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      for (int qr = 0; qr < P.world; ++qr) *reinterpret_cast<float4*>(P.peers.ws[qr] + P.dHred_off + idx * 4) = acc;
+    }
+  }
+  __threadfence_system();
+  named_bar_sync(2, PEPI_THREADS);
+  if (leader)
+    for (int qr = 0; qr < P.world; ++qr)
+      st_release_sys(reinterpret_cast<int*>(P.peers.ws[qr] + P.done_off) + 2 * it.tile_id + e.rank, P.epoch);
+}
+
 __device__ __forceinline__ void epi_dh(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv) {
   const int t = it.m0 + e.rank * HM + e.rit;  // compact row
   const int hw = it.N / 2;
@@ -537,7 +598,7 @@ __device__ __forceinline__ void mma_item(const PItem& it, uint64_t* full_bar, ui
 // ------------------------------------------------------------------ kernel
 // ADAMW = 1: the backward queue with AdamW fused into the dW epilogue (cce_backward_adamw);
 // a separate instantiation so its epilogue's register demand leaves the default kernel alone.
-template <int ADAMW>
+template <int ADAMW, int P2P>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     cce_pair_kernel(const __grid_constant__ CUtensorMap tmHcK, const __grid_constant__ CUtensorMap tmWK,
                     const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
@@ -819,6 +880,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         if constexpr (!ADAMW) epi_fwd(g, taddr, e, it, k.nv);
       } else if (it.type == PT_G) {
         if (!(P.strict & 32)) epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
+      } else if (it.type == PT_RED) {
+        if constexpr (P2P) epi_reduce(P, e, it, k.nv, leader);
       } else if (it.type == PT_DW) {
         if constexpr (ADAMW) {
           // the chunk's dH tiles read W_c through the TMA: the update waits until every
@@ -874,8 +937,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
             r.pad = it.num_kb;
           }
           if (it.type == PT_G) atomicAdd(&g_done[it.c], 1);
-          else {
-            if (it.type == PT_DH) atomicAdd(&dh_flag[it.tile_id], 1);
+          else if (it.type != PT_RED) {
+            if (it.type == PT_DH) {
+              const int old = atomicAdd(&dh_flag[it.tile_id], 1);
+              if constexpr (P2P) {
+                // the second half of the last chunk's tile: its partial dH is final here ->
+                // ready[prank][tile] in every rank (after a system-scope fence)
+                if (it.c == P.n_chunks - 1 && old == 2 * P.n_chunks - 1) {
+                  __threadfence_system();
+                  for (int qr = 0; qr < P.world; ++qr)
+                    st_release_sys(reinterpret_cast<int*>(P.peers.ws[qr] + P.ready_off) + P.prank * P.tmax + it.tile_id,
+                                   P.epoch);
+                }
+              }
+            }
             atomicAdd(&w_done[it.c], 1);
           }
           atomicAdd(done_total, 1);

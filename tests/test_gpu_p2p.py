@@ -40,7 +40,7 @@ ws = h.workspace(N, D, hi - lo, dev)
 mine = cce.cce_p2p_export(ws)
 allh = [None] * world
 dist.all_gather_object(allh, mine)
-cce.cce_p2p_attach(h.h, ws, [a[0] for a in allh], [a[1] for a in allh])
+cce.cce_p2p_attach(h.h, ws, N, D, [a[0] for a in allh], [a[1] for a in allh])
 dist.barrier()
 one = torch.ones((), dtype=torch.float32, device=dev)
 for step in range(0 if rank == absent else 2):
