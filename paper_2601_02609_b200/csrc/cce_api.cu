@@ -703,9 +703,15 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   if (N > 0) {
     // an empty shard (V_local == 0) merges zero tiles: (m=-inf, d=0, z_y=0) for every row
     ProfScope ps(h, s, 4);
+    StatsPush push{};
+    if (h->cfg.flags & CCE_FLAG_P2P_COMBINE) {  // a9 fused: every rank's slot `rank`, including ours
+      for (int r = 0; r < h->cfg.world; ++r)
+        push.dst[r] = reinterpret_cast<float4*>(h->peers.ws[r] + L.stats_all) + (size_t)h->cfg.rank * L.Npad;
+      push.n = h->cfg.world;
+    }
     k_merge_tiles<<<(unsigned)((L.Npad + 31) / 32), 32 * MERGE_SL, 0, s>>>(
         at<float2>(ws, L.part), V_local > 0 ? (int)L.Tv : 0, (int)L.Npad, at<float>(ws, L.zy_c), nvp,
-        (h->cfg.label_smoothing > 0.f && V_local > 0) ? at<float>(ws, L.zs_part) : nullptr, stats);
+        (h->cfg.label_smoothing > 0.f && V_local > 0) ? at<float>(ws, L.zs_part) : nullptr, stats, push);
   }
   h->have_fwd = false;
   h->norm = norm != nullptr;
@@ -722,12 +728,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   if (h->cfg.flags & CCE_FLAG_P2P_COMBINE) {
     // a9 over peer memory: push this rank's stats into every rank's all-ranks array, raise
     // the flag, wait for every rank's
-    const int epoch = ++h->epoch;
-    if (N > 0) {
-      ProfScope ps(h, s, 4);
-      k_p2p_push_stats<<<grid_for(L.Npad, 256, 2 * h->num_sms), 256, 0, s>>>(
-          stats, (int)L.Npad, nvp, h->peers, (unsigned long long)L.stats_all, h->cfg.rank, h->cfg.world);
-    }
+    const int epoch = ++h->epoch;  // (the merge above already stored the stats into every rank)
     k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_STATS, h->cfg.rank, h->cfg.world,
                                   epoch);
     k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_STATS, h->cfg.world, epoch, errp);

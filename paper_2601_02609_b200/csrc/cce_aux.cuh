@@ -103,6 +103,13 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ H, long long ldh
   }
 }
 
+// CCE_FLAG_P2P_COMBINE: the merged stats also go straight into every rank's all-ranks array
+// (slot of this rank, peer memory), so the exchange needs no separate kernel (a9 fused).
+struct StatsPush {
+  float4* dst[8];  // every rank's stats_all + rank * Npad (peer memory), or unused
+  int n;           // number of destinations (0: no push)
+};
+
 constexpr int MERGE_SL = 16;  // tile slices per merge block (512 threads: two blocks per SM, one wave)
 // a4 (local part): merge the per-vocabulary-tile (m, d) partials of each valid
 // row with the online-softmax merge:
@@ -114,7 +121,8 @@ constexpr int MERGE_SL = 16;  // tile slices per merge block (512 threads: two b
 // the same fixed order into the 4th stat (sum_v z_v of the row over this shard).
 __global__ void __launch_bounds__(32 * MERGE_SL) k_merge_tiles(const float2* __restrict__ part, int Tv, int Npad,
                                                       const float* __restrict__ zy_c, const int* __restrict__ n_valid,
-                                                      const float* __restrict__ zs_part, float4* __restrict__ stats) {
+                                                      const float* __restrict__ zs_part, float4* __restrict__ stats,
+                                                      const StatsPush push) {
   __shared__ float2 red[MERGE_SL][33];
   __shared__ float redz[MERGE_SL][33];
   const int nv = *n_valid;
@@ -173,8 +181,11 @@ __global__ void __launch_bounds__(32 * MERGE_SL) k_merge_tiles(const float2* __r
       }
       Z += redz[k][lane];
     }
-    stats[i] = make_float4(M, S, zy_c[i], Z);
+    const float4 st = make_float4(M, S, zy_c[i], Z);
+    stats[i] = st;
+    for (int k = 0; k < push.n; ++k) push.dst[k][i] = st;
   }
+  if (push.n) __threadfence_system();  // the peer stores are visible before the flag (next kernel)
 }
 
 

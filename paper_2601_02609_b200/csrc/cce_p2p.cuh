@@ -2,7 +2,7 @@
 // (CCE_FLAG_P2P_COMBINE): every rank's workspace is mapped into
 // every other rank (CUDA IPC), and
 //   a9  the merged per-row stats are PUSHED into each rank's all-ranks array by the
-//       kernel that produced them (k_p2p_push_stats, stores over NVLink), then a release
+//       kernel that produced them (k_merge_tiles, stores over NVLink), then a release
 //       flag per (kind, source rank) is raised in every peer and waited for;
 //   a10 inside the backward kernel (cce_pair.cuh, RED items): as soon as every rank's
 //       last-chunk dH tile is final, the tile's owner (tile % world) sums it over the ranks
@@ -37,18 +37,6 @@ __device__ __forceinline__ unsigned long long p2p_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-
-// This rank's stats rows -> slot `rank` of every rank's all-ranks array (rank-major [world][Npad]).
-__global__ void k_p2p_push_stats(const float4* __restrict__ stats, int Npad, const int* __restrict__ n_valid,
-                                 PeerPtrs peers, unsigned long long stats_all_off, int rank, int world) {
-  const int nv = *n_valid;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
-    const float4 v = stats[i];
-    for (int r = 0; r < world; ++r)
-      reinterpret_cast<float4*>(peers.ws[r] + stats_all_off)[(size_t)rank * Npad + i] = v;
-  }
-  __threadfence_system();
 }
 
 // Raise flag (kind, rank) = epoch in every rank (one thread; the kernel before it on the
