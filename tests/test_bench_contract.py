@@ -1,0 +1,37 @@
+"""bench.py's JSON-line contract, checked on CPU through the reference arm (the oracle on the
+host cores, the one leg that runs without a GPU): one line, the required keys, the reference
+arm's extra fields.  The GPU arm's line is produced on the B200 (profiles/r01_bench.json)."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "tiny",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["steps"] == 1 and d["warmup"] == 3
+    assert d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_committed_gpu_bench_line_has_the_contract_keys():
+    """The committed B200 line (profiles/r01_bench.json): roofline, cpu_baseline, e2e, clocks,
+    launch count and memory report present and consistent."""
+    path = os.path.join(ROOT, "profiles", "r01_bench.json")
+    d = json.loads(open(path).read().strip().splitlines()[-1])
+    for k in ("roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches", "memory"):
+        assert k in d, k
+    r = d["roofline"]
+    assert r["bound"] == "tensor" and 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["gpu_launches"] > 0 and d["memory"]["no_NxV_buffer"] is True
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
