@@ -176,6 +176,38 @@ static bool make_map_blocked(CUtensorMap* m, const void* base, uint64_t rows, ui
   return r == CUDA_SUCCESS;
 }
 
+// 3-D bf16 view of a row-major matrix [rows][cols] (row stride `ld` elements) as 64-column
+// blocks: dims {64, rows, cols / 64}, strides {ld * 2 bytes, 128 bytes}; box {64, box_rows,
+// box_blocks}.  One TMA instruction then fetches box_blocks MN-major 64-column boxes that
+// land in shared memory exactly as box_blocks separate 2-D boxes would (8 KB apart).
+static bool make_map_colblocks(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                               uint32_t box_rows, uint32_t box_blocks) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {64, rows, cols / 64};
+  cuuint64_t strides[2] = {ld * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, box_blocks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static bool make_map_blocked2(CUtensorMap* m, const void* base, uint64_t rows, uint64_t blocks, uint32_t box_rows,
+                              uint32_t box_blocks) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {64, rows, blocks};
+  cuuint64_t strides[2] = {128, rows * 128};
+  cuuint32_t box[3] = {64, box_rows, box_blocks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // ------------------------------------------------------------------ NCCL (dlopen)
 namespace {
 struct NcclId {
@@ -322,7 +354,10 @@ cce_status launch_gemm(cce_handle* h, const CUtensorMap& a, const CUtensorMap& b
 }
 cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                        const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5, const CUtensorMap& m6,
-                       const pairk::PairParams& pp, cudaStream_t s, int prof_class) {
+                       const pairk::PairParams& pp, cudaStream_t s, int prof_class, const CUtensorMap* m7 = nullptr,
+                       const CUtensorMap* m8 = nullptr) {
+  const CUtensorMap& x7 = m7 ? *m7 : m3;
+  const CUtensorMap& x8 = m8 ? *m8 : m5;
   static bool attr = false;
   if (!attr) {
     const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
@@ -336,11 +371,11 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
   {
     ProfScope ps(h, s, prof_class);
     if (pp.g.adamw)
-      pairk::cce_pair_kernel<1, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
+      pairk::cce_pair_kernel<1, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, pp);
     else if (pp.world > 1)
-      pairk::cce_pair_kernel<0, 1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
+      pairk::cce_pair_kernel<0, 1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, pp);
     else
-      pairk::cce_pair_kernel<0, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, pp);
+      pairk::cce_pair_kernel<0, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, pp);
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
@@ -938,9 +973,19 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       // backward: G / DW / DH tiles of every chunk from one work queue
       const bool quad = (h->cfg.flags & (CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY)) != 0;
       CUtensorMap mHcK, mWK, mGMN, mHcMN, mGK, mWMN;
+      // CCE_TMA3D (default 1, pair kernel): one TMA instruction per operand per k-block --
+      // the dW item's G^T and Hc boxes and the dH item's W_c boxes come as 3-D boxes of two
+      // 64-column blocks (4 -> 2 and 3 -> 2 instructions per k-block)
+      const char* et = getenv("CCE_TMA3D");
+      const bool t3 = !quad && (!et || atoi(et) != 0);
+      CUtensorMap mHcMN3, mWMN3;
+      if (t3 && (!make_map_colblocks(&mHcMN3, Hc, D, L.Npad, D, 64, 2) ||
+                 !make_map_colblocks(&mWMN3, h->W, D, V_local, h->ldw, 64, 2)))
+        return CCE_ERR_CUDA;
       if (!make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM) ||
           !make_map(&mWK, h->W, D, V_local, h->ldw, quad ? 64 : pairk::PN / 2) ||
-          !make_map_blocked(&mGMN, G, L.Npad, h->slots * (L.C / 64), 64) ||
+          (t3 ? !make_map_blocked2(&mGMN, G, L.Npad, h->slots * (L.C / 64), 64, 2)
+              : !make_map_blocked(&mGMN, G, L.Npad, h->slots * (L.C / 64), 64)) ||
           !make_map(&mHcMN, Hc, D, L.Npad, D, 64) ||
           !make_map_blocked(&mGK, G, L.Npad, h->slots * (L.C / 64), quad ? 64 : pairk::HM) ||
           !make_map(&mWMN, h->W, D, V_local, h->ldw, 64))
@@ -963,6 +1008,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       if (pp.lookahead < 0) pp.lookahead = 0;
       while (pp.lookahead > 0 && (pp.lookahead + 1) * pp.qblock > slots) --pp.lookahead;
       pp.prefetch = 0;  // L2 prefetch measured harmful (adds L2 requests); env CCE_PREFETCH to experiment
+      pp.tma3d = t3 ? 1 : 0;
       if (const char* e = getenv("CCE_PREFETCH")) pp.prefetch = atoi(e);
       pp.sched = at<int>(ws, L.sched);
       pp.trace = static_cast<TraceRec*>(h->trace);
@@ -982,7 +1028,8 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       CUtensorMap mDH;
       if (!make_map_f32(&mDH, dH32, D, L.Npad, D, 32, 32)) return CCE_ERR_CUDA;
       cce_status st = quad ? launch_quad(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1)
-                           : launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1);
+                           : launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, t3 ? &mHcMN3 : nullptr,
+                                         t3 ? &mWMN3 : nullptr);
       if (st != CCE_OK) return st;
     } else {
     CUtensorMap mHcK, mWK, mHcMN, mGMN, mWMN, mGK;

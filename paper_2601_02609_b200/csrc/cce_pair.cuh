@@ -73,6 +73,7 @@ struct PairParams {
   int lookahead;   // backward queue: G of chunk block b + lookahead is queued before W of block b
   int qblock;      // chunks per block of the backward queue ((lookahead + 1) * qblock <= slots)
   int prefetch;    // k-blocks of L2 prefetch (TMA prefetch.tensor) beyond the SMEM ring
+  int tma3d;       // backward: tmGMN / tmHcMN3 / tmWMN3 are 3-D boxes of two 64-column blocks
   int strict;      // debug bit 0: serialise every item behind all earlier ones;
                    // debug bit 1: skip operand loads (measures raw MMA throughput; garbage results)
   // CCE_FLAG_P2P_COMBINE, fused into this kernel (P2P instantiation): when rank r's last-chunk
@@ -603,7 +604,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     cce_pair_kernel(const __grid_constant__ CUtensorMap tmHcK, const __grid_constant__ CUtensorMap tmWK,
                     const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
                     const __grid_constant__ CUtensorMap tmGK, const __grid_constant__ CUtensorMap tmWMN,
-                    const __grid_constant__ CUtensorMap tmDH, const PairParams P) {
+                    const __grid_constant__ CUtensorMap tmDH, const __grid_constant__ CUtensorMap tmHcMN3,
+                    const __grid_constant__ CUtensorMap tmWMN3, const PairParams P) {
   const GemmParams& g = P.g;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -635,6 +637,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     if (P.mode == 1) {
       tma_prefetch_desc(&tmGMN); tma_prefetch_desc(&tmHcMN); tma_prefetch_desc(&tmGK); tma_prefetch_desc(&tmWMN);
       tma_prefetch_desc(&tmDH);
+      if (P.tma3d) { tma_prefetch_desc(&tmHcMN3); tma_prefetch_desc(&tmWMN3); }
     }
     for (int s = 0; s < PSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 2 * PEPI_WARPS); }
@@ -761,6 +764,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
               tma_load_2d_pair(&tmHcK, fb, a, kb * BK, it.m0 + hr);
               tma_load_2d_pair(&tmWK, fb, b, kb * BK, it.n0 + hn);
             }
+          } else if (it.type == PT_DW && P.tma3d) {
+            // one instruction per operand: G^T (2 vocabulary blocks), Hc (2 hidden blocks, or
+            // the 2-D map for a 128-wide tail tile)
+            tma_load_3d_pair(&tmGMN, fb, a, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64);
+            if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmHcMN3, fb, b, 0, kb * BK, (it.n0 + hn) / 64);
+            else tma_load_2d_pair(&tmHcMN, fb, b, it.n0 + hn, kb * BK);
+          } else if (it.type == PT_DH && P.tma3d) {
+            tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb);
+            if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmWMN3, fb, b, 0, c0 + kb * BK, (it.n0 + hn) / 64);
+            else tma_load_2d_pair(&tmWMN, fb, b, it.n0 + hn, c0 + kb * BK);
           } else if (it.type == PT_DW) {
 #pragma unroll
             for (int j = 0; j < HM / 64; ++j) {
