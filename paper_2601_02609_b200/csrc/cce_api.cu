@@ -714,8 +714,14 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     } else {
       const bool quad = (h->cfg.flags & (CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY)) != 0;
       CUtensorMap tA, tB;
-      if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM)) return CCE_ERR_CUDA;
-      if (!make_map(&tB, W, D, V_local, ldw, quad ? 64 : pairk::PN / 2)) return CCE_ERR_CUDA;
+      if (pairk::KPS > 1 && !quad) {  // KPS k-blocks per box (column-block views)
+        if (!make_map_colblocks(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM, pairk::KPS) ||
+            !make_map_colblocks(&tB, W, D, V_local, ldw, pairk::PN / 2, pairk::KPS))
+          return CCE_ERR_CUDA;
+      } else {
+        if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM)) return CCE_ERR_CUDA;
+        if (!make_map(&tB, W, D, V_local, ldw, quad ? 64 : pairk::PN / 2)) return CCE_ERR_CUDA;
+      }
       pairk::PairParams pp{};
       pp.g = p;
       pp.mode = 0;
@@ -977,18 +983,23 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       // the dW item's G^T and Hc boxes and the dH item's W_c boxes come as 3-D boxes of two
       // 64-column blocks (4 -> 2 and 3 -> 2 instructions per k-block)
       const char* et = getenv("CCE_TMA3D");
-      const bool t3 = !quad && (!et || atoi(et) != 0);
+      const bool t3 = !quad && (pairk::KPS > 1 || !et || atoi(et) != 0);  // KPS > 1 needs the 3-D boxes
       CUtensorMap mHcMN3, mWMN3;
-      if (t3 && (!make_map_colblocks(&mHcMN3, Hc, D, L.Npad, D, 64, 2) ||
-                 !make_map_colblocks(&mWMN3, h->W, D, V_local, h->ldw, 64, 2)))
+      const uint32_t kr = pairk::KPS * 64;  // k-rows per box (MN-major operands)
+      if (t3 && (!make_map_colblocks(&mHcMN3, Hc, D, L.Npad, D, kr, 2) ||
+                 !make_map_colblocks(&mWMN3, h->W, D, V_local, h->ldw, kr, 2)))
         return CCE_ERR_CUDA;
-      if (!make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM) ||
-          !make_map(&mWK, h->W, D, V_local, h->ldw, quad ? 64 : pairk::PN / 2) ||
-          (t3 ? !make_map_blocked2(&mGMN, G, L.Npad, h->slots * (L.C / 64), 64, 2)
+      const bool k2 = pairk::KPS > 1 && !quad;
+      if ((k2 ? !make_map_colblocks(&mHcK, Hc, D, L.Npad, D, pairk::HM, pairk::KPS)
+              : !make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM)) ||
+          (k2 ? !make_map_colblocks(&mWK, h->W, D, V_local, h->ldw, pairk::PN / 2, pairk::KPS)
+              : !make_map(&mWK, h->W, D, V_local, h->ldw, quad ? 64 : pairk::PN / 2)) ||
+          (t3 ? !make_map_blocked2(&mGMN, G, L.Npad, h->slots * (L.C / 64), kr, 2)
               : !make_map_blocked(&mGMN, G, L.Npad, h->slots * (L.C / 64), 64)) ||
-          !make_map(&mHcMN, Hc, D, L.Npad, D, 64) ||
-          !make_map_blocked(&mGK, G, L.Npad, h->slots * (L.C / 64), quad ? 64 : pairk::HM) ||
-          !make_map(&mWMN, h->W, D, V_local, h->ldw, 64))
+          !make_map(&mHcMN, Hc, D, L.Npad, D, k2 ? kr : 64) ||
+          (k2 ? !make_map_blocked2(&mGK, G, L.Npad, h->slots * (L.C / 64), pairk::HM, pairk::KPS)
+              : !make_map_blocked(&mGK, G, L.Npad, h->slots * (L.C / 64), quad ? 64 : pairk::HM)) ||
+          !make_map(&mWMN, h->W, D, V_local, h->ldw, k2 ? kr : 64))
         return CCE_ERR_CUDA;
       if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
       pairk::PairParams pp{};

@@ -49,6 +49,18 @@ constexpr int PA_BYTES = HM * BK * 2;        // 16 KB
 constexpr int PB_BYTES = (PN / 2) * BK * 2;  // 16 KB
 constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES;
 constexpr int PRING = 4;
+// KPS k-blocks (64 wide) per ring stage, loaded with one 3-D TMA box per operand: the
+// per-k-block cost of the single-thread producer (TMA issue, expect_tx, barrier round
+// trip) was the limit -- KPS = 2 (3 stages x 64 KB) took the backward's dW / dH / G items
+// from 677 / 711 / 684 to 522 / 524 / 572 cycles per k-block (floor 512).
+#ifndef CCE_KPS
+#define CCE_KPS 2
+#endif
+constexpr int KPS = CCE_KPS;
+static_assert(KPS >= 1 && KPS <= 3 && PSTAGES % KPS == 0, "k-blocks per stage");
+constexpr int KSTAGES = PSTAGES / KPS;
+constexpr int KA_BYTES = KPS * PA_BYTES;
+constexpr int KB_BYTES = KPS * PB_BYTES;
 constexpr int PEPI_WARPS = 8;
 constexpr int PEPI_THREADS = 32 * PEPI_WARPS;
 constexpr int PTHREADS = 128 + PEPI_THREADS;
@@ -596,6 +608,37 @@ __device__ __forceinline__ void mma_item(const PItem& it, uint64_t* full_bar, ui
   }
 }
 
+// KPS > 1: stage s holds k-blocks KPS s .. KPS s + KPS - 1.  K-major operands: k-block kh
+// 16 KB further; MN-major operands (boxes {64, 64 KPS k-rows, MN blocks}): k-block kh 8 KB
+// further and the two 64-wide MN blocks KPS x 8 KB apart (leading byte offset).
+template <bool A_MN, bool B_MN>
+__device__ __forceinline__ void mma_item_k2(const PItem& it, uint64_t* full_bar, uint64_t* empty_bar, uint32_t a_base,
+                                            uint32_t b_base, uint32_t tmem_d, uint32_t& stage, uint32_t& phase) {
+  const uint32_t idesc = idesc_bf16_f32(PM, it.N, A_MN ? 1 : 0, B_MN ? 1 : 0);
+  const int ns = (it.num_kb + KPS - 1) / KPS;
+  for (int st = 0; st < ns; ++st) {
+    mbar_wait(&full_bar[stage], phase);
+    tc_fence_after();
+    if (elect_one()) {
+#pragma unroll
+      for (int kh = 0; kh < KPS; ++kh) {
+        const int kb = KPS * st + kh;
+        if (kb < it.num_kb) {
+          const uint64_t ad = sdesc_sw128(a_base + stage * KA_BYTES + kh * (A_MN ? 8192 : 16384), A_MN ? KPS * 8192 : 16, 1024);
+          const uint64_t bd = sdesc_sw128(b_base + stage * KB_BYTES + kh * (B_MN ? 8192 : 16384), B_MN ? KPS * 8192 : 16, 1024);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16_pair(tmem_d, ad + (uint64_t)(A_MN ? 128 * kk : 2 * kk),
+                           bd + (uint64_t)(B_MN ? 128 * kk : 2 * kk), idesc, (kb | kk) ? 1u : 0u);
+        }
+      }
+      umma_commit_pair(&empty_bar[stage]);
+    }
+    __syncwarp();
+    if (++stage == KSTAGES) { stage = 0; phase ^= 1; }
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 // ADAMW = 1: the backward queue with AdamW fused into the dW epilogue (cce_backward_adamw);
 // a separate instantiation so its epilogue's register demand leaves the default kernel alone.
@@ -610,7 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + PSTAGES * PA_BYTES;
+  uint8_t* sB = smem + KSTAGES * KA_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + PSTAGES * PSTAGE_BYTES);
   uint64_t* empty_bar = full_bar + PSTAGES;
   uint64_t* tfull_bar = empty_bar + PSTAGES;
@@ -639,7 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       tma_prefetch_desc(&tmDH);
       if (P.tma3d) { tma_prefetch_desc(&tmHcMN3); tma_prefetch_desc(&tmWMN3); }
     }
-    for (int s = 0; s < PSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < KSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 2 * PEPI_WARPS); }
     for (int r = 0; r < PRING; ++r) {
       mbar_init(&rfull_bar[r], 1);
@@ -729,6 +772,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         const int slot_blk0 = (it.c % P.slots) * (g.C / 64);  // first 64-column block of the slot
         const int c0 = it.c * g.C;
         unsigned long long tl0 = 0;
+        if constexpr (KPS > 1) {
+          // one 3-D box per operand per stage (KPS k-blocks); a ragged last stage: the k-blocks
+          // past num_kb are zero-filled (OOB) or zero rows / columns and their MMAs are skipped
+          const int ns = (it.num_kb + KPS - 1) / KPS;
+          for (int st = 0; st < ns; ++st) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            if (P.trace && st == 0) tl0 = gtimer();
+            uint8_t* a = sA + stage * KA_BYTES;
+            uint8_t* b = sB + stage * KB_BYTES;
+            const uint32_t fb = full_leader0 + stage * 8;
+            const int kb0 = KPS * st;
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * KPS * (PA_BYTES + b_bytes));
+            if (it.type == PT_FWD || it.type == PT_G) {
+              tma_load_3d_pair(&tmHcK, fb, a, 0, it.m0 + hr, kb0);
+              tma_load_3d_pair(&tmWK, fb, b, 0, it.n0 + hn, kb0);
+            } else if (it.type == PT_DW) {
+              tma_load_3d_pair(&tmGMN, fb, a, 0, kb0 * BK, slot_blk0 + (it.m0 + hr) / 64);
+              if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmHcMN3, fb, b, 0, kb0 * BK, (it.n0 + hn) / 64);
+              else tma_load_2d_pair(&tmHcMN, fb, b, it.n0 + hn, kb0 * BK);
+            } else {  // PT_DH
+              tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb0);
+              if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmWMN3, fb, b, 0, c0 + kb0 * BK, (it.n0 + hn) / 64);
+              else tma_load_2d_pair(&tmWMN, fb, b, it.n0 + hn, c0 + kb0 * BK);
+            }
+            if (++stage == KSTAGES) { stage = 0; phase ^= 1; }
+          }
+        } else
         for (int kb = 0; kb < it.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if (P.trace && kb == 0) tl0 = gtimer();
@@ -826,7 +896,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         const unsigned long long cm0 = P.trace ? clock64() : 0ull;
         unsigned long long fw = 0;
         unsigned long long* fwp = P.trace ? &fw : nullptr;
-        if (it.type == PT_DW)
+        if constexpr (KPS > 1) {
+          if (it.type == PT_DW)
+            mma_item_k2<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
+          else if (it.type == PT_DH)
+            mma_item_k2<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
+          else
+            mma_item_k2<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
+        } else if (it.type == PT_DW)
           mma_item<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
         else if (it.type == PT_DH)
           mma_item<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
