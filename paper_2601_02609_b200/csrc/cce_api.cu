@@ -355,9 +355,10 @@ cce_status launch_gemm(cce_handle* h, const CUtensorMap& a, const CUtensorMap& b
 cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                        const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5, const CUtensorMap& m6,
                        const pairk::PairParams& pp, cudaStream_t s, int prof_class, const CUtensorMap* m7 = nullptr,
-                       const CUtensorMap* m8 = nullptr) {
+                       const CUtensorMap* m8 = nullptr, const CUtensorMap* m9 = nullptr) {
   const CUtensorMap& x7 = m7 ? *m7 : m3;
   const CUtensorMap& x8 = m8 ? *m8 : m5;
+  const CUtensorMap& x9 = m9 ? *m9 : m4;
   static bool attr = false;
   if (!attr) {
     const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
@@ -371,11 +372,11 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
   {
     ProfScope ps(h, s, prof_class);
     if (pp.g.adamw)
-      pairk::cce_pair_kernel<1, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, pp);
+      pairk::cce_pair_kernel<1, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, x9, pp);
     else if (pp.world > 1)
-      pairk::cce_pair_kernel<0, 1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, pp);
+      pairk::cce_pair_kernel<0, 1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, x9, pp);
     else
-      pairk::cce_pair_kernel<0, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, pp);
+      pairk::cce_pair_kernel<0, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, x9, pp);
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
@@ -1020,6 +1021,11 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       while (pp.lookahead > 0 && (pp.lookahead + 1) * pp.qblock > slots) --pp.lookahead;
       pp.prefetch = 0;  // L2 prefetch measured harmful (adds L2 requests); env CCE_PREFETCH to experiment
       pp.tma3d = t3 ? 1 : 0;
+      // dlogits written by TMA stores from the epilogue's staging tiles (env CCE_GTMA=0: st.global)
+      CUtensorMap mGst;
+      const char* eg = getenv("CCE_GTMA");
+      pp.gtma = (!quad && (!eg || atoi(eg) != 0)) ? 1 : 0;
+      if (pp.gtma && !make_map_blocked2(&mGst, G, L.Npad, h->slots * (L.C / 64), 32, 1)) return CCE_ERR_CUDA;
       if (const char* e = getenv("CCE_PREFETCH")) pp.prefetch = atoi(e);
       pp.sched = at<int>(ws, L.sched);
       pp.trace = static_cast<TraceRec*>(h->trace);
@@ -1040,7 +1046,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       if (!make_map_f32(&mDH, dH32, D, L.Npad, D, 32, 32)) return CCE_ERR_CUDA;
       cce_status st = quad ? launch_quad(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1)
                            : launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, t3 ? &mHcMN3 : nullptr,
-                                         t3 ? &mWMN3 : nullptr);
+                                         t3 ? &mWMN3 : nullptr, pp.gtma ? &mGst : nullptr);
       if (st != CCE_OK) return st;
     } else {
     CUtensorMap mHcK, mWK, mHcMN, mGMN, mWMN, mGK;

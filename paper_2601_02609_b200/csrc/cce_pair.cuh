@@ -86,6 +86,7 @@ struct PairParams {
   int qblock;      // chunks per block of the backward queue ((lookahead + 1) * qblock <= slots)
   int prefetch;    // k-blocks of L2 prefetch (TMA prefetch.tensor) beyond the SMEM ring
   int tma3d;       // backward: tmGMN / tmHcMN3 / tmWMN3 are 3-D boxes of two 64-column blocks
+  int gtma;        // backward: the dlogits tiles are written by TMA stores (tmGst) from the staging tiles
   int strict;      // debug bit 0: serialise every item behind all earlier ones;
                    // debug bit 1: skip operand loads (measures raw MMA throughput; garbage results)
   // CCE_FLAG_P2P_COMBINE, fused into this kernel (P2P instantiation): when rank r's last-chunk
@@ -261,7 +262,7 @@ __device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, con
 }
 
 __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv,
-                                      float scale, __nv_bfloat16* gslot) {
+                                      float scale, __nv_bfloat16* gslot, const CUtensorMap* tmGst, int gblk0) {
   // G = s (exp(S - lse) - 1[v = y]) with s folded into the exponent.  With
   // label smoothing eps and z-loss lambda:
   //   G = s [(1 + 2 lambda lse) exp(S - lse) - (1 - eps) 1[v = y] - eps / V]
@@ -325,6 +326,19 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
                        pack_bf16(gg[8 * q4 + 4], gg[8 * q4 + 5]), pack_bf16(gg[8 * q4 + 6], gg[8 * q4 + 7]));
       }
     }
+    if (tmGst) {
+      // one TMA store of the warp's 32 x 64 tile (the staging XOR pattern is the 128-byte
+      // swizzle the map expects); the next block waits until the store has read the tile
+      fence_proxy_async_shared();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(tmGst, stg, 0, row0, gblk0 + (lcol64 >> 6));
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+      __syncwarp();
+      continue;
+    }
     __syncwarp();
     // 32 rows x 128 B of block (lcol64 / 64) are contiguous in the blocked layout
     uint4* dst = reinterpret_cast<uint4*>(gslot + ((size_t)(lcol64 >> 6) * p.Npad + row0) * 64);
@@ -333,6 +347,10 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
       const int r = i * 4 + (lane >> 3), c = lane & 7;
       dst[r * 8 + c] = stg[r * 8 + (c ^ (r & 7))];
     }
+    __syncwarp();
+  }
+  if (tmGst) {  // the dlogits are in global memory before the item is published
+    if (lane == 0) bulk_wait_all();
     __syncwarp();
   }
 }
@@ -648,7 +666,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
                     const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
                     const __grid_constant__ CUtensorMap tmGK, const __grid_constant__ CUtensorMap tmWMN,
                     const __grid_constant__ CUtensorMap tmDH, const __grid_constant__ CUtensorMap tmHcMN3,
-                    const __grid_constant__ CUtensorMap tmWMN3, const PairParams P) {
+                    const __grid_constant__ CUtensorMap tmWMN3, const __grid_constant__ CUtensorMap tmGst,
+                    const PairParams P) {
   const GemmParams& g = P.g;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -969,7 +988,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       } else if (it.type == PT_FWD) {
         if constexpr (!ADAMW) epi_fwd(g, taddr, e, it, k.nv);
       } else if (it.type == PT_G) {
-        if (!(P.strict & 32)) epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
+        if (!(P.strict & 32))
+          epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C,
+                P.gtma ? &tmGst : nullptr, (it.c % P.slots) * (g.C / 64));
       } else if (it.type == PT_RED) {
         if constexpr (P2P) epi_reduce(P, e, it, k.nv, leader);
       } else if (it.type == PT_DW) {

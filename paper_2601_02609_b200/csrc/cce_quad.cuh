@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(QTHREADS, 1)
         } else if (it.type == PT_FWD) {
           pairk::epi_fwd(g, taddr, e, it, k.nv);
         } else if (it.type == PT_G) {
-          pairk::epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C);
+          pairk::epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C, nullptr, 0);
         } else if (it.type == PT_DW) {
           pairk::epi_dw(g, taddr, e, it, have_acc);
         } else {
