@@ -35,7 +35,13 @@ N, D = H.shape
 V = W.shape[0]
 lo, hi = cce.shard_range(V, rank, world)
 Wr = W[lo:hi].contiguous()
-h = cce.CCEHandle(vocab_total=V, vocab_offset=lo, rank=rank, world=world, flags=cce.FLAG_P2P_COMBINE)
+mode = os.environ.get("CCE_MODE", "plain")   # plain | ls (label smoothing + z-loss) | rms (RMSNorm prologue)
+h = cce.CCEHandle(vocab_total=V, vocab_offset=lo, rank=rank, world=world, flags=cce.FLAG_P2P_COMBINE,
+                  label_smoothing=0.1 if mode == "ls" else 0.0, z_loss=1e-4 if mode == "ls" else 0.0)
+if mode == "rms":
+    Xb, gb = workload.make_rmsnorm_inputs(606, N, D)
+    Xt = torch.from_numpy(Xb.view(np.int16)).view(torch.bfloat16).to(dev)
+    gt = torch.from_numpy(gb.view(np.int16)).view(torch.bfloat16).to(dev)
 ws = h.workspace(N, D, hi - lo, dev)
 mine = cce.cce_p2p_export(ws)
 allh = [None] * world
@@ -44,10 +50,15 @@ cce.cce_p2p_attach(h.h, ws, N, D, [a[0] for a in allh], [a[1] for a in allh])
 dist.barrier()
 one = torch.ones((), dtype=torch.float32, device=dev)
 for step in range(0 if rank == absent else 2):
-    loss, lse, nv = h.forward(H, Wr, y)
     dH = torch.empty_like(H)
     dW = torch.empty_like(Wr)
-    h.backward(one, dH, dW)
+    if mode == "rms":
+        loss, lse, nv = h.forward_rmsnorm(Xt, gt, 1e-6, Wr, y)
+        dg = torch.empty_like(gt)
+        h.backward_rmsnorm(one, dH, dg, dW)
+    else:
+        loss, lse, nv = h.forward(H, Wr, y)
+        h.backward(one, dH, dW)
     torch.cuda.synchronize()
 err = cce.cce_get_error(h.h)
 if rank == absent:
@@ -70,12 +81,12 @@ def _free_port():
     return port
 
 
-def _run(tmp_path, world, absent=-1):
+def _run(tmp_path, world, absent=-1, mode="plain"):
     import __graft_entry__
     __graft_entry__.build()
     script = tmp_path / "worker.py"
     script.write_text(WORKER)
-    env = dict(os.environ, CCE_ROOT=ROOT, CCE_PORT=str(_free_port()), CCE_ABSENT=str(absent))
+    env = dict(os.environ, CCE_ROOT=ROOT, CCE_PORT=str(_free_port()), CCE_ABSENT=str(absent), CCE_MODE=mode)
     procs = [subprocess.Popen([sys.executable, str(script), str(r), str(world), str(tmp_path / f"r{r}.npz")], env=env,
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT) for r in range(world)]
     logs = []
@@ -118,3 +129,25 @@ def test_p2p_missing_peer_times_out_instead_of_hanging(tmp_path):
     res = _run(tmp_path, 2, absent=1)
     assert int(res[0]["err"]) == 7
     assert np.isnan(float(res[0]["loss"]))
+
+
+@pytest.mark.parametrize("mode", ["ls", "rms"])
+def test_p2p_exchange_with_regularised_loss_and_rmsnorm(tmp_path, mode):
+    """The peer-memory exchange carries the label-smoothing logit sums (4th stat) and feeds
+    the RMSNorm prologue's backward (dH reduced across ranks before dX / dgamma)."""
+    res = _run(tmp_path, 2, mode=mode)
+    p = workload.make_problem(700, 128, 3000, seed=606, ignore="bern40")
+    if mode == "ls":
+        ref = oracle.cce(p["H"], p["W"], p["labels"], label_smoothing=0.1, z_loss=1e-4)
+        dref = ref["dH"]
+    else:
+        X, g = workload.make_rmsnorm_inputs(606, 700, 128)
+        ref = oracle.cce_rmsnorm(X, g, p["W"], p["labels"], eps=1e-6)
+        dref = ref["dX"]
+    f = lambda b: (b.astype(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    for r in res:
+        assert int(r["err"]) == 0
+        assert np.array_equal(r["dH"], res[0]["dH"])
+    assert abs(float(res[0]["loss"]) - ref["loss"]) <= TOL_LOSS
+    assert rel_fro(f(res[0]["dH"]), dref) <= TOL_GRAD
+    assert rel_fro(np.concatenate([f(r["dW"]) for r in res]), ref["dW"]) <= TOL_GRAD
