@@ -951,6 +951,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
     p.dw_fp32 = (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0;
     p.dw_accumulate = (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0;
     p.dloss_c = nullptr;
+    if (const char* e = getenv("CCE_DBG_G")) p.dbg = atoi(e);
     if (opt) {
       p.adamw = 1;
       p.lr = opt->lr; p.beta1 = opt->beta1; p.beta2 = opt->beta2; p.eps = opt->eps; p.wd = opt->weight_decay;

@@ -86,7 +86,9 @@ struct GemmParams {
   const __nv_bfloat16* Win;  // the forward's W (theta when master == nullptr), row stride ldw
   __nv_bfloat16* Wout;       // bf16(theta_new), row stride ldw: == Win (in place) or a second buffer
   int ldw;
-  int adamw_inplace;         // Wout == Win: the chunk's dW epilogue waits for its dH items
+  int adamw_inplace;
+  int dbg;                   // debug (env CCE_DBG_G; garbage results): bit 0 skip the dlogits stores,
+                             // bit 1 skip the exponentials -- isolates the epilogue's energy cost         // Wout == Win: the chunk's dW epilogue waits for its dH items
 };
 
 

@@ -298,7 +298,7 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
       const int col0 = c0 + lcol0;
       float gg[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) gg[i] = ex2(fmaf(v[i], LOG2E, -off2));
+      for (int i = 0; i < 32; ++i) gg[i] = (p.dbg & 2) ? v[i] : ex2(fmaf(v[i], LOG2E, -off2));
       if (sa < 0.f) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) gg[i] = -gg[i];
@@ -331,7 +331,7 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
       // swizzle the map expects); the next block waits until the store has read the tile
       fence_proxy_async_shared();
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0 && !(p.dbg & 1)) {
         tma_store_3d(tmGst, stg, 0, row0, gblk0 + (lcol64 >> 6));
         bulk_commit();
         bulk_wait_read<0>();
