@@ -325,3 +325,37 @@ def test_nccl_path_on_one_rank(dev):
     assert a["loss"] == b["loss"]
     for k in ("lse_bits", "dH_bits", "dW_bits"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_unsupported_flag_combinations(dev):
+    """Host-side validation on a real device: combinations the library does not implement
+    are refused with CCE_ERR_UNSUPPORTED (2) before anything is enqueued."""
+    import ctypes
+    import paper_2601_02609_b200 as cce
+    L = cce.lib()
+    cfg = cce.cce_config()
+    L.cce_config_default(ctypes.byref(cfg))
+    cfg.vocab_total = 1000
+    h = ctypes.c_void_p()
+    for flags in (cce.FLAG_P2P_COMBINE | cce.FLAG_QUAD, cce.FLAG_P2P_COMBINE | cce.FLAG_ONE_CTA,
+                  cce.FLAG_P2P_COMBINE | cce.FLAG_DH_SEQ_SHARD, cce.FLAG_P2P_COMBINE | cce.FLAG_EXTERNAL_COMBINE):
+        cfg.flags = flags
+        assert L.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 2, flags
+    # world > 1 needs a communicator, the split-phase flag or the peer-memory flag
+    cfg.flags = 0
+    cfg.world, cfg.rank = 2, 0
+    assert L.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 1
+    cfg.flags = cce.FLAG_EXTERNAL_COMBINE
+    assert L.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 0
+    L.cce_destroy(h)
+
+
+def test_split_phase_finish_without_pending_phase(dev):
+    import torch
+    import paper_2601_02609_b200 as cce
+    h = cce.CCEHandle(vocab_total=1000, world=2, rank=0, vocab_offset=0, flags=cce.FLAG_EXTERNAL_COMBINE)
+    with pytest.raises(cce.CCEError):
+        cce.cce_forward_finish(h.h)
+    with pytest.raises(cce.CCEError):
+        cce.cce_backward_finish(h.h)
+    h.close()
