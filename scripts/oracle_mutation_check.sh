@@ -12,7 +12,7 @@ muts=(
  's/out\[d\] += g \* hr\[d\];/out[d] += g * w[d];/'                   # transposed operand in dW
  's/row_loss\[n\] = (1.0 - eps) \* (l - z\[y\])/row_loss[n] = (1.0 - eps) * (l + z[y])/'  # sign
  's/return m + log(s);/return log(s);/'                                # dropped max shift
- 's/double g = scale \* row_grad(zv, lse\[n\]/double g = scale * row_grad(zv, lse[0]/'  # wrong index
+ 's/double g = rscale\[n\] \* row_grad(zv, lse\[n\]/double g = rscale[n] * row_grad(zv, lse[0]/'  # wrong index
  's/return (1.0 - eps) \* ce + eps \* uni + zl;/return (1.0 - eps) * (ce + zl) + eps * uni;/'  # z-loss grad blended (Liger order)
  's/+ lam \* l \* l;/+ (1.0 - eps) * lam * l * l;/'                  # z-loss term blended (Liger order)
  's/double uni = p - 1.0 \/ (double)V;/double uni = p - 1.0 \/ (double)(V - 1);/'  # wrong uniform mass
