@@ -107,6 +107,42 @@ def normal_bf16(seed: int, stream: int, rows: int, cols: int, std: float,
     return out.reshape(rows, cols)
 
 
+def _as_i64(c: int) -> int:
+    """uint64 constant -> the int64 with the same bits."""
+    c &= M64
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+def _lsr(z, k: int):
+    """Logical right shift of int64 bit patterns (torch's >> is arithmetic)."""
+    return (z >> k) & ((1 << (64 - k)) - 1)
+
+
+def normal_bf16_torch(seed: int, stream: int, rows: int, cols: int, std: float, device,
+                      row_start: int = 0, chunk_elems: int = 1 << 27):
+    """normal_bf16 evaluated with torch int64 / fp64 ops on `device` (for inputs too large
+    to draw with numpy in a test, e.g. a 2.5e9-element W): the same splitmix64 counters,
+    Irwin-Hall sum and round-to-nearest-even casts, so the bits equal normal_bf16's
+    (tests/test_workload.py checks that on CPU).  Returns a [rows, cols] torch.bfloat16."""
+    import torch
+    key = _as_i64(int(_key(seed, stream)))
+    total = rows * cols
+    base = row_start * cols
+    out = torch.empty(total, dtype=torch.bfloat16, device=device)
+    for s in range(0, total, chunk_elems):
+        c = min(chunk_elems, total - s)
+        z = torch.arange(base + s, base + s + c, dtype=torch.int64, device=device) + key
+        z = z + _as_i64(0x9E3779B97F4A7C15)
+        z = (z ^ _lsr(z, 30)) * _as_i64(0xBF58476D1CE4E5B9)
+        z = (z ^ _lsr(z, 27)) * _as_i64(0x94D049BB133111EB)
+        h = z ^ _lsr(z, 31)
+        sm = (h & 0xFFFF) + (_lsr(h, 16) & 0xFFFF) + (_lsr(h, 32) & 0xFFFF) + _lsr(h, 48)
+        u = (sm.to(torch.float64) + 2.0) * (1.0 / 65536.0)
+        out[s:s + c] = (((u - 2.0) * math.sqrt(3.0)) * std).to(torch.float32).to(torch.bfloat16)
+        del z, h, sm, u
+    return out.view(rows, cols)
+
+
 _ZIPF_CACHE: dict = {}
 
 
