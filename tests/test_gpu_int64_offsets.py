@@ -96,3 +96,52 @@ def test_lse_loss_and_dW_rows_past_2_pow_31_elements():
     ref = oracle.dW_rows(H, W[pick], lab_sub, lse_ref, 1.0 / nvalid, np.arange(len(pick)))
     for i in range(len(pick)):
         assert rel_fro(dW_got[i], ref[i]) <= TOL_GRAD, (int(pick[i]), rel_fro(dW_got[i], ref[i]))
+
+
+def test_lse_and_dH_rows_past_2_pow_31_token_elements():
+    """The token side: N = 163,840 x D = 16,384 (H 5.4 GB, 10% ignored, so the compacted
+    rows pass 2^31 elements too, from compact row 131,072 on) against a small vocabulary
+    (V = 4,000, ragged tail tile).  LSE and dH are compared on rows before and past the
+    boundary, computed by oracle.rows one by one; dW by the zero-column-sum property."""
+    import torch
+    import __graft_entry__
+    import paper_2601_02609_b200 as cce
+    __graft_entry__.build()
+    dev = torch.device("cuda:0")
+    Nt, Dt, Vt = 163840, 16384, 4000
+    valid = workload.bernoulli_valid_mask(SEED, Nt, 0.1)
+    labels = np.where(valid, workload.randint(SEED, workload.S_LABEL, 0, Nt, 0, Vt - 1),
+                      workload.IGNORE_INDEX).astype(np.int32)
+    W = workload.normal_bf16(SEED, workload.S_W, Vt, Dt, 1.0 / math.sqrt(Dt))
+    Hd = workload.normal_bf16_torch(SEED, workload.S_H, Nt, Dt, 1.0, dev)
+    Wd = torch.from_numpy(W.view(np.int16)).view(torch.bfloat16).to(dev)
+    yd = torch.from_numpy(labels).to(dev)
+    h = cce.CCEHandle(vocab_total=Vt)
+    loss, lse, nv = h.forward(Hd, Wd, yd)
+    dH = torch.empty((Nt, Dt), dtype=torch.bfloat16, device=dev)
+    dW = torch.empty((Vt, Dt), dtype=torch.bfloat16, device=dev)
+    h.backward(torch.ones((), dtype=torch.float32, device=dev), dH, dW)
+    torch.cuda.synchronize()
+    h.close()
+    vrows = np.nonzero(valid)[0]
+    nvalid = len(vrows)
+    assert int(nv.item()) == nvalid and nvalid * Dt > (1 << 31)
+    assert bool(torch.isfinite(dH.float()).all()) and bool(torch.isfinite(dW.float()).all())
+    assert bool((dH[torch.from_numpy(~valid).to(dev)] == 0).all())
+    dWf = dW.float()
+    assert dWf.sum(0).norm().item() <= 1e-2 * dWf.norm().item()
+
+    # valid rows around compact row 131,072 (the 2^31-element boundary of the compact copy),
+    # around original row 131,072, and the last rows
+    pick = np.unique(np.concatenate([vrows[[0, 1, 131070, 131071, 131072, 131073, nvalid - 2, nvalid - 1]],
+                                     vrows[np.searchsorted(vrows, [131071, 131072, 140000])]]))
+    pick_d = torch.from_numpy(pick).to(dev)
+    H_pick = Hd[pick_d].view(torch.int16).cpu().numpy().view(np.uint16)
+    dH_pick = (dH[pick_d].view(torch.int16).cpu().numpy().astype(np.uint16).astype(np.uint32) << 16) \
+        .view(np.float32).astype(np.float64)
+    lse_ref, _, dH_ref = oracle.rows(H_pick, W, labels[pick], np.arange(len(pick)), scale=1.0 / nvalid)
+    lse_g = lse.cpu().numpy().astype(np.float64)[pick]
+    rel = np.abs(lse_g - lse_ref) / np.maximum(np.abs(lse_ref), 1.0)
+    assert rel.max() <= TOL_LSE, rel.max()
+    for i in range(len(pick)):
+        assert rel_fro(dH_pick[i], dH_ref[i]) <= TOL_GRAD, (int(pick[i]), rel_fro(dH_pick[i], dH_ref[i]))
