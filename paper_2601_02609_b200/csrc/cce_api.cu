@@ -1027,6 +1027,10 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       const char* eg = getenv("CCE_GTMA");
       pp.gtma = (!quad && (!eg || atoi(eg) != 0)) ? 1 : 0;
       if (pp.gtma && !make_map_blocked2(&mGst, G, L.Npad, h->slots * (L.C / 64), 32, 1)) return CCE_ERR_CUDA;
+#ifndef CCE_G_EARLY_DEFAULT
+#define CCE_G_EARLY_DEFAULT 1
+#endif
+      pp.g_early = CCE_G_EARLY_DEFAULT;  // accumulator released before the last dlogits store drains
       if (const char* e = getenv("CCE_PREFETCH")) pp.prefetch = atoi(e);
       pp.sched = at<int>(ws, L.sched);
       pp.trace = static_cast<TraceRec*>(h->trace);

@@ -86,6 +86,7 @@ struct PairParams {
   int qblock;      // chunks per block of the backward queue ((lookahead + 1) * qblock <= slots)
   int prefetch;    // k-blocks of L2 prefetch (TMA prefetch.tensor) beyond the SMEM ring
   int tma3d;       // backward: tmGMN / tmHcMN3 / tmWMN3 are 3-D boxes of two 64-column blocks
+  int g_early;     // backward, gtma: release the accumulator before draining the last dlogits store
   int gtma;        // backward: the dlogits tiles are written by TMA stores (tmGst) from the staging tiles
   int strict;      // debug bit 0: serialise every item behind all earlier ones;
                    // debug bit 1: skip operand loads (measures raw MMA throughput; garbage results)
@@ -262,7 +263,8 @@ __device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, con
 }
 
 __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv,
-                                      float scale, __nv_bfloat16* gslot, const CUtensorMap* tmGst, int gblk0) {
+                                      float scale, __nv_bfloat16* gslot, const CUtensorMap* tmGst, int gblk0,
+                                      bool early = false) {
   // G = s (exp(S - lse) - 1[v = y]) with s folded into the exponent.  With
   // label smoothing eps and z-loss lambda:
   //   G = s [(1 + 2 lambda lse) exp(S - lse) - (1 - eps) 1[v = y] - eps / V]
@@ -334,7 +336,7 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
       if (lane == 0 && !(p.dbg & 1)) {
         tma_store_3d(tmGst, stg, 0, row0, gblk0 + (lcol64 >> 6));
         bulk_commit();
-        bulk_wait_read<0>();
+        if (j2 + 1 < PN / 2 / 64 || !early) bulk_wait_read<0>();  // early: the last one is drained by the caller
       }
       __syncwarp();
       continue;
@@ -349,7 +351,10 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
     }
     __syncwarp();
   }
-  if (tmGst) {  // the dlogits are in global memory before the item is published
+  // TMA path, early: the caller releases the accumulator first (every TMEM read has
+  // retired), then drains the stores (bulk_wait_all) before the item is published and
+  // before the staging tile is reused
+  if (tmGst && !early) {
     if (lane == 0) bulk_wait_all();
     __syncwarp();
   }
@@ -990,7 +995,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       } else if (it.type == PT_G) {
         if (!(P.strict & 32))
           epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C,
-                P.gtma ? &tmGst : nullptr, (it.c % P.slots) * (g.C / 64));
+                P.gtma ? &tmGst : nullptr, (it.c % P.slots) * (g.C / 64), P.g_early);
       } else if (it.type == PT_RED) {
         if constexpr (P2P) epi_reduce(P, e, it, k.nv, leader);
       } else if (it.type == PT_DW) {
@@ -1021,6 +1026,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           if (rank == 0) mbar_arrive(&tempty_bar[acc]);
           else mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);  // TMEM reads retired (wait::ld)
         }
+      }
+      if (it.type == PT_G && P.gtma && P.g_early) {  // epi_g's last dlogits store: in global memory before publishing
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
       }
       if (P.mode == 0 && P.trace && leader && rank == 0 && it.q < P.trace_cap) {
         P.trace[it.q].q_type_c = ((unsigned long long)it.q << 32) | ((unsigned long long)it.type << 16) | (unsigned)it.c;
