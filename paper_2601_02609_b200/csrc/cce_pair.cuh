@@ -289,7 +289,7 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
   const int lane = e.rit & 31;
   uint4* stg = reinterpret_cast<uint4*>(e.stage);  // [32 rows][8 x 16 B]
   const int row0 = it.m0 + e.rank * HM + (e.rit & ~31);  // first row of this warp
-#pragma unroll 1
+#pragma unroll
   for (int j2 = 0; j2 < PN / 2 / 64; ++j2) {
     const int lcol64 = (it.n0 - c0) + cb + j2 * 64;  // 64-column block within the chunk
 #pragma unroll
