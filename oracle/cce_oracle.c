@@ -481,12 +481,20 @@ void oracle_rmsnorm_bwd(const double *dy, const double *x, const double *gamma, 
     }
 }
 
-/* fp64 -> bf16 bit pattern, round to nearest even (the CE path consumes bf16 H). */
+/* fp64 -> bf16 bit pattern: fp64 -> fp32 (RNE), then fp32 -> bf16 (RNE, ties to the even
+ * bf16 pattern; overflow rounds to inf, NaN stays a quiet NaN of the same sign).  The CE
+ * path consumes bf16 H formed in fp32 arithmetic (reading R18), hence the two
+ * steps.  Pinned by tests/test_oracle_pins.py::test_to_bf16_* (exact rational rounding
+ * and torch's float32 -> bfloat16 cast on ties, +-1 ulp, subnormals, the max, NaN). */
 void oracle_to_bf16(const double *a, int64_t n, uint16_t *out) {
     for (int64_t i = 0; i < n; ++i) {
-        const float f = (float)a[i];   /* fp64 -> fp32 (RNE), then fp32 -> bf16 (RNE) */
+        const float f = (float)a[i];
         uint32_t u;
         memcpy(&u, &f, 4);
+        if ((u & 0x7FFFFFFFu) > 0x7F800000u) {   /* NaN: keep the sign, quiet */
+            out[i] = (uint16_t)((u >> 16) | 0x0040u);
+            continue;
+        }
         u += 0x7FFFu + ((u >> 16) & 1u);
         out[i] = (uint16_t)(u >> 16);
     }

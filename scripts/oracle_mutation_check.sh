@@ -36,6 +36,13 @@ muts+=(
  's/c1 \/= (double)D;/c1 \/= 1.0;/'                                                       # dropped mean in c1
  's/dgamma\[k\] += dyr\[k\] \* (xr\[k\] \* rs);/dgamma[k] += dyr[k] * xr[k];/'           # dgamma without rstd
 )
+# bf16 rounding (oracle_to_bf16)
+muts+=(
+ 's/u += 0x7FFFu + ((u >> 16) \& 1u);/u += 0u;/'                         # truncation
+ 's/u += 0x7FFFu + ((u >> 16) \& 1u);/u += 0x8000u;/'                    # ties away from zero
+ 's/u += 0x7FFFu + ((u >> 16) \& 1u);/u += 0x7FFFu + (((u >> 16) \& 1u) ^ 1u);/'  # ties to odd
+ 's/if ((u \& 0x7FFFFFFFu) > 0x7F800000u) {/if (0) {/'  # NaN branch dropped
+)
 fail=0
 for m in "${muts[@]}"; do
   cp /tmp/oracle_orig.c oracle/cce_oracle.c

@@ -594,3 +594,90 @@ def test_rmsnorm_skipped_rows_and_composite():
     assert abs(float(loss) - r["loss"]) <= 1e-12
     np.testing.assert_allclose(r["dX"], xt.grad.numpy(), rtol=1e-10, atol=1e-14)
     np.testing.assert_allclose(r["dgamma"], gt.grad.numpy(), rtol=1e-10, atol=1e-14)
+
+
+# ---------------------------------------------------------------- bf16 rounding (oracle_to_bf16)
+def _bf16_exact(x32):
+    """Round a float32 value to bf16 with exact rationals: the nearest multiple of the bf16
+    spacing at x's binade, ties to the even significand, overflow past the largest finite
+    bf16 (plus half its spacing) to inf.  Independent of the oracle's bit manipulation."""
+    from fractions import Fraction
+    if math.isnan(x32):
+        return None
+    if math.isinf(x32):
+        return x32
+    q = Fraction(float(x32))
+    if q == 0:
+        return math.copysign(0.0, x32)
+    a = abs(q)
+    e = max(math.floor(math.log2(a)), -126)          # bf16 shares fp32's exponent range
+    while Fraction(2) ** e > a:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= a and e >= -126:
+        e += 1
+    e = max(e, -126)
+    ulp = Fraction(2) ** (e - 7)                    # 8 significand bits (7 stored)
+    k, r = divmod(a, ulp)
+    if r > ulp / 2 or (r == ulp / 2 and k % 2 == 1):
+        k += 1
+    v = k * ulp
+    bf_max = (2 - Fraction(1, 2 ** 7)) * Fraction(2) ** 127
+    out = math.inf if v > bf_max else float(v)
+    return -out if q < 0 else out
+
+
+def _bits_to_f64(b):
+    return (np.asarray(b, np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def _f32(bits):
+    return np.array(bits, dtype=np.uint32).view(np.float32)
+
+
+def _bf16_cases():
+    """float32 inputs at every place a rounding mistake shows: exact ties with an even and
+    an odd bf16 significand, one fp32 ulp either side of each tie, negatives, fp32 and bf16
+    subnormals, the largest finite bf16 and the tie above it (-> inf), zeros, infinities."""
+    base = []
+    for hi in (0x3F80, 0x3F81, 0x4049, 0x404A, 0x0001, 0x0002, 0x007F, 0x0080, 0x7F7E, 0x7F7F, 0x1234, 0x1235):
+        t = (hi << 16) | 0x8000                     # exact tie between hi and hi + 1
+        base += [t, t - 1, t + 1, (hi << 16), (hi << 16) | 0x7FFF, (hi << 16) | 0xFFFF]
+    base += [0x00000001, 0x00000002, 0x00008000, 0x00007FFF, 0x00018000, 0x7F7FFFFF,
+             0x00000000, 0x7F800000]
+    base = np.array(base, dtype=np.uint32)
+    return np.concatenate([base, base | np.uint32(0x80000000)])
+
+
+def test_to_bf16_exact_rounding():
+    """oracle.to_bf16 on float32-representable inputs equals exact round-to-nearest-even."""
+    x = _f32(_bf16_cases()).astype(np.float64)
+    got = _bits_to_f64(oracle.to_bf16(x))
+    for xi, gi in zip(x, got):
+        want = _bf16_exact(np.float32(xi))
+        assert (gi == want and math.copysign(1, gi) == math.copysign(1, want)), (float(xi), gi, want)
+
+
+def test_to_bf16_matches_torch_cast():
+    """... and torch's float32 -> bfloat16 cast, bit for bit (including inf on overflow);
+    fp64 inputs go through fp32 first, as the oracle's reading R18 states."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(11)
+    x = np.concatenate([_f32(_bf16_cases()).astype(np.float64),
+                        rng.standard_normal(20000) * 10.0 ** rng.uniform(-40, 38, 20000)])
+    ours = oracle.to_bf16(x)
+    ref = torch.tensor(x.astype(np.float32)).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(ours, ref)
+
+
+def test_to_bf16_double_rounding_and_nan():
+    """fp64 -> fp32 -> bf16: a double just above a bf16 tie that rounds onto the tie in fp32
+    then ties to even (the two-step definition); NaN stays NaN with its sign."""
+    tie = np.float64(_f32([0x3F808000])[0])               # 1 + 2^-8: tie, even neighbour 0x3F80
+    just_above = tie + 2.0 ** -40                         # fp32 rounds it back onto the tie
+    assert np.float32(just_above) == np.float32(tie)
+    assert oracle.to_bf16(np.array([just_above]))[0] == 0x3F80
+    assert oracle.to_bf16(np.array([tie + 2.0 ** -23]))[0] == 0x3F81   # a whole fp32 ulp above
+    nan = oracle.to_bf16(np.array([np.nan, -np.nan, _f32([0x7FFFFFFF])[0].astype(np.float64)]))
+    f = _bits_to_f64(nan)
+    assert np.isnan(f).all()
+    assert (nan[1] & 0x8000) and not (nan[0] & 0x8000)
