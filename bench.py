@@ -5,13 +5,17 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen05b] [--impl reference]
 
 One step = cce_forward + cce_backward (dloss = 1) over one batch of synthetic
-inputs already resident in HBM.  N > 1 (torchrun): the vocabulary is sharded
+inputs already resident in HBM.  N > 1 (torchrun, or self-launched through
+torch.distributed.run when WORLD_SIZE is unset): the vocabulary is sharded
 (rank r owns W rows [off_r, off_r + V/N)); H and labels are replicated; per-row
 (max, sum-exp, target-logit) stats are allgathered and dH is all-reduced with
 NCCL inside the library.  Total work is fixed as N grows ("strong" scaling).
 Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on
 the launching stream, with a 256 MB L2 flush (outside the events) between
 steps; barrier + synchronize on both sides; max over ranks.
+Parity inside the bench: after the warm-up every rank's loss and per-row LSE are
+compared with the oracle golden (tests/golden/<config>_seed42.npz, written offline by
+scripts/make_golden*.py from oracle/ only) and checked bit-identical across ranks.
 Prints one JSON line (rank 0).
 """
 from __future__ import annotations
@@ -182,6 +186,46 @@ def reference_arm(args):
     return 0
 
 
+def _self_launch(args_gpus):
+    """`python bench.py --gpus N` without torchrun: re-exec under torch.distributed.run (one
+    process per GPU, rendezvous on 127.0.0.1) and pass its exit code through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args_gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def golden_check(args, c, lse, loss_v, nvt, world, dist, dev):
+    """Parity inside the bench: loss and every valid row's LSE against the oracle golden
+    (fp64, computed offline by scripts/make_golden*.py, which call only oracle/), and the
+    outputs bit-identical on every rank (the rank-order merge makes them so)."""
+    import numpy as np
+    import torch
+    out = {}
+    path = os.path.join(ROOT, "tests", "golden", f"{args.config}_seed{args.seed}.npz")
+    if os.path.exists(path):
+        g = np.load(path)
+        rows = g["valid_rows"].astype(np.int64)
+        lse_g = lse.double().cpu().numpy()[rows]
+        rel = np.abs(lse_g - g["lse"]) / np.maximum(np.abs(g["lse"]), 1.0)
+        loss_ref = float(np.mean(g["lse"] - g["zy"]))
+        out = {"golden": os.path.relpath(path, ROOT), "lse_max_rel_err": float(rel.max()),
+               "loss_abs_err": abs(loss_v - loss_ref), "rows_checked": int(len(rows))}
+        out["ok"] = bool(rel.max() <= 1e-3 and abs(loss_v - loss_ref) <= 2e-3 and int(nvt) == len(rows))
+    if world > 1:
+        # identical LSE bits and loss on every rank
+        digest = torch.tensor([float(lse.view(torch.int32).long().sum().item()), loss_v], dtype=torch.float64,
+                              device=dev)
+        alld = [torch.zeros_like(digest) for _ in range(world)]
+        dist.all_gather(alld, digest)
+        out["ranks_identical"] = bool(all(torch.equal(alld[0], d) for d in alld))
+        out["ok"] = bool(out.get("ok", True) and out["ranks_identical"])
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -193,12 +237,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--flags", type=int, default=0, help="cce_config.flags (2 = per-chunk backward schedule)")
+    ap.add_argument("--flags", type=int, default=0, help="extra cce_config.flags bits (e.g. 64 = float32 gradients)")
     ap.add_argument("--combine", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1: the sharded exchange through NCCL or over peer memory (CCE_FLAG_P2P_COMBINE)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _self_launch(args.gpus)
 
     import numpy as np
     import torch
@@ -211,10 +257,6 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            print(json.dumps({"error": "--gpus N > 1 must be launched with torchrun"}), flush=True)
-            return 2
     # CCE_BENCH_ONE_GPU=1 (testing the N > 1 plumbing on a one-GPU box): every rank on cuda:0,
     # gloo for the host-side process group, --combine p2p for the exchange (NCCL refuses two
     # ranks on one GPU).  The timings of such a run are time-sliced, not a scaling result.
@@ -277,6 +319,10 @@ def main():
     # sanity: finite loss, non-zero finite grads
     assert math.isfinite(loss.item()) and int(nvt.item()) == n_valid
     assert torch.isfinite(dW.float()).all() and dW.float().abs().sum().item() > 0
+    parity = golden_check(args, c, lse, float(loss.item()), int(nvt.item()), world, dist, dev)
+    if parity.get("ok") is False:
+        print(json.dumps({"error": "in-bench parity failed", "parity": parity}), flush=True)
+        return 3
 
     # memory report: one step between cudaMemGetInfo / torch peak readings.  The
     # library never allocates (caller-owned workspace), so the device's free memory and the
@@ -406,7 +452,7 @@ def main():
                        "cce_step_host, one synchronised step at a time"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(workload.make_config(args.config, seed=args.seed))
 
     if world > 1:
@@ -429,6 +475,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": int(launches),
             "memory": memory,
+            "parity": parity,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
             "wall_s_timed_region": wall,
             "clocks": clocks,

@@ -71,24 +71,10 @@ typedef enum {
 
 /* flags */
 #define CCE_FLAG_NONE 0u
-/* Backward schedule: 0 (default) = one persistent work-queue launch for all
- * chunks; CCE_FLAG_BWD_PER_CHUNK = three launches per vocabulary chunk (the
- * straightforward schedule, kept for A/B measurements and tests). */
-#define CCE_FLAG_BWD_PER_CHUNK 2u
-/* Kernels: 0 (default) = CTA-pair kernels (tcgen05.mma.cta_group::2, 256-row
- * tiles); CCE_FLAG_ONE_CTA = single-CTA 128x256-tile kernels (kept for A/B). */
-#define CCE_FLAG_ONE_CTA 4u
-/* Kernels (default): persistent CTA-pair kernels (clusters of 2, tcgen05.mma.cta_group::2,
- * 256 x 256 tiles).  CCE_FLAG_PAIR names the default explicitly.  CCE_FLAG_QUAD = 4-CTA
- * clusters (two pairs sharing one operand by TMA multicast), plus single pairs running
- * the same work queue on the SMs 4-CTA clusters cannot use (measured slower on B200:
- * the multicast couples the two pairs' pipelines; kept for A/B). */
-#define CCE_FLAG_PAIR 8u
-#define CCE_FLAG_QUAD 32u
-/* With CCE_FLAG_QUAD (or alone): quad kernels on the co-resident 4-CTA clusters only. */
-#define CCE_FLAG_QUAD_ONLY 16u
-/* Gradient modes (pair / quad kernels only, CCE_FLAG_ONE_CTA
- * returns CCE_ERR_UNSUPPORTED): CCE_FLAG_GRAD_FP32 = dH and dW are float32 arrays;
+/* Flag bits 2, 4, 8, 16 and 32 named round-1 A/B kernel variants (per-chunk launches,
+ * 1-CTA tiles, 4-CTA multicast clusters), all measured slower than the default CTA-pair
+ * kernel and removed; cce_create rejects them (CCE_ERR_INVALID_VALUE), like any unknown bit. */
+/* Gradient modes: CCE_FLAG_GRAD_FP32 = dH and dW are float32 arrays;
  * CCE_FLAG_ACCUMULATE = dH += gradient and dW += gradient (micro-batch accumulation
  * into .grad, the paper's 4-8 step accumulation) instead of overwrite.
  * Accumulation adds in fp32 and rounds once (bf16 outputs); ignored rows of dH are
@@ -115,7 +101,10 @@ typedef enum {
  * tensor-core work tile by tile; release / acquire flags per step, waits bounded
  * (a peer that never signals makes cce_get_error return CCE_ERR_NCCL and loss NaN instead
  * of hanging).  Needs cce_p2p_attach; world <= 8; not with a communicator,
- * CCE_FLAG_EXTERNAL_COMBINE or CCE_FLAG_DH_SEQ_SHARD.  One backward per forward. */
+ * CCE_FLAG_EXTERNAL_COMBINE or CCE_FLAG_DH_SEQ_SHARD.  One backward per forward.  Every rank must
+ * own a non-empty shard at world > 1 (cce_forward returns CCE_ERR_UNSUPPORTED for V_local == 0:
+ * an empty shard runs no backward kernel, so it could neither flag nor reduce its dH tiles).
+ * Forward-only loops are safe: the stats exchange is double-buffered by step parity. */
 #define CCE_FLAG_P2P_COMBINE 1024u
 
 /* Reduction of the per-token losses (cce_config.reduction). */
@@ -138,8 +127,7 @@ typedef struct {
    *     l_n = (1-eps)(lse_n - z_y) + eps (lse_n - mean_v z_v)
    *   z_loss lambda >= 0: Def. Z-Loss, added: l_n += lambda lse_n^2
    * and their gradients.  mean_v runs over the GLOBAL
-   * vocabulary (vocab_total).  The CTA-pair / quad kernels support both; with
-   * CCE_FLAG_ONE_CTA a non-zero value makes cce_forward return CCE_ERR_UNSUPPORTED. */
+   * vocabulary (vocab_total). */
   float label_smoothing;
   float z_loss;
   /* CCE_REDUCTION_MEAN (default) / SUM / NONE.  With NONE, cce_forward's `loss` is an
@@ -204,7 +192,7 @@ cce_status cce_backward(cce_handle *h, const float *dloss, void *dH, void *dW, v
  *   rstd_n = 1 / sqrt((1/D) sum_i X[n,i]^2 + eps),  H[n,i] = (X[n,i] rstd_n) gamma_i
  * in fp32 (Alg. Fused RMSNorm Forward), fused into the gather of the valid
  * rows (ignored rows are never read) with rstd cached in the workspace ("Cache rstd for
- * backward").  eps >= 0; D <= 8192; gamma 16-byte aligned.  Other arguments and
+ * backward").  eps > 0 (else CCE_ERR_INVALID_VALUE: an all-zero row would give rstd = inf); D <= 8192; gamma 16-byte aligned.  Other arguments and
  * outputs as cce_forward.  X and gamma must stay alive and unmodified until the matching
  * backward has been enqueued.
  */
@@ -274,9 +262,8 @@ typedef struct {
  * opt->W_out == NULL it is UPDATED IN PLACE (bf16(theta_new)) and must be writable:
  * the epilogue of a chunk's dW tiles then waits until that chunk's dH tiles (which
  * read W) are complete, so the update never races the backward's own reads.  With
- * opt->W_out a distinct buffer (same shape and row stride as W), W is only read.  Pair kernel (the default)
- * only: CCE_FLAG_ONE_CTA / CCE_FLAG_QUAD / CCE_FLAG_ACCUMULATE return
- * CCE_ERR_UNSUPPORTED.  opt->m / opt->v NULL -> CCE_ERR_INVALID_VALUE.
+ * opt->W_out a distinct buffer (same shape and row stride as W), W is only read.
+ * CCE_FLAG_ACCUMULATE returns CCE_ERR_UNSUPPORTED.  opt->m / opt->v NULL -> CCE_ERR_INVALID_VALUE.
  */
 cce_status cce_backward_adamw(cce_handle *h, const float *dloss, void *dH, const cce_adamw_params *opt,
                               void *stream);

@@ -32,13 +32,7 @@ EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_byt
            "cce_forward_rmsnorm", "cce_backward_rmsnorm", "cce_combine_offsets", "cce_forward_finish",
            "cce_backward_finish", "cce_step_host_async", "cce_p2p_export", "cce_p2p_attach"]
 PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
-# "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH); with
-# FLAG_BWD_PER_CHUNK it is the per-chunk recompute/dlogits launches only.
-FLAG_BWD_PER_CHUNK = 2
-FLAG_ONE_CTA = 4
-FLAG_PAIR = 8
-FLAG_QUAD_ONLY = 16
-FLAG_QUAD = 32
+# "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH)
 FLAG_GRAD_FP32 = 64
 FLAG_ACCUMULATE = 128
 FLAG_EXTERNAL_COMBINE = 256
@@ -187,7 +181,19 @@ def cce_workspace_bytes(h, N: int, D: int, V_local: int) -> int:
     return int(lib().cce_workspace_bytes(h, N, D, V_local))
 
 
+def _check_layout(where, *rows_major, vec=()):
+    """The C ABI takes a row stride only: rows must be dense (stride(1) == 1) and the
+    1-D arrays contiguous, else the kernels would read the wrong elements."""
+    for t in rows_major:
+        if t is not None and t.dim() == 2 and t.shape[1] > 1 and t.stride(1) != 1:
+            raise ValueError(f"{where}: 2-D inputs need unit column stride (got strides {tuple(t.stride())})")
+    for t in vec:
+        if t is not None and not t.is_contiguous():
+            raise ValueError(f"{where}: 1-D inputs must be contiguous")
+
+
 def cce_forward(h, H, W, labels, loss, lse, n_valid, workspace, stream=None):
+    _check_layout("cce_forward", H, W, vec=(labels, lse))
     N, D = H.shape
     V_local = W.shape[0]
     _check(lib().cce_forward(h, _ptr(H), N, D, H.stride(0), _ptr(W), V_local, W.stride(0), _ptr(labels), _ptr(loss),
@@ -196,6 +202,7 @@ def cce_forward(h, H, W, labels, loss, lse, n_valid, workspace, stream=None):
 
 
 def cce_forward_rmsnorm(h, X, gamma, eps, W, labels, loss, lse, n_valid, workspace, stream=None):
+    _check_layout("cce_forward_rmsnorm", X, W, vec=(gamma, labels, lse))
     N, D = X.shape
     V_local = W.shape[0]
     _check(lib().cce_forward_rmsnorm(h, _ptr(X), N, D, X.stride(0), _ptr(gamma), float(eps), _ptr(W), V_local,
@@ -365,6 +372,9 @@ class CCEHandle:
         self.vocab_total = vocab_total
         self.ignore_index = ignore_index
         self._ws = None
+        # bumped by every forward: the backward computes gradients for the LAST forward on
+        # this handle (cce.h: one forward/backward pair in flight), so autograd checks it
+        self.generation = 0
 
     def workspace(self, N, D, V_local, device):
         import torch
@@ -381,6 +391,7 @@ class CCEHandle:
                 else torch.empty((), dtype=torch.float32, device=H.device))
         lse = torch.empty(N, dtype=torch.float32, device=H.device) if want_lse else None
         nv = torch.empty((), dtype=torch.int32, device=H.device)
+        self.generation += 1
         cce_forward(self.h, H, W, labels, loss, lse, nv, ws, stream)
         return loss, lse, nv
 
@@ -396,6 +407,7 @@ class CCEHandle:
                 else torch.empty((), dtype=torch.float32, device=X.device))
         lse = torch.empty(N, dtype=torch.float32, device=X.device) if want_lse else None
         nv = torch.empty((), dtype=torch.int32, device=X.device)
+        self.generation += 1
         cce_forward_rmsnorm(self.h, X, gamma, eps, W, labels, loss, lse, nv, ws, stream)
         return loss, lse, nv
 
@@ -426,8 +438,11 @@ def _check_inputs(H, W, labels):
     import torch
     if not (H.is_cuda and W.is_cuda and labels.is_cuda):
         raise ValueError("linear_cross_entropy: tensors must be on a CUDA device (no CPU fallback)")
+    if not (H.device == W.device == labels.device):
+        raise ValueError("linear_cross_entropy: H, W and labels must be on the same device")
     if H.dtype != torch.bfloat16 or W.dtype != torch.bfloat16 or labels.dtype != torch.int32:
         raise TypeError("linear_cross_entropy: H, W must be bfloat16 and labels int32")
+    _check_layout("linear_cross_entropy", H, W, vec=(labels,))
 
 
 def _make_function():
@@ -437,22 +452,31 @@ def _make_function():
         @staticmethod
         def forward(ctx, H, W, labels, handle):
             loss, lse, nv = handle.forward(H, W, labels)
+            # the library keeps this forward's state in the handle (like autograd-saved
+            # tensors: H, W, labels must stay alive and unmodified until the backward);
+            # a later forward on the same handle replaces it, which backward detects
             ctx.handle = handle
-            ctx.shapes = (H.shape, W.shape)
-            ctx.save_for_backward(H, W, labels)
+            ctx.generation = handle.generation
+            ctx.meta = (tuple(H.shape), tuple(W.shape), H.dtype, H.device)
+            ctx.keep = (H, W, labels)  # keep-alive only (never read back)
             ctx.mark_non_differentiable(lse, nv)
             return loss, lse, nv
 
         @staticmethod
         def backward(ctx, dloss, _dlse, _dnv):
             import torch
-            (H, W, labels) = ctx.saved_tensors
-            dH = torch.empty_like(H) if H.stride(0) == H.shape[1] else torch.empty(H.shape, dtype=H.dtype, device=H.device)
-            dW = torch.empty(W.shape, dtype=W.dtype, device=W.device)
+            if ctx.handle.generation != ctx.generation:
+                raise RuntimeError("linear_cross_entropy: the CCEHandle ran another forward before this "
+                                   "backward (one forward/backward pair in flight per handle, cce.h); "
+                                   "use one handle per loss call")
+            hs, ws, dt, dev = ctx.meta
+            dH = torch.empty(hs, dtype=dt, device=dev)
+            dW = torch.empty(ws, dtype=dt, device=dev)
             if dloss is None:
-                shape = (H.shape[0],) if ctx.handle.reduction == REDUCTION_NONE else ()
-                dloss = torch.zeros(shape, dtype=torch.float32, device=H.device)
+                shape = (hs[0],) if ctx.handle.reduction == REDUCTION_NONE else ()
+                dloss = torch.zeros(shape, dtype=torch.float32, device=dev)
             ctx.handle.backward(dloss.contiguous().float(), dH, dW)
+            ctx.keep = None
             return dH, dW, None, None
 
     return CCEFunction

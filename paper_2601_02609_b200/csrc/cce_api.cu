@@ -15,11 +15,9 @@
 
 #include "../../include/cce.h"
 #include "cce_aux.cuh"
-#include "cce_bwd.cuh"
-#include "cce_gemm.cuh"
+#include "cce_common.cuh"
 #include "cce_p2p.cuh"
 #include "cce_pair.cuh"
-#include "cce_quad.cuh"
 
 using namespace cce;
 
@@ -32,8 +30,8 @@ struct cce_handle {
   cce_config cfg;
   int device = 0;
   int num_sms = 148;
-  int64_t chunk = CCE_CHUNK;  // backward vocabulary chunk (env CCE_CHUNK overrides; multiple of 256)
-  int slots = GBUF_SLOTS;     // dlogits ring slots (env CCE_SLOTS overrides, 2..8)
+  int64_t chunk = CCE_CHUNK;  // backward vocabulary chunk (compile-time; multiple of 256)
+  int slots = GBUF_SLOTS;     // dlogits ring slots
   // state saved by the forward for the backward (like autograd-saved tensors)
   bool have_fwd = false;
   const void* W = nullptr;
@@ -64,9 +62,6 @@ struct cce_handle {
   int64_t ldx = 0;
   const void* gamma = nullptr;
   int64_t launches = 0;
-  int quad_clusters = -1;           // co-resident 4-CTA clusters (queried once)
-  cudaStream_t side = nullptr;      // forked stream for the NP = 1 co-launch
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* trace = nullptr;  // cce_debug_trace: per-item records of the backward
   size_t trace_bytes = 0;
   void* fwd_trace = nullptr;  // ... and of the forward (second half of the buffer)
@@ -156,21 +151,6 @@ static bool make_map_f32(CUtensorMap* m, const void* base, uint64_t cols, uint64
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-// 3-D bf16 tensor map over the column-blocked dlogits ring [blocks][rows][64]:
-// dims {64, rows, blocks}, box {64, box_rows, 1}, 128-byte swizzle.
-static bool make_map_blocked(CUtensorMap* m, const void* base, uint64_t rows, uint64_t blocks, uint32_t box_rows) {
-  PFN_encodeTiled enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {64, rows, blocks};
-  cuuint64_t strides[2] = {128, rows * 128};
-  cuuint32_t box[3] = {64, box_rows, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -290,7 +270,9 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
     L.p2p_flags = take(3 * P2P_MAX * 4);
     L.p2p_ready = take((size_t)P2P_MAX * L.p2p_tmax * 4);  // ready[rank][tile]
     L.p2p_done = take((size_t)2 * L.p2p_tmax * 4);         // done[tile][cta of the pair]
-    L.stats_all = take((size_t)world * L.Npad * 16);
+    // double-buffered by step parity: rank r's next forward pushes into the other half
+    // while a slower peer may still be reading this step's (forward-only loops too)
+    L.stats_all = take((size_t)2 * world * L.Npad * 16);
     L.dHred = take((size_t)L.Npad * D * 4);
     L.dH32 = take((size_t)L.Npad * D * 4);
   }
@@ -311,7 +293,7 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
   if (!p2p) L.dH32 = take((size_t)L.Npad * D * 4);
   L.n_chunks = (V_local + L.C - 1) / L.C;
   // backward work queue: head | g_done[n] | w_done[n] | dh_flag[tiles_d * ceil(Npad/BN)]
-  L.sched_ints = 2 + 2 * L.n_chunks + ((D + BM - 1) / BM) * ((L.Npad + BN - 1) / BN);
+  L.sched_ints = 2 + 2 * L.n_chunks + ((D + 127) / 128) * ((L.Npad + BN - 1) / BN);
   L.sched = take((size_t)L.sched_ints * 4);
   L.rstd_c = take((size_t)L.Npad * 4);            // RMSNorm prologue: rstd per compact row
   L.gpart = take((size_t)RMS_GP * D * 4);          // RMSNorm backward: per-block dgamma partials
@@ -336,22 +318,6 @@ int grid_for(long long work, int threads, int cap) {
   return (int)g;
 }
 
-template <int MODE>
-cce_status launch_gemm(cce_handle* h, const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
-                       cudaStream_t s) {
-  static bool attr_set[4] = {false, false, false, false};
-  if (!attr_set[MODE]) {
-    if (cudaFuncSetAttribute(cce_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES) !=
-        cudaSuccess)
-      return CCE_ERR_CUDA;
-    attr_set[MODE] = true;
-  }
-  {
-    ProfScope ps(h, s, MODE);
-    cce_gemm_kernel<MODE><<<h->num_sms, GEMM_THREADS, GEMM_SMEM_BYTES, s>>>(a, b, p);
-  }
-  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
-}
 cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                        const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5, const CUtensorMap& m6,
                        const pairk::PairParams& pp, cudaStream_t s, int prof_class, const CUtensorMap* m7 = nullptr,
@@ -359,15 +325,13 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
   const CUtensorMap& x7 = m7 ? *m7 : m3;
   const CUtensorMap& x8 = m8 ? *m8 : m5;
   const CUtensorMap& x9 = m9 ? *m9 : m4;
-  static bool attr = false;
-  if (!attr) {
-    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    if (cudaFuncSetAttribute(pairk::cce_pair_kernel<0, 0>, a, pairk::PSMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(pairk::cce_pair_kernel<1, 0>, a, pairk::PSMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(pairk::cce_pair_kernel<0, 1>, a, pairk::PSMEM) != cudaSuccess)
-      return CCE_ERR_CUDA;
-    attr = true;
-  }
+  // the >48 KB dynamic shared memory opt-in is per device: set on every launch (cheap,
+  // thread-safe, correct when one process drives several GPUs)
+  const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if (cudaFuncSetAttribute(pairk::cce_pair_kernel<0, 0>, a, pairk::PSMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(pairk::cce_pair_kernel<1, 0>, a, pairk::PSMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(pairk::cce_pair_kernel<0, 1>, a, pairk::PSMEM) != cudaSuccess)
+    return CCE_ERR_CUDA;
   const int grid = (h->num_sms / 2) * 2;  // whole CTA pairs
   {
     ProfScope ps(h, s, prof_class);
@@ -377,94 +341,6 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
       pairk::cce_pair_kernel<0, 1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, x9, pp);
     else
       pairk::cce_pair_kernel<0, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, x9, pp);
-  }
-  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
-}
-template <int NP>
-cudaError_t launch_quad_np(int grid, cudaStream_t s, const CUtensorMap& m0, const CUtensorMap& m1,
-                           const CUtensorMap& m2, const CUtensorMap& m3, const CUtensorMap& m4,
-                           const CUtensorMap& m5, const CUtensorMap& m6, const pairk::PairParams& pp) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(quadk::QTHREADS, 1, 1);
-  cfg.dynamicSmemBytes = quadk::QSMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2 * NP;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, quadk::cce_quad_kernel<NP>, m0, m1, m2, m3, m4, m5, m6, pp);
-}
-
-// How many 4-CTA clusters of the quad kernel can be co-resident (GPC packing leaves
-// SMs stranded), computed once per device.
-int quad_clusters(cce_handle* h) {
-  if (h->quad_clusters >= 0) return h->quad_clusters;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(h->num_sms / 4 * 4, 1, 1);
-  cfg.blockDim = dim3(quadk::QTHREADS, 1, 1);
-  cfg.dynamicSmemBytes = quadk::QSMEM;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 4;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, quadk::cce_quad_kernel<2>, &cfg) != cudaSuccess || n <= 0) {
-    cudaGetLastError();
-    n = h->num_sms / 4;
-  }
-  if (n > h->num_sms / 4) n = h->num_sms / 4;
-  if (const char* e = getenv("CCE_QUAD_CLUSTERS")) {  // debug / A-B: cap the 4-CTA clusters
-    const int c = atoi(e);
-    if (c >= 0 && c < n) n = c;
-  }
-  h->quad_clusters = n;
-  return n;
-}
-
-// The quad kernel on every co-resident 4-CTA cluster plus, on a forked stream, the
-// NP = 1 variant on the SMs the 4-CTA clusters strand; both drain the same queue.
-cce_status launch_quad(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
-                       const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5, const CUtensorMap& m6,
-                       const pairk::PairParams& pp, cudaStream_t s, int prof_class) {
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(quadk::cce_quad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, quadk::QSMEM) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(quadk::cce_quad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, quadk::QSMEM) !=
-            cudaSuccess)
-      return CCE_ERR_CUDA;
-    attr = true;
-  }
-  const int nq = quad_clusters(h);
-  const int rest_pairs = (h->cfg.flags & CCE_FLAG_QUAD_ONLY) && nq > 0 ? 0 : (h->num_sms - 4 * nq) / 2;
-  ProfScope ps(h, s, prof_class);
-  if (nq == 0) {
-    if (launch_quad_np<1>(2 * rest_pairs, s, m0, m1, m2, m3, m4, m5, m6, pp) != cudaSuccess) return CCE_ERR_CUDA;
-    return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
-  }
-  if (rest_pairs > 0) {
-    if (!h->side) {
-      if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
-        return CCE_ERR_CUDA;
-    }
-    if (cudaEventRecord(h->ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(h->side, h->ev_fork, 0) != cudaSuccess)
-      return CCE_ERR_CUDA;
-  }
-  if (launch_quad_np<2>(4 * nq, s, m0, m1, m2, m3, m4, m5, m6, pp) != cudaSuccess) return CCE_ERR_CUDA;
-  if (rest_pairs > 0) {
-    h->launches++;
-    if (launch_quad_np<1>(2 * rest_pairs, h->side, m0, m1, m2, m3, m4, m5, m6, pp) != cudaSuccess) return CCE_ERR_CUDA;
-    if (cudaEventRecord(h->ev_join, h->side) != cudaSuccess || cudaStreamWaitEvent(s, h->ev_join, 0) != cudaSuccess)
-      return CCE_ERR_CUDA;
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
@@ -500,7 +376,7 @@ const char* cce_status_string(cce_status s) {
 }
 
 const char* cce_build_info(void) {
-  return "cce sm_100a tcgen05/TMA engine BM=128 BN=256 BK=64 stages=4 chunk=" "8192";
+  return "cce sm_100a tcgen05.mma.cta_group::2 / TMA pair engine, tiles 256x256, BK=64 x 2 per stage, 3 stages, chunk=8192";
 }
 
 cce_status cce_create(cce_handle** out, const cce_config* cfg) {
@@ -515,9 +391,11 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
     return CCE_ERR_INVALID_VALUE;
   if ((cfg->flags & CCE_FLAG_P2P_COMBINE) &&
       (cfg->nccl_comm || cfg->world > P2P_MAX ||
-       (cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD | CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY |
-                      CCE_FLAG_ONE_CTA))))
+       (cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD))))
     return CCE_ERR_UNSUPPORTED;
+  const uint32_t known = CCE_FLAG_GRAD_FP32 | CCE_FLAG_ACCUMULATE | CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD |
+                         CCE_FLAG_P2P_COMBINE;
+  if (cfg->flags & ~known) return CCE_ERR_INVALID_VALUE;
   if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
   if (!(cfg->label_smoothing >= 0.f && cfg->label_smoothing < 1.f) || !(cfg->z_loss >= 0.f && cfg->z_loss < 1e30f))
     return CCE_ERR_INVALID_VALUE;
@@ -532,14 +410,6 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
   h->cfg = *cfg;
   h->device = dev;
   h->num_sms = sms > 0 ? sms : 148;
-  if (const char* e = getenv("CCE_CHUNK")) {
-    const long long c = atoll(e);
-    if (c >= 256 && c % 256 == 0) h->chunk = c;
-  }
-  if (const char* e = getenv("CCE_SLOTS")) {
-    const int v = atoi(e);
-    if (v >= 2 && v <= 8) h->slots = v;
-  }
   *out = h;
   return CCE_OK;
 }
@@ -551,9 +421,6 @@ cce_status cce_destroy(cce_handle* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : h->pool) cudaEventDestroy(e);
-  if (h->side) cudaStreamDestroy(h->side);
-  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-  if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (auto& e : h->stages)
     if (e.consumed) cudaEventDestroy(e.consumed);
   if (h->ev_copied) cudaEventDestroy(h->ev_copied);
@@ -635,7 +502,8 @@ cce_status cce_forward_rmsnorm(cce_handle* h, const void* X, int64_t N, int64_t 
                                float eps, const void* W, int64_t V_local, int64_t ldw, const int32_t* labels,
                                float* loss, float* lse, int32_t* n_valid, void* workspace, size_t workspace_bytes,
                                void* stream) {
-  if (!h || !gamma || !(eps >= 0.f) || !std::isfinite(eps)) return CCE_ERR_INVALID_VALUE;
+  // eps > 0 (Def. RMSNorm): an all-zero row would otherwise give rstd = inf
+  if (!h || !gamma || !(eps > 0.f) || !std::isfinite(eps)) return CCE_ERR_INVALID_VALUE;
   if (!aligned16(gamma) || D > 8192) return CCE_ERR_UNSUPPORTED;
   NormArgs na{gamma, eps};
   return forward_impl(h, X, N, D, ldx, W, V_local, ldw, labels, loss, lse, n_valid, workspace, workspace_bytes, stream,
@@ -659,6 +527,9 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) &&
       (!h->p2p_attached || workspace != h->p2p_ws || N != h->p2p_N || D != h->p2p_D))
     return CCE_ERR_INVALID_VALUE;  // peers address this workspace (layout of the attached N, D)
+  // P2P: every rank's backward kernel raises its dH-tile flags and runs its share of the
+  // cross-rank reduction; an empty shard would launch no kernel and stall its peers
+  if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) && h->cfg.world > 1 && V_local == 0) return CCE_ERR_UNSUPPORTED;
   if (!get_encode()) return CCE_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void* ws = workspace;
@@ -691,8 +562,6 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     p.D = (int)D;
     p.V_local = (int)V_local;
     p.Npad = (int)L.Npad;
-    p.c0 = 0;
-    p.width = (int)V_local;
     p.C = (int)L.C;
     p.vocab_offset = (int)h->cfg.vocab_offset;
     p.n_valid = nvp;
@@ -703,41 +572,21 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     p.z_loss = h->cfg.z_loss;
     p.inv_vtotal = (float)(1.0 / (double)h->cfg.vocab_total);
     p.zs_part = h->cfg.label_smoothing > 0.f ? at<float>(ws, L.zs_part) : nullptr;
-    if (h->cfg.flags & CCE_FLAG_ONE_CTA) {
-      if (h->cfg.label_smoothing != 0.f || h->cfg.z_loss != 0.f || h->cfg.reduction != CCE_REDUCTION_MEAN ||
-          (h->cfg.flags & (CCE_FLAG_GRAD_FP32 | CCE_FLAG_ACCUMULATE)))
-        return CCE_ERR_UNSUPPORTED;
-      CUtensorMap tA, tB;
-      if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, BM)) return CCE_ERR_CUDA;
-      if (!make_map(&tB, W, D, V_local, ldw, BN)) return CCE_ERR_CUDA;
-      cce_status st = launch_gemm<MODE_FWD>(h, tA, tB, p, s);
-      if (st != CCE_OK) return st;
-    } else {
-      const bool quad = (h->cfg.flags & (CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY)) != 0;
-      CUtensorMap tA, tB;
-      if (pairk::KPS > 1 && !quad) {  // KPS k-blocks per box (column-block views)
-        if (!make_map_colblocks(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM, pairk::KPS) ||
-            !make_map_colblocks(&tB, W, D, V_local, ldw, pairk::PN / 2, pairk::KPS))
-          return CCE_ERR_CUDA;
-      } else {
-        if (!make_map(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM)) return CCE_ERR_CUDA;
-        if (!make_map(&tB, W, D, V_local, ldw, quad ? 64 : pairk::PN / 2)) return CCE_ERR_CUDA;
-      }
-      pairk::PairParams pp{};
-      pp.g = p;
-      pp.mode = 0;
-      pp.n_chunks = 0;
-      pp.slots = h->slots;
-      pp.prefetch = 0;
-      if (const char* e = getenv("CCE_PREFETCH_FWD")) pp.prefetch = atoi(e);
-      if (const char* e = getenv("CCE_DEBUG_STRICT")) pp.strict = atoi(e);
-      pp.sched = at<int>(ws, L.sched);
-      pp.trace = static_cast<TraceRec*>(h->fwd_trace);
-      pp.trace_cap = (int)(h->fwd_trace_bytes / sizeof(TraceRec));
-      cce_status st = quad ? launch_quad(h, tA, tB, tA, tA, tA, tA, tA, pp, s, 0)
-                           : launch_pair(h, tA, tB, tA, tA, tA, tA, tA, pp, s, 0);
-      if (st != CCE_OK) return st;
-    }
+    // KPS k-blocks per box (column-block views)
+    CUtensorMap tA, tB;
+    if (!make_map_colblocks(&tA, at<void>(ws, L.Hc), D, L.Npad, D, pairk::HM, pairk::KPS) ||
+        !make_map_colblocks(&tB, W, D, V_local, ldw, pairk::PN / 2, pairk::KPS))
+      return CCE_ERR_CUDA;
+    pairk::PairParams pp{};
+    pp.g = p;
+    pp.mode = 0;
+    pp.n_chunks = 0;
+    pp.slots = h->slots;
+    pp.sched = at<int>(ws, L.sched);
+    pp.trace = static_cast<TraceRec*>(h->fwd_trace);
+    pp.trace_cap = (int)(h->fwd_trace_bytes / sizeof(TraceRec));
+    cce_status st = launch_pair(h, tA, tB, tA, tA, tA, tA, tA, pp, s, 0);
+    if (st != CCE_OK) return st;
   }
 
   // a4: merge tiles -> per-rank stats; a9: allgather across vocabulary shards
@@ -747,8 +596,9 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     ProfScope ps(h, s, 4);
     StatsPush push{};
     if (h->cfg.flags & CCE_FLAG_P2P_COMBINE) {  // a9 fused: every rank's slot `rank`, including ours
+      const size_t half = (size_t)((h->epoch + 1) & 1) * h->cfg.world * L.Npad;  // this step's half
       for (int r = 0; r < h->cfg.world; ++r)
-        push.dst[r] = reinterpret_cast<float4*>(h->peers.ws[r] + L.stats_all) + (size_t)h->cfg.rank * L.Npad;
+        push.dst[r] = reinterpret_cast<float4*>(h->peers.ws[r] + L.stats_all) + half + (size_t)h->cfg.rank * L.Npad;
       push.n = h->cfg.world;
     }
     k_merge_tiles<<<(unsigned)((L.Npad + 31) / 32), 32 * MERGE_SL, 0, s>>>(
@@ -774,7 +624,8 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_STATS, h->cfg.rank, h->cfg.world,
                                   epoch);
     k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_STATS, h->cfg.world, epoch, errp);
-    return forward_tail(h, at<float4>(ws, L.stats_all), loss, lse, n_valid, s);
+    return forward_tail(h, at<float4>(ws, L.stats_all) + (size_t)(epoch & 1) * h->cfg.world * L.Npad, loss, lse,
+                        n_valid, s);
   }
   if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) {
     // a9 done by the caller: it gathers every rank's `stats` into `stats_all`, then calls
@@ -893,8 +744,7 @@ cce_status cce_backward_adamw(cce_handle* h, const float* dloss, void* dH, const
   if (!h->have_fwd) return CCE_ERR_NO_FORWARD;
   if (!adamw_params_ok(opt)) return CCE_ERR_INVALID_VALUE;
   if (h->cfg.flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_P2P_COMBINE)) return CCE_ERR_UNSUPPORTED;
-  if (h->cfg.flags & (CCE_FLAG_ONE_CTA | CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY | CCE_FLAG_ACCUMULATE))
-    return CCE_ERR_UNSUPPORTED;
+  if (h->cfg.flags & CCE_FLAG_ACCUMULATE) return CCE_ERR_UNSUPPORTED;
   if (!adamw_aligned(opt) || (h->D % 8) != 0 || (opt->W_out && !aligned16(opt->W_out))) return CCE_ERR_UNSUPPORTED;
   return backward_impl(h, dloss, dH, const_cast<void*>(h->W), opt, stream);
 }
@@ -951,7 +801,6 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
     p.dw_fp32 = (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0;
     p.dw_accumulate = (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0;
     p.dloss_c = nullptr;
-    if (const char* e = getenv("CCE_DBG_G")) p.dbg = atoi(e);
     if (opt) {
       p.adamw = 1;
       p.lr = opt->lr; p.beta1 = opt->beta1; p.beta2 = opt->beta2; p.eps = opt->eps; p.wd = opt->weight_decay;
@@ -973,131 +822,52 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
     p.ls_eps = h->cfg.label_smoothing;
     p.z_loss = h->cfg.z_loss;
     p.inv_vtotal = (float)(1.0 / (double)h->cfg.vocab_total);
-    int slots = h->slots, strict = 0;
-    if (const char* e = getenv("CCE_DEBUG_SLOTS")) slots = atoi(e) >= 2 && atoi(e) <= h->slots ? atoi(e) : h->slots;
-    if (const char* e = getenv("CCE_DEBUG_STRICT")) strict = atoi(e);
-    if (!(h->cfg.flags & CCE_FLAG_ONE_CTA)) {
-      // CTA-pair (or quad: two pairs sharing an operand by TMA multicast) persistent
-      // backward: G / DW / DH tiles of every chunk from one work queue
-      const bool quad = (h->cfg.flags & (CCE_FLAG_QUAD | CCE_FLAG_QUAD_ONLY)) != 0;
-      CUtensorMap mHcK, mWK, mGMN, mHcMN, mGK, mWMN;
-      // CCE_TMA3D (default 1, pair kernel): one TMA instruction per operand per k-block --
-      // the dW item's G^T and Hc boxes and the dH item's W_c boxes come as 3-D boxes of two
-      // 64-column blocks (4 -> 2 and 3 -> 2 instructions per k-block)
-      const char* et = getenv("CCE_TMA3D");
-      const bool t3 = !quad && (pairk::KPS > 1 || !et || atoi(et) != 0);  // KPS > 1 needs the 3-D boxes
-      CUtensorMap mHcMN3, mWMN3;
-      const uint32_t kr = pairk::KPS * 64;  // k-rows per box (MN-major operands)
-      if (t3 && (!make_map_colblocks(&mHcMN3, Hc, D, L.Npad, D, kr, 2) ||
-                 !make_map_colblocks(&mWMN3, h->W, D, V_local, h->ldw, kr, 2)))
-        return CCE_ERR_CUDA;
-      const bool k2 = pairk::KPS > 1 && !quad;
-      if ((k2 ? !make_map_colblocks(&mHcK, Hc, D, L.Npad, D, pairk::HM, pairk::KPS)
-              : !make_map(&mHcK, Hc, D, L.Npad, D, pairk::HM)) ||
-          (k2 ? !make_map_colblocks(&mWK, h->W, D, V_local, h->ldw, pairk::PN / 2, pairk::KPS)
-              : !make_map(&mWK, h->W, D, V_local, h->ldw, quad ? 64 : pairk::PN / 2)) ||
-          (t3 ? !make_map_blocked2(&mGMN, G, L.Npad, h->slots * (L.C / 64), kr, 2)
-              : !make_map_blocked(&mGMN, G, L.Npad, h->slots * (L.C / 64), 64)) ||
-          !make_map(&mHcMN, Hc, D, L.Npad, D, k2 ? kr : 64) ||
-          (k2 ? !make_map_blocked2(&mGK, G, L.Npad, h->slots * (L.C / 64), pairk::HM, pairk::KPS)
-              : !make_map_blocked(&mGK, G, L.Npad, h->slots * (L.C / 64), quad ? 64 : pairk::HM)) ||
-          !make_map(&mWMN, h->W, D, V_local, h->ldw, k2 ? kr : 64))
-        return CCE_ERR_CUDA;
-      if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
-      pairk::PairParams pp{};
-      pp.g = p;
-      pp.mode = 1;
-      pp.n_chunks = (int)L.n_chunks;
-      pp.slots = slots;
-      pp.strict = strict;
-      // queue order (pair kernel): blocks of `qblock` chunks; G of block b + lookahead is
-      // queued before W of block b; deadlock-free iff (lookahead + 1) * qblock <= slots
-      pp.qblock = 1;
-      pp.lookahead = 1;
-      if (const char* e = getenv("CCE_QBLOCK")) pp.qblock = atoi(e);
-      if (const char* e = getenv("CCE_LOOKAHEAD")) pp.lookahead = atoi(e);
-      if (pp.qblock < 1) pp.qblock = 1;
-      if (pp.qblock > slots) pp.qblock = slots;
-      if (pp.lookahead < 0) pp.lookahead = 0;
-      while (pp.lookahead > 0 && (pp.lookahead + 1) * pp.qblock > slots) --pp.lookahead;
-      pp.prefetch = 0;  // L2 prefetch measured harmful (adds L2 requests); env CCE_PREFETCH to experiment
-      pp.tma3d = t3 ? 1 : 0;
-      // dlogits written by TMA stores from the epilogue's staging tiles (env CCE_GTMA=0: st.global)
-      CUtensorMap mGst;
-      const char* eg = getenv("CCE_GTMA");
-      pp.gtma = (!quad && (!eg || atoi(eg) != 0)) ? 1 : 0;
-      if (pp.gtma && !make_map_blocked2(&mGst, G, L.Npad, h->slots * (L.C / 64), 32, 1)) return CCE_ERR_CUDA;
-#ifndef CCE_G_EARLY_DEFAULT
-#define CCE_G_EARLY_DEFAULT 1
-#endif
-      pp.g_early = CCE_G_EARLY_DEFAULT;  // accumulator released before the last dlogits store drains
-      if (const char* e = getenv("CCE_PREFETCH")) pp.prefetch = atoi(e);
-      pp.sched = at<int>(ws, L.sched);
-      pp.trace = static_cast<TraceRec*>(h->trace);
-      pp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
-      if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) && h->cfg.world > 1) {
-        pp.peers = h->peers;
-        pp.world = h->cfg.world;
-        pp.prank = h->cfg.rank;
-        pp.epoch = h->epoch;
-        pp.tmax = (int)L.p2p_tmax;
-        pp.ready_off = L.p2p_ready;
-        pp.done_off = L.p2p_done;
-        pp.dH32_off = L.dH32;
-        pp.dHred_off = L.dHred;
-        pp.err = nvp + 1;
-      }
-      CUtensorMap mDH;
-      if (!make_map_f32(&mDH, dH32, D, L.Npad, D, 32, 32)) return CCE_ERR_CUDA;
-      cce_status st = quad ? launch_quad(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1)
-                           : launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, t3 ? &mHcMN3 : nullptr,
-                                         t3 ? &mWMN3 : nullptr, pp.gtma ? &mGst : nullptr);
-      if (st != CCE_OK) return st;
-    } else {
-    CUtensorMap mHcK, mWK, mHcMN, mGMN, mWMN, mGK;
-    if (!make_map(&mHcK, Hc, D, L.Npad, D, BM) || !make_map(&mWK, h->W, D, V_local, h->ldw, BN) ||
-        !make_map(&mHcMN, Hc, D, L.Npad, D, 64) || !make_map(&mGMN, G, L.C, h->slots * L.Npad, L.C, 64) ||
-        !make_map(&mWMN, h->W, D, V_local, h->ldw, 64) || !make_map(&mGK, G, L.C, h->slots * L.Npad, L.C, BN))
+    const int slots = h->slots;
+    // CTA-pair persistent backward: G / DW / DH tiles of every chunk from one work queue.
+    // One TMA instruction per operand per stage: K-major boxes of KPS 64-column blocks
+    // (Hc, W_c, dlogits rows), MN-major boxes of two 64-column blocks x KPS k-blocks
+    // (dlogits columns, Hc / W_c for the 256-wide hidden tiles; the 2-D maps serve the
+    // 128-wide tail tile).
+    CUtensorMap mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mHcMN3, mWMN3, mGst, mDH;
+    const uint32_t kr = pairk::KPS * 64;  // k-rows per box (MN-major operands)
+    if (!make_map_colblocks(&mHcMN3, Hc, D, L.Npad, D, kr, 2) ||
+        !make_map_colblocks(&mWMN3, h->W, D, V_local, h->ldw, kr, 2) ||
+        !make_map_colblocks(&mHcK, Hc, D, L.Npad, D, pairk::HM, pairk::KPS) ||
+        !make_map_colblocks(&mWK, h->W, D, V_local, h->ldw, pairk::PN / 2, pairk::KPS) ||
+        !make_map_blocked2(&mGMN, G, L.Npad, slots * (L.C / 64), kr, 2) ||
+        !make_map(&mHcMN, Hc, D, L.Npad, D, kr) ||
+        !make_map_blocked2(&mGK, G, L.Npad, slots * (L.C / 64), pairk::HM, pairk::KPS) ||
+        !make_map(&mWMN, h->W, D, V_local, h->ldw, kr) ||
+        !make_map_blocked2(&mGst, G, L.Npad, slots * (L.C / 64), 32, 1) ||  // dlogits TMA stores
+        !make_map_f32(&mDH, dH32, D, L.Npad, D, 32, 32))
       return CCE_ERR_CUDA;
-    if (h->cfg.flags & CCE_FLAG_BWD_PER_CHUNK) {
-      // reference schedule: three launches per vocabulary chunk
-      for (int64_t c0 = 0; c0 < V_local; c0 += L.C) {
-        p.c0 = (int)c0;
-        p.width = (int)((V_local - c0) < L.C ? (V_local - c0) : L.C);
-        p.dh_accumulate = c0 > 0 ? 1 : 0;
-        cce_status st;
-        if ((st = launch_gemm<MODE_G>(h, mHcK, mWK, p, s)) != CCE_OK) return st;
-        if ((st = launch_gemm<MODE_DW>(h, mHcMN, mGMN, p, s)) != CCE_OK) return st;
-        if ((st = launch_gemm<MODE_DH>(h, mWMN, mGK, p, s)) != CCE_OK) return st;
-      }
-    } else {
-      // one persistent launch: all chunks' G / DW / DH tiles from a device work queue
-      static bool attr = false;
-      if (!attr) {
-        if (cudaFuncSetAttribute(cce_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
-            cudaSuccess)
-          return CCE_ERR_CUDA;
-        attr = true;
-      }
-      if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
-      BwdParams bp;
-      bp.g = p;
-      bp.g.c0 = 0;
-      bp.g.width = 0;
-      bp.g.dh_accumulate = 0;
-      bp.n_chunks = (int)L.n_chunks;
-      bp.sched = at<int>(ws, L.sched);
-      bp.trace = static_cast<TraceRec*>(h->trace);
-      bp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
-      bp.slots = slots;
-      bp.strict = strict;
-      {
-        ProfScope ps(h, s, 1);
-        cce_bwd_kernel<<<h->num_sms, GEMM_THREADS, BWD_SMEM_BYTES, s>>>(mHcK, mWK, mHcMN, mGMN, mWMN, mGK, bp);
-      }
-      if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
+    if (cudaMemsetAsync(at<int>(ws, L.sched), 0, (size_t)L.sched_ints * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
+    pairk::PairParams pp{};
+    pp.g = p;
+    pp.mode = 1;
+    pp.n_chunks = (int)L.n_chunks;
+    pp.slots = slots;
+    // queue order: G of chunk c + 1 is queued before W of chunk c (deadlock-free iff
+    // (lookahead + 1) * qblock <= slots; measured: larger blocks / lookaheads are equal)
+    pp.qblock = 1;
+    pp.lookahead = 1;
+    pp.sched = at<int>(ws, L.sched);
+    pp.trace = static_cast<TraceRec*>(h->trace);
+    pp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));
+    if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) && h->cfg.world > 1) {
+      pp.peers = h->peers;
+      pp.world = h->cfg.world;
+      pp.prank = h->cfg.rank;
+      pp.epoch = h->epoch;
+      pp.tmax = (int)L.p2p_tmax;
+      pp.ready_off = L.p2p_ready;
+      pp.done_off = L.p2p_done;
+      pp.dH32_off = L.dH32;
+      pp.dHred_off = L.dHred;
+      pp.err = nvp + 1;
     }
-    }
+    cce_status st = launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, &mHcMN3, &mWMN3, &mGst);
+    if (st != CCE_OK) return st;
   } else if (V_local > 0 && N == 0 && opt) {
     // no rows: zero gradient, the optimizer step still applies (decay, moment decay)
     if (h->ldw != D) return CCE_ERR_UNSUPPORTED;

@@ -34,8 +34,7 @@
 // Hidden-dimension tiles are 256 wide with a 128-wide tail (D = 896 -> 256,256,256,128),
 // so no MMA work is wasted and dW / dH rows are written as contiguous vectors.
 #pragma once
-#include "cce_bwd.cuh"
-#include "cce_gemm.cuh"
+#include "cce_common.cuh"
 #include "cce_p2p.cuh"
 
 namespace cce {
@@ -53,11 +52,8 @@ constexpr int PRING = 4;
 // per-k-block cost of the single-thread producer (TMA issue, expect_tx, barrier round
 // trip) was the limit -- KPS = 2 (3 stages x 64 KB) took the backward's dW / dH / G items
 // from 677 / 711 / 684 to 522 / 524 / 572 cycles per k-block (floor 512).
-#ifndef CCE_KPS
-#define CCE_KPS 2
-#endif
-constexpr int KPS = CCE_KPS;
-static_assert(KPS >= 1 && KPS <= 3 && PSTAGES % KPS == 0, "k-blocks per stage");
+constexpr int KPS = 2;
+static_assert(PSTAGES % KPS == 0, "k-blocks per stage");
 constexpr int KSTAGES = PSTAGES / KPS;
 constexpr int KA_BYTES = KPS * PA_BYTES;
 constexpr int KB_BYTES = KPS * PB_BYTES;
@@ -84,12 +80,6 @@ struct PairParams {
   int slots;       // Gbuf ring slots
   int lookahead;   // backward queue: G of chunk block b + lookahead is queued before W of block b
   int qblock;      // chunks per block of the backward queue ((lookahead + 1) * qblock <= slots)
-  int prefetch;    // k-blocks of L2 prefetch (TMA prefetch.tensor) beyond the SMEM ring
-  int tma3d;       // backward: tmGMN / tmHcMN3 / tmWMN3 are 3-D boxes of two 64-column blocks
-  int g_early;     // backward, gtma: release the accumulator before draining the last dlogits store
-  int gtma;        // backward: the dlogits tiles are written by TMA stores (tmGst) from the staging tiles
-  int strict;      // debug bit 0: serialise every item behind all earlier ones;
-                   // debug bit 1: skip operand loads (measures raw MMA throughput; garbage results)
   // CCE_FLAG_P2P_COMBINE, fused into this kernel (P2P instantiation): when rank r's last-chunk
   // DH(tile) is complete it raises ready[r][tile] in every rank; RED(tile) items (tiles
   // tile % world == rank, queued last) wait for every rank's ready flag, sum the tile's partial
@@ -263,8 +253,7 @@ __device__ __forceinline__ void epi_fwd(const GemmParams& p, uint32_t taddr, con
 }
 
 __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv,
-                                      float scale, __nv_bfloat16* gslot, const CUtensorMap* tmGst, int gblk0,
-                                      bool early = false) {
+                                      float scale, const CUtensorMap* tmGst, int gblk0) {
   // G = s (exp(S - lse) - 1[v = y]) with s folded into the exponent.  With
   // label smoothing eps and z-loss lambda:
   //   G = s [(1 + 2 lambda lse) exp(S - lse) - (1 - eps) 1[v = y] - eps / V]
@@ -300,7 +289,7 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
       const int col0 = c0 + lcol0;
       float gg[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) gg[i] = (p.dbg & 2) ? v[i] : ex2(fmaf(v[i], LOG2E, -off2));
+      for (int i = 0; i < 32; ++i) gg[i] = ex2(fmaf(v[i], LOG2E, -off2));
       if (sa < 0.f) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) gg[i] = -gg[i];
@@ -328,36 +317,19 @@ __device__ __forceinline__ void epi_g(const GemmParams& p, uint32_t taddr, const
                        pack_bf16(gg[8 * q4 + 4], gg[8 * q4 + 5]), pack_bf16(gg[8 * q4 + 6], gg[8 * q4 + 7]));
       }
     }
-    if (tmGst) {
-      // one TMA store of the warp's 32 x 64 tile (the staging XOR pattern is the 128-byte
-      // swizzle the map expects); the next block waits until the store has read the tile
-      fence_proxy_async_shared();
-      __syncwarp();
-      if (lane == 0 && !(p.dbg & 1)) {
-        tma_store_3d(tmGst, stg, 0, row0, gblk0 + (lcol64 >> 6));
-        bulk_commit();
-        if (j2 + 1 < PN / 2 / 64 || !early) bulk_wait_read<0>();  // early: the last one is drained by the caller
-      }
-      __syncwarp();
-      continue;
-    }
+    // one TMA store of the warp's 32 x 64 tile (the staging XOR pattern is the 128-byte
+    // swizzle the map expects); the next block waits until the store has read the tile
+    fence_proxy_async_shared();
     __syncwarp();
-    // 32 rows x 128 B of block (lcol64 / 64) are contiguous in the blocked layout
-    uint4* dst = reinterpret_cast<uint4*>(gslot + ((size_t)(lcol64 >> 6) * p.Npad + row0) * 64);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = i * 4 + (lane >> 3), c = lane & 7;
-      dst[r * 8 + c] = stg[r * 8 + (c ^ (r & 7))];
+    if (lane == 0) {
+      tma_store_3d(tmGst, stg, 0, row0, gblk0 + (lcol64 >> 6));
+      bulk_commit();
+      if (j2 + 1 < PN / 2 / 64) bulk_wait_read<0>();  // the last one is drained by the caller
     }
     __syncwarp();
   }
-  // TMA path, early: the caller releases the accumulator first (every TMEM read has
-  // retired), then drains the stores (bulk_wait_all) before the item is published and
-  // before the staging tile is reused
-  if (tmGst && !early) {
-    if (lane == 0) bulk_wait_all();
-    __syncwarp();
-  }
+  // the caller releases the accumulator first (every TMEM read has retired), then drains
+  // the stores (bulk_wait_all) before the item is published and before the staging tile is reused
 }
 
 __device__ __forceinline__ void epi_dw(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it,
@@ -533,33 +505,6 @@ __device__ __forceinline__ void epi_reduce(const PairParams& P, const PEpi& e, c
       st_release_sys(reinterpret_cast<int*>(P.peers.ws[qr] + P.done_off) + 2 * it.tile_id + e.rank, P.epoch);
 }
 
-__device__ __forceinline__ void epi_dh(const GemmParams& p, uint32_t taddr, const PEpi& e, const PItem& it, int nv) {
-  const int t = it.m0 + e.rank * HM + e.rit;  // compact row
-  const int hw = it.N / 2;
-  const int cb = e.half * hw;
-  const bool acc = it.c > 0;
-#pragma unroll 1
-  for (int j = 0; j < hw / 32; ++j) {
-    float v[32];
-    tmem_ld32(taddr + cb + j * 32, v);
-    const int d0 = it.n0 + cb + j * 32;
-    if (t < nv && d0 < p.D) {
-      float4* dst = reinterpret_cast<float4*>(p.dH32 + (size_t)t * p.D + d0);
-      if (acc) {
-        float4 o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = __ldcg(dst + i);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          v[4 * i] += o[i].x; v[4 * i + 1] += o[i].y; v[4 * i + 2] += o[i].z; v[4 * i + 3] += o[i].w;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) __stcg(dst + i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
-    }
-  }
-}
-
 // dH epilogue through the TMA: each warp moves its 32 rows x 32 columns of the fp32
 // accumulator into its 4 KB staging tile (128-byte swizzle: conflict-free) and issues one
 // bulk tensor store (first chunk) or bulk reduce-add (later chunks) into dH32; the L2
@@ -600,38 +545,9 @@ __device__ __forceinline__ void epi_dh_tma(const CUtensorMap* tmDH, uint32_t tad
 }
 
 // ------------------------------------------------------------------ MMA issue (leader warp)
-// All 32 lanes wait on the full barrier; one elected lane issues the 4 K=16 pair MMAs
-// of a 64-wide k-block and commits the stage back to both CTAs' empty barriers.  The
-// descriptors are built once per k-block; the per-K step is a constant added to the
-// start-address field (+32 B K-major, +2 KB MN-major, in 16-byte units).
-template <bool A_MN, bool B_MN>
-__device__ __forceinline__ void mma_item(const PItem& it, uint64_t* full_bar, uint64_t* empty_bar, uint32_t a_base,
-                                         uint32_t b_base, uint32_t tmem_d, uint32_t& stage, uint32_t& phase,
-                                         unsigned long long* wait_ns) {
-  const uint32_t idesc = idesc_bf16_f32(PM, it.N, A_MN ? 1 : 0, B_MN ? 1 : 0);
-  for (int kb = 0; kb < it.num_kb; ++kb) {
-    if (wait_ns) {
-      const unsigned long long w0 = gtimer();
-      mbar_wait(&full_bar[stage], phase);
-      *wait_ns += gtimer() - w0;
-    }
-    mbar_wait(&full_bar[stage], phase);
-    tc_fence_after();
-    const uint64_t ad = sdesc_sw128(a_base + stage * PA_BYTES, A_MN ? 8192 : 16, 1024);
-    const uint64_t bd = sdesc_sw128(b_base + stage * PB_BYTES, B_MN ? 8192 : 16, 1024);
-    if (elect_one()) {
-#pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk)
-        umma_bf16_pair(tmem_d, ad + (uint64_t)(A_MN ? 128 * kk : 2 * kk), bd + (uint64_t)(B_MN ? 128 * kk : 2 * kk),
-                       idesc, (kb | kk) ? 1u : 0u);
-      umma_commit_pair(&empty_bar[stage]);
-    }
-    __syncwarp();
-    if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
-  }
-}
-
-// KPS > 1: stage s holds k-blocks KPS s .. KPS s + KPS - 1.  K-major operands: k-block kh
+// All 32 lanes wait on the full barrier; one elected lane issues the K=16 pair MMAs of the
+// stage's k-blocks and commits the stage back to both CTAs' empty barriers.
+// Stage s holds k-blocks KPS s .. KPS s + KPS - 1.  K-major operands: k-block kh
 // 16 KB further; MN-major operands (boxes {64, 64 KPS k-rows, MN blocks}): k-block kh 8 KB
 // further and the two 64-wide MN blocks KPS x 8 KB apart (leading byte offset).
 template <bool A_MN, bool B_MN>
@@ -704,7 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     if (P.mode == 1) {
       tma_prefetch_desc(&tmGMN); tma_prefetch_desc(&tmHcMN); tma_prefetch_desc(&tmGK); tma_prefetch_desc(&tmWMN);
       tma_prefetch_desc(&tmDH);
-      if (P.tma3d) { tma_prefetch_desc(&tmHcMN3); tma_prefetch_desc(&tmWMN3); }
+      tma_prefetch_desc(&tmHcMN3); tma_prefetch_desc(&tmWMN3); tma_prefetch_desc(&tmGst);
     }
     for (int s = 0; s < KSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 2 * PEPI_WARPS); }
@@ -727,7 +643,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   k.n_dt = (g.D + PN - 1) / PN;
   k.n_dh = k.t256 * k.n_dt;
   k.tv = (g.V_local + PN - 1) / PN;
-  const int slot_rows = g.Npad;
 
   if (warp == 3) {
     if (lane == 0 && rank == 0) {
@@ -737,9 +652,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       while (true) {
         const int q = atomicAdd(head, 1);
         PItem it = decode(P, k, q);
-        // debug bits 256 / 512 / 1024: run only the G / DW / DH items (no dependencies;
-        // measures one item type's throughput in isolation, results are garbage)
-        if ((P.strict & 1792) && it.type != PT_END && !((P.strict >> (8 + it.type - PT_G)) & 1)) continue;
         if (P.trace) it.t_deq = gtimer();
         mbar_wait(&rempty_l[rs], rph ^ 1);
         mbar_wait(&rempty_p[rs], rph ^ 1);
@@ -759,11 +671,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       // ===== TMA producer (both CTAs): next item from the local ring, dependencies, loads
       uint32_t stage = 0, phase = 0, rs = 0, rph = 0;
       const uint32_t full_leader0 = mapa_shared(smem_u32(&full_bar[0]), 0);
-      // debug bit 262144: L2 cache-policy hints on the backward's loads (measured: no gain;
-      // off by default -- the hinted instruction form itself cost ~2% in an A/B)
-      const bool hints = P.mode == 1 && (P.strict & 262144);
-      const uint64_t pol_keep = hints ? policy_evict_last() : policy_evict_normal();
-      const uint64_t pol_g = (P.strict & 4096) ? policy_evict_first() : policy_evict_normal();
       while (true) {
         if (rank == 0) mbar_wait(&rfull_bar[rs], rph);
         else mbar_wait_cluster(&rfull_bar[rs], rph);
@@ -772,9 +679,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         else mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&rempty_p[rs]), 0));
         if (++rs == PRING) { rs = 0; rph ^= 1; }
         if (it.type == PT_END) break;
-        if (P.mode == 1 && !(P.strict & 1792)) {
+        if (P.mode == 1) {
           // dependencies: only on items earlier in the queue (deadlock-free)
-          if (P.strict & 1) wait_ge(done_total, 2 * it.q);
           if (it.type == PT_G) {
             if (it.c >= P.slots) {
               const int wc = it.c - P.slots;
@@ -782,9 +688,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
             }
           } else {
             wait_ge(&g_done[it.c], 2 * p_n_g(k, p_chunk_width(g, it.c)));
-            // DH(c, tile) after DH(c-1, tile) is enforced where the epilogue issues its
-            // reduce-add; debug bit 8 also holds the operand loads back
-            if (it.type == PT_DH && (P.strict & 8)) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
+            // DH(c, tile) after DH(c-1, tile) is enforced where the epilogue issues its reduce-add
           }
           fence_proxy_async_global();
         }
@@ -796,99 +700,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         const int slot_blk0 = (it.c % P.slots) * (g.C / 64);  // first 64-column block of the slot
         const int c0 = it.c * g.C;
         unsigned long long tl0 = 0;
-        if constexpr (KPS > 1) {
-          // one 3-D box per operand per stage (KPS k-blocks); a ragged last stage: the k-blocks
-          // past num_kb are zero-filled (OOB) or zero rows / columns and their MMAs are skipped
-          const int ns = (it.num_kb + KPS - 1) / KPS;
-          for (int st = 0; st < ns; ++st) {
-            mbar_wait(&empty_bar[stage], phase ^ 1);
-            if (P.trace && st == 0) tl0 = gtimer();
-            uint8_t* a = sA + stage * KA_BYTES;
-            uint8_t* b = sB + stage * KB_BYTES;
-            const uint32_t fb = full_leader0 + stage * 8;
-            const int kb0 = KPS * st;
-            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * KPS * (PA_BYTES + b_bytes));
-            if (it.type == PT_FWD || it.type == PT_G) {
-              tma_load_3d_pair(&tmHcK, fb, a, 0, it.m0 + hr, kb0);
-              tma_load_3d_pair(&tmWK, fb, b, 0, it.n0 + hn, kb0);
-            } else if (it.type == PT_DW) {
-              tma_load_3d_pair(&tmGMN, fb, a, 0, kb0 * BK, slot_blk0 + (it.m0 + hr) / 64);
-              if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmHcMN3, fb, b, 0, kb0 * BK, (it.n0 + hn) / 64);
-              else tma_load_2d_pair(&tmHcMN, fb, b, it.n0 + hn, kb0 * BK);
-            } else {  // PT_DH
-              tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb0);
-              if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmWMN3, fb, b, 0, c0 + kb0 * BK, (it.n0 + hn) / 64);
-              else tma_load_2d_pair(&tmWMN, fb, b, it.n0 + hn, c0 + kb0 * BK);
-            }
-            if (++stage == KSTAGES) { stage = 0; phase ^= 1; }
-          }
-        } else
-        for (int kb = 0; kb < it.num_kb; ++kb) {
+        // one 3-D box per operand per stage (KPS k-blocks); a ragged last stage: the k-blocks
+        // past num_kb are zero-filled (OOB) or zero rows / columns and their MMAs are skipped
+        const int ns = (it.num_kb + KPS - 1) / KPS;
+        for (int st = 0; st < ns; ++st) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (P.trace && kb == 0) tl0 = gtimer();
-          uint8_t* a = sA + stage * PA_BYTES;
-          uint8_t* b = sB + stage * PB_BYTES;
+          if (P.trace && st == 0) tl0 = gtimer();
+          uint8_t* a = sA + stage * KA_BYTES;
+          uint8_t* b = sB + stage * KB_BYTES;
           const uint32_t fb = full_leader0 + stage * 8;
-          // the leader arms its full barrier with BOTH CTAs' bytes; the peer's TMA only
-          // signals completion bytes there (no per-stage remote arrive / release fence)
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (PA_BYTES + b_bytes));
-          // L2 prefetch `prefetch` k-blocks ahead of this load (hides HBM latency beyond
-          // the 6-stage SMEM ring; no SMEM or barrier involved)
-          const int pk = kb + P.prefetch;
-          if (P.prefetch > 0 && pk < it.num_kb) {
-            if (it.type == PT_FWD || it.type == PT_G) {
-              tma_prefetch_2d(&tmHcK, pk * BK, it.m0 + hr);
-              tma_prefetch_2d(&tmWK, pk * BK, it.n0 + hn);
-            } else if (it.type == PT_DW) {
-#pragma unroll
-              for (int j = 0; j < HM / 64; ++j) tma_prefetch_3d(&tmGMN, 0, pk * BK, slot_blk0 + (it.m0 + hr) / 64 + j);
-              for (int j = 0; j < it.N / 2 / 64; ++j) tma_prefetch_2d(&tmHcMN, it.n0 + hn + j * 64, pk * BK);
-            } else {
-              tma_prefetch_3d(&tmGK, 0, it.m0 + hr, slot_blk0 + pk);
-              for (int j = 0; j < it.N / 2 / 64; ++j) tma_prefetch_2d(&tmWMN, it.n0 + hn + j * 64, c0 + pk * BK);
-            }
-          }
-          // L2 policies (backward): the reused operands (Hc, the W chunk) evict_last, the
-          // dlogits ring per pol_g (debug bits 2048 / 4096 switch the hints off / G to evict_first)
+          const int kb0 = KPS * st;
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * KPS * (PA_BYTES + b_bytes));
           if (it.type == PT_FWD || it.type == PT_G) {
-            if (hints) {
-              tma_load_2d_pair_hint(&tmHcK, fb, a, kb * BK, it.m0 + hr, pol_keep);
-              tma_load_2d_pair_hint(&tmWK, fb, b, kb * BK, it.n0 + hn, pol_keep);
-            } else {
-              tma_load_2d_pair(&tmHcK, fb, a, kb * BK, it.m0 + hr);
-              tma_load_2d_pair(&tmWK, fb, b, kb * BK, it.n0 + hn);
-            }
-          } else if (it.type == PT_DW && P.tma3d) {
-            // one instruction per operand: G^T (2 vocabulary blocks), Hc (2 hidden blocks, or
-            // the 2-D map for a 128-wide tail tile)
-            tma_load_3d_pair(&tmGMN, fb, a, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64);
-            if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmHcMN3, fb, b, 0, kb * BK, (it.n0 + hn) / 64);
-            else tma_load_2d_pair(&tmHcMN, fb, b, it.n0 + hn, kb * BK);
-          } else if (it.type == PT_DH && P.tma3d) {
-            tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb);
-            if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmWMN3, fb, b, 0, c0 + kb * BK, (it.n0 + hn) / 64);
-            else tma_load_2d_pair(&tmWMN, fb, b, it.n0 + hn, c0 + kb * BK);
+            tma_load_3d_pair(&tmHcK, fb, a, 0, it.m0 + hr, kb0);
+            tma_load_3d_pair(&tmWK, fb, b, 0, it.n0 + hn, kb0);
           } else if (it.type == PT_DW) {
-#pragma unroll
-            for (int j = 0; j < HM / 64; ++j) {
-              if (hints)
-                tma_load_3d_pair_hint(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j, pol_g);
-              else
-                tma_load_3d_pair(&tmGMN, fb, a + j * 8192, 0, kb * BK, slot_blk0 + (it.m0 + hr) / 64 + j);
-            }
-            for (int j = 0; j < it.N / 2 / 64; ++j) {
-                if (hints) tma_load_2d_pair_hint(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK, pol_keep);
-                else tma_load_2d_pair(&tmHcMN, fb, b + j * 8192, it.n0 + hn + j * 64, kb * BK);
-              }
+            tma_load_3d_pair(&tmGMN, fb, a, 0, kb0 * BK, slot_blk0 + (it.m0 + hr) / 64);
+            if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmHcMN3, fb, b, 0, kb0 * BK, (it.n0 + hn) / 64);
+            else tma_load_2d_pair(&tmHcMN, fb, b, it.n0 + hn, kb0 * BK);
           } else {  // PT_DH
-            if (hints) tma_load_3d_pair_hint(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb, pol_g);
-            else tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb);
-            for (int j = 0; j < it.N / 2 / 64; ++j) {
-                if (hints) tma_load_2d_pair_hint(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK, pol_keep);
-                else tma_load_2d_pair(&tmWMN, fb, b + j * 8192, it.n0 + hn + j * 64, c0 + kb * BK);
-              }
+            tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb0);
+            if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmWMN3, fb, b, 0, c0 + kb0 * BK, (it.n0 + hn) / 64);
+            else tma_load_2d_pair(&tmWMN, fb, b, it.n0 + hn, c0 + kb0 * BK);
           }
-          if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
+          if (++stage == KSTAGES) { stage = 0; phase ^= 1; }
         }
         if (P.trace && rank == 0 && it.q < P.trace_cap) {
           P.trace[it.q].t_load0 = tl0;
@@ -918,27 +753,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         const uint32_t tmem_d = tmem_base + acc * PN;
         const unsigned long long tm0 = P.trace ? gtimer() : 0ull;
         const unsigned long long cm0 = P.trace ? clock64() : 0ull;
-        unsigned long long fw = 0;
-        unsigned long long* fwp = P.trace ? &fw : nullptr;
-        if constexpr (KPS > 1) {
-          if (it.type == PT_DW)
-            mma_item_k2<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
-          else if (it.type == PT_DH)
-            mma_item_k2<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
-          else
-            mma_item_k2<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
-        } else if (it.type == PT_DW)
-          mma_item<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+        if (it.type == PT_DW)
+          mma_item_k2<true, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
         else if (it.type == PT_DH)
-          mma_item<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+          mma_item_k2<false, true>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
         else
-          mma_item<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase, fwp);
+          mma_item_k2<false, false>(it, full_bar, empty_bar, a_base, b_base, tmem_d, stage, phase);
         if (elect_one()) umma_commit_pair(&tfull_bar[acc]);
         __syncwarp();
         if (P.trace && lane == 0 && it.q < P.trace_cap) {
           P.trace[it.q].t_mma0 = tm0;
           P.trace[it.q].t_mma1 = gtimer();
-          P.trace[it.q].t_full_wait = fw;
           P.trace[it.q].r0 = clock64() - cm0;
         }
       }
@@ -978,31 +803,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         acc = acc_it & 1;
         const uint32_t acc_phase = (acc_it >> 1) & 1;
         ++acc_it;
-        if (P.strict & 16) {
-          const uint32_t ba = smem_u32(&tfull_bar[acc]);
-          while (!mbar_try_wait(ba, acc_phase)) __nanosleep(256);
-        } else {
-          mbar_wait(&tfull_bar[acc], acc_phase);
-        }
+        mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
       }
       const uint32_t taddr = tmem_base + acc * PN + ((uint32_t)(e.q * 32) << 16);
       const unsigned long long t_epi0 = P.trace ? gtimer() : 0ull;
-      if (P.strict & 4) {
-        // debug: skip the epilogue entirely (no TMEM reads, no stores)
-      } else if (it.type == PT_FWD) {
+      if (it.type == PT_FWD) {
         if constexpr (!ADAMW) epi_fwd(g, taddr, e, it, k.nv);
       } else if (it.type == PT_G) {
-        if (!(P.strict & 32))
-          epi_g(g, taddr, e, it, k.nv, scale, g.gbuf + (size_t)(it.c % P.slots) * slot_rows * g.C,
-                P.gtma ? &tmGst : nullptr, (it.c % P.slots) * (g.C / 64), P.g_early);
+        epi_g(g, taddr, e, it, k.nv, scale, &tmGst, (it.c % P.slots) * (g.C / 64));
       } else if (it.type == PT_RED) {
         if constexpr (P2P) epi_reduce(P, e, it, k.nv, leader);
       } else if (it.type == PT_DW) {
         if constexpr (ADAMW) {
           // the chunk's dH tiles read W_c through the TMA: the update waits until every
           // DH(c, row tile, this hidden tile) item is complete (earlier in the queue)
-          if (g.adamw_inplace && warp == 4 && !(P.strict & 1792)) {
+          if (g.adamw_inplace && warp == 4) {
             const int dt = it.n0 / PN;
             for (int rt = lane; rt < k.t256; rt += 32) wait_ge(&dh_flag[rt * k.n_dt + dt], 2 * (it.c + 1));
           }
@@ -1013,11 +829,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         }
       } else {
         // DH(c-1, tile) halves published; re-acquire so the .cg loads below see them
-        if (leader && !(P.strict & 1792)) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
+        if (leader) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
         named_bar_sync(2, PEPI_THREADS);
         fence_proxy_async_global();  // the acquired flag orders the TMA reduce below
-        if (P.strict & 524288) epi_dh(g, taddr, e, it, k.nv);  // debug: the load-add-store epilogue
-        else if (!(P.strict & 64)) epi_dh_tma(&tmDH, taddr, e, it);
+        epi_dh_tma(&tmDH, taddr, e, it);
       }
       if (have_acc) {
         tc_fence_before();
@@ -1027,7 +842,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           else mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);  // TMEM reads retired (wait::ld)
         }
       }
-      if (it.type == PT_G && P.gtma && P.g_early) {  // epi_g's last dlogits store: in global memory before publishing
+      if (it.type == PT_G) {  // epi_g's last dlogits store: in global memory before publishing
         if (lane == 0) bulk_wait_all();
         __syncwarp();
       }

@@ -35,8 +35,6 @@ def test_tiny_config(dev, seed):
     _check(workload.make_config("tiny", seed=seed), dev)
 
 
-@pytest.mark.parametrize("flags", [0, 32, 16, "pairs_only", 4, 6],
-                         ids=["pair", "quad+pairs", "quad_only", "quad_queue_on_pairs", "cta1_queue", "cta1_per_chunk"])
 @pytest.mark.parametrize("N,D,V,ign", [
     (700, 128, 3000, "bern40"),        # ragged rows (5.5 tiles), ragged vocab (11.7 tiles)
     (257, 64, 256, "none"),             # exactly one vocab tile, one ragged row
@@ -44,13 +42,9 @@ def test_tiny_config(dev, seed):
     (384, 896, 9000, "bern40"),         # Qwen hidden size, 2 chunks
     (1000, 128, 41000, "bern40"),       # 6 chunks: Gbuf ring slots reused, dH accumulated 6x
 ])
-def test_multi_tile_shapes(dev, N, D, V, ign, flags, monkeypatch):
+def test_multi_tile_shapes(dev, N, D, V, ign):
     p = workload.make_problem(N, D, V, seed=N + V, ignore=ign)
-    if flags == "pairs_only":
-        # the quad work queue drained by single CTA pairs only (the co-launch variant)
-        monkeypatch.setenv("CCE_QUAD_CLUSTERS", "0")
-        flags = 32
-    _check(p, dev, flags=flags)
+    _check(p, dev)
 
 
 @pytest.mark.parametrize("N,D,V,ign", [
@@ -72,7 +66,6 @@ def test_large_hidden_sizes(dev, N, D, V, ign):
     (700, 128, 3000, "bern40", 0),       # ragged rows / vocabulary
     (384, 896, 9000, "bern40", 0),       # Qwen hidden size, 2 chunks
     (1000, 128, 41000, "bern40", 0),     # 6 chunks
-    (384, 896, 9000, "bern40", 32),      # quad kernels share the epilogues
 ])
 def test_label_smoothing_and_z_loss(dev, N, D, V, ign, flags, eps, lam):
     """the regularised loss (Def. Smoothed CE P:266-276, Def. Z-Loss
@@ -83,7 +76,6 @@ def test_label_smoothing_and_z_loss(dev, N, D, V, ign, flags, eps, lam):
 
 @pytest.mark.parametrize("reduction,eps,lam,flags", [
     ("sum", 0.0, 0.0, 0), ("none", 0.0, 0.0, 0), ("sum", 0.1, 1e-4, 0), ("none", 0.1, 1e-3, 0),
-    ("none", 0.0, 0.0, 32),     # quad kernels
 ])
 def test_reductions(dev, reduction, eps, lam, flags):
     """SURVEY 8(f) NEXT #3: sum and per-token ("none", per-row upstream gradients) losses."""
@@ -128,20 +120,6 @@ def test_label_smoothing_and_z_loss_regimes(dev, regime):
     """W = 0 (loss = ln V + lam ln^2 V exactly) and confident targets."""
     p = workload.make_problem(300, 128, 5000, seed=17, ignore="bern40", regime=regime)
     _check(p, dev, label_smoothing=0.1, z_loss=1e-3)
-
-
-def test_regularised_loss_rejected_by_one_cta_kernels(dev):
-    import paper_2601_02609_b200 as cce
-    p = workload.make_problem(100, 64, 500, seed=12, ignore="bern10")
-    H, W, y = to_dev(p, dev)
-    for kw in ({"label_smoothing": 0.1}, {"reduction": "sum"}, {"flags": cce.FLAG_GRAD_FP32}):
-        kw = dict(kw)
-        kw["flags"] = kw.get("flags", 0) | cce.FLAG_ONE_CTA
-        h = cce.CCEHandle(vocab_total=500, **kw)
-        with pytest.raises(cce.CCEError) as ei:
-            h.forward(H, W, y)
-        assert ei.value.status == 2     # CCE_ERR_UNSUPPORTED
-        h.close()
 
 
 @pytest.mark.parametrize("regime", ["peaked", "extreme", "zero"])
@@ -337,8 +315,7 @@ def test_unsupported_flag_combinations(dev):
     L.cce_config_default(ctypes.byref(cfg))
     cfg.vocab_total = 1000
     h = ctypes.c_void_p()
-    for flags in (cce.FLAG_P2P_COMBINE | cce.FLAG_QUAD, cce.FLAG_P2P_COMBINE | cce.FLAG_ONE_CTA,
-                  cce.FLAG_P2P_COMBINE | cce.FLAG_DH_SEQ_SHARD, cce.FLAG_P2P_COMBINE | cce.FLAG_EXTERNAL_COMBINE):
+    for flags in (cce.FLAG_P2P_COMBINE | cce.FLAG_DH_SEQ_SHARD, cce.FLAG_P2P_COMBINE | cce.FLAG_EXTERNAL_COMBINE):
         cfg.flags = flags
         assert L.cce_create(ctypes.byref(h), ctypes.byref(cfg)) == 2, flags
     # world > 1 needs a communicator, the split-phase flag or the peer-memory flag
@@ -358,4 +335,35 @@ def test_split_phase_finish_without_pending_phase(dev):
         cce.cce_forward_finish(h.h)
     with pytest.raises(cce.CCEError):
         cce.cce_backward_finish(h.h)
+    h.close()
+
+
+def test_autograd_refuses_a_stale_handle(dev):
+    """the library keeps the forward state in the handle; two forwards on one
+    handle before the first backward must fail loudly, not return the second's gradients."""
+    import torch
+    import paper_2601_02609_b200 as cce
+    p = workload.make_problem(100, 64, 500, seed=31, ignore="bern10")
+    H, W, y = to_dev(p, dev)
+    Hr = H.clone().requires_grad_(True)
+    h = cce.CCEHandle(vocab_total=500)
+    l1 = cce.linear_cross_entropy(Hr, W, y, handle=h)
+    l2 = cce.linear_cross_entropy(Hr, W, y, handle=h)
+    l2.backward(retain_graph=True)              # the latest forward: fine
+    with pytest.raises(RuntimeError, match="another forward"):
+        l1.backward()
+    h.close()
+
+
+def test_rmsnorm_eps_must_be_positive(dev):
+    import torch
+    import paper_2601_02609_b200 as cce
+    h = cce.CCEHandle(vocab_total=500)
+    X = torch.zeros(8, 64, dtype=torch.bfloat16, device=dev)
+    g = torch.ones(64, dtype=torch.bfloat16, device=dev)
+    W = torch.zeros(500, 64, dtype=torch.bfloat16, device=dev)
+    y = torch.zeros(8, dtype=torch.int32, device=dev)
+    with pytest.raises(cce.CCEError) as ei:
+        h.forward_rmsnorm(X, g, 0.0, W, y)
+    assert ei.value.status == 1
     h.close()
