@@ -71,10 +71,11 @@ for name, rec in (("forward", allrec[1]), ("backward", allrec[0])):
     cyc = rec[:, 13].astype(np.float64)
     lat = rec[:, 15].astype(np.float64)
     print(f" {name}: items {len(rec)} span {ep1.max():.1f} us; sum of dep-wait {np.sum(rdy-deq):.0f} us")
-    npk = rec[:, 14].astype(np.int64)
+    # DW / DH items grouped by their hidden tile (column offset n0): a narrow tail tile shows up
+    npk = np.where((typ == 2) | (typ == 3), (rec[:, 6] & np.uint64(0xFFFFFFFF)).astype(np.int64), 0)
     for t, npv in sorted(set(zip(typ.tolist(), npk.tolist()))):
         m = (typ == t) & (npk == npv)
-        print(f"   {NAMES[t]:3s}{'/NP' + str(npv) if npv else '':5s} n={m.sum():6d} kb={kb[m].mean():5.1f} | mma window {np.mean(m1[m]-m0[m]):7.2f} us "
+        print(f"   {NAMES[t]:3s}{'@' + str(npv) if npv else '':5s} n={m.sum():6d} kb={kb[m].mean():5.1f} | mma window {np.mean(m1[m]-m0[m]):7.2f} us "
               f"(full-wait {np.mean(fw[m]):6.2f}) | load window {np.mean(l1[m]-l0[m]):7.2f} | "
               f"mma_end->epi0 {np.mean(ep0[m]-m1[m]):6.2f} | epi {np.mean(ep1[m]-ep0[m]):6.2f} | dep-wait {np.mean(rdy[m]-deq[m]):6.2f} | "
               f"per-kb {np.mean((m1[m]-m0[m])/np.maximum(kb[m],1)):.3f} us, {np.mean(cyc[m]/np.maximum(kb[m],1)):.0f} cyc"

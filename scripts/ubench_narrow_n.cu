@@ -9,26 +9,26 @@
 #include "../paper_2601_02609_b200/csrc/sm100.cuh"
 using namespace cce;
 
-template <int N, int AMN>
+template <int N, int AMN, int M = 256, int PAIR = 1, int KB = 1>
 __global__ void __launch_bounds__(128, 1) knarrow(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar[8];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 8; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc_pair(&slot, 512);
+  if (warp == 1) { if (PAIR) tmem_alloc_pair(&slot, 512); else tmem_alloc(&slot, 512); }
   tc_fence_before();
-  cluster_sync_all();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = slot;
   if (warp == 0 && lane == 0 && rank == 0) {
     const uint32_t a = smem_u32(smem), b = smem_u32(smem + 65536);
-    const uint32_t idesc = idesc_bf16_f32(256, N, AMN, 0);
+    const uint32_t idesc = idesc_bf16_f32(M, N, AMN, 0);
     uint32_t ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const unsigned long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -36,29 +36,30 @@ __global__ void __launch_bounds__(128, 1) knarrow(int iters, unsigned long long*
       if (it >= 8) { mbar_wait(&bar[s], ph[s]); ph[s] ^= 1; }
       tc_fence_after();
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint64_t ad = AMN ? sdesc_sw128(a + (s & 1) * 32768 + k * 2048, 8192, 1024)
-                                : sdesc_sw128(a + (s & 1) * 16384 + k * 32, 16, 1024);
-        const uint64_t bd = sdesc_sw128(b + (s & 1) * 8192 + k * 32, 16, 1024);
-        umma_bf16_pair(tmem + (it & 1) * 256, ad, bd, idesc, k > 0 ? 1u : 0u);
+      for (int k = 0; k < 4 * KB; ++k) {
+        const uint64_t ad = AMN ? sdesc_sw128(a + (s & 1) * 32768 + (k & 3) * 2048, 8192, 1024)
+                                : sdesc_sw128(a + (s & 1) * 16384 + (k & 3) * 32, 16, 1024);
+        const uint64_t bd = sdesc_sw128(b + (s & 1) * 8192 + (k & 3) * 32, 16, 1024);
+        if (PAIR) umma_bf16_pair(tmem + (it & 1) * 256, ad, bd, idesc, k > 0 ? 1u : 0u);
+        else umma_bf16(tmem + (it & 1) * 256, ad, bd, idesc, k > 0 ? 1u : 0u);
       }
-      umma_commit_pair(&bar[s]);
+      if (PAIR) umma_commit_pair(&bar[s]); else umma_commit(&bar[s]);
     }
     for (int s = 0; s < 8; ++s) mbar_wait(&bar[s], ph[s]);
     out[blockIdx.x] = clock64() - t0;
   }
   __syncwarp();
   tc_fence_before();
-  cluster_sync_all();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc_pair(tmem, 512);
+  if (warp == 1) { if (PAIR) tmem_dealloc_pair(tmem, 512); else tmem_dealloc(tmem, 512); }
 }
 
-template <int N, int AMN>
+template <int N, int AMN, int M = 256, int PAIR = 1, int KB = 1>
 void run(int grid, int iters) {
   unsigned long long* d;
   cudaMalloc(&d, grid * 8);
-  auto k = knarrow<N, AMN>;
+  auto k = knarrow<N, AMN, M, PAIR, KB>;
   const int sm = 100 * 1024;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaLaunchConfig_t cfg = {};
@@ -67,7 +68,7 @@ void run(int grid, int iters) {
   cfg.dynamicSmemBytes = sm;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.x = PAIR ? 2 : 1;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -85,17 +86,24 @@ void run(int grid, int iters) {
   unsigned long long h[256];
   cudaMemcpy(h, d, grid * 8, cudaMemcpyDeviceToHost);
   unsigned long long mx = 0;
-  for (int i = 0; i < grid; i += 2) mx = h[i] > mx ? h[i] : mx;
-  const double flops = (double)(grid / 2) * iters * 4 * 256.0 * N * 16 * 2;
-  printf("N=%3d A_%s err=%s: %.3f ms, %.1f TFLOP/s, cycles per 64-k-block %.1f (floor %d)\n", N,
-         AMN ? "MN" : "K ", cudaGetErrorString(err), ms, flops / ms / 1e9, (double)mx / iters, 2 * N);
+  for (int i = 0; i < grid; i += (PAIR ? 2 : 1)) mx = h[i] > mx ? h[i] : mx;
+  const double flops = (double)(PAIR ? grid / 2 : grid) * iters * 4 * KB * (double)M * N * 16 * 2;
+  const int floor = (M > 128 ? M : 128) * N / (256 * (PAIR ? 2 : 1)) * 4;
+  printf("KB=%d %s M=%3d N=%3d A_%s err=%s: %.3f ms, %.1f TFLOP/s, cycles per 64-k-block %.1f (tensor floor %d)\n",
+         KB, PAIR ? "cta_group::2" : "cta_group::1", M, N, AMN ? "MN" : "K ", cudaGetErrorString(err), ms,
+         flops / ms / 1e9, (double)mx / iters / KB, floor);
   cudaFree(d);
 }
 
 int main() {
-  const int it = 20000;
-  run<256, 0>(148, it); run<128, 0>(148, it); run<112, 0>(148, it); run<96, 0>(148, it);
-  run<80, 0>(148, it); run<64, 0>(148, it); run<48, 0>(148, it);
-  run<256, 1>(148, it); run<128, 1>(148, it); run<96, 1>(148, it); run<64, 1>(148, it);
+  const int it = 10000;
+  // KB = 2: 8 MMAs per commit, as the pair kernel issues them (two 64-wide k-blocks per stage)
+  run<256, 0, 256, 1, 2>(148, it); run<240, 0, 256, 1, 2>(148, it); run<224, 0, 256, 1, 2>(148, it);
+  run<208, 0, 256, 1, 2>(148, it); run<192, 0, 256, 1, 2>(148, it); run<160, 0, 256, 1, 2>(148, it);
+  run<128, 0, 256, 1, 2>(148, it);
+  run<224, 1, 256, 1, 2>(148, it); run<128, 1, 256, 1, 2>(148, it);
+  // narrow N with many MMAs per commit (design B's shapes: N = 64..96)
+  run<256, 0, 256, 1, 4>(148, it); run<128, 0, 256, 1, 4>(148, it); run<96, 0, 256, 1, 4>(148, it);
+  run<64, 0, 256, 1, 4>(148, it);
   return 0;
 }
