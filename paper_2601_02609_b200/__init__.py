@@ -38,6 +38,7 @@ FLAG_ACCUMULATE = 128
 FLAG_EXTERNAL_COMBINE = 256
 FLAG_DH_SEQ_SHARD = 512
 FLAG_P2P_COMBINE = 1024
+FLAG_DESIGN_B = 2048
 REDUCTION_MEAN, REDUCTION_SUM, REDUCTION_NONE = 0, 1, 2
 _REDUCTIONS = {"mean": REDUCTION_MEAN, "sum": REDUCTION_SUM, "none": REDUCTION_NONE}
 

@@ -16,6 +16,7 @@
 #include "../../include/cce.h"
 #include "cce_aux.cuh"
 #include "cce_common.cuh"
+#include "cce_designb.cuh"
 #include "cce_p2p.cuh"
 #include "cce_pair.cuh"
 
@@ -240,10 +241,13 @@ struct Layout {
   int64_t Npad, Tv, C;
   int64_t n_chunks, sched_ints;
   size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, dloss_c, gbuf,
-      dH32, sched, rstd_c, gpart, dHo, p2p_flags, p2p_ready, p2p_done, dHred, total;
+      dH32, sched, rstd_c, gpart, dHo, p2p_flags, p2p_ready, p2p_done, dHred, b_opart, b_spart, b_U, total;
+  int64_t b_maxseg;  // CCE_FLAG_DESIGN_B: partial slots per CTA
   int64_t p2p_tmax;  // dH tiles the P2P flag arrays hold: ceil(D/256) x Npad/256
   int64_t seq_slice;  // CCE_FLAG_DH_SEQ_SHARD: rows per rank of the original-order dH (0 otherwise)
 };
+
+constexpr int DSB_GRID = 148;  // design-B kernel: one CTA per SM (partial slots are laid out for this grid)
 
 Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, int slots, uint32_t flags = 0) {
   const bool seq = (flags & CCE_FLAG_DH_SEQ_SHARD) != 0;
@@ -300,6 +304,13 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
   // CCE_FLAG_DH_SEQ_SHARD: this rank's partial dH in original row order, world x slice rows
   L.seq_slice = seq ? (N + world - 1) / world : 0;
   L.dHo = take(seq ? (size_t)world * L.seq_slice * D * 4 : 0);
+  // CCE_FLAG_DESIGN_B: per-CTA O' / (m, d_nt, z_y) partials of the forward, U [Npad][D] fp32
+  const bool db = (flags & CCE_FLAG_DESIGN_B) != 0;
+  const int64_t btiles = (L.Npad + dsb::NX - 1) / dsb::NX;
+  L.b_maxseg = db ? (btiles + DSB_GRID - 1) / DSB_GRID + 2 : 0;
+  L.b_opart = take(db ? (size_t)DSB_GRID * L.b_maxseg * dsb::NX * D * 4 : 0);
+  L.b_spart = take(db ? (size_t)DSB_GRID * L.b_maxseg * dsb::NX * 16 : 0);
+  L.b_U = take(db ? (size_t)L.Npad * D * 4 : 0);
   L.total = o;
   return L;
 }
@@ -341,6 +352,20 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
       pairk::cce_pair_kernel<0, 1><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, x9, pp);
     else
       pairk::cce_pair_kernel<0, 0><<<grid, pairk::PTHREADS, pairk::PSMEM, s>>>(m0, m1, m2, m3, m4, m5, m6, x7, x8, x9, pp);
+  }
+  return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+}
+}  // namespace
+
+namespace {
+cce_status launch_designb(cce_handle* h, const CUtensorMap& tX, const CUtensorMap& tY1, const CUtensorMap& tY2,
+                          const dsb::Params& P, cudaStream_t s, int prof_class) {
+  if (cudaFuncSetAttribute(dsb::cce_designb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dsb::SMEM) !=
+      cudaSuccess)
+    return CCE_ERR_CUDA;
+  {
+    ProfScope ps(h, s, prof_class);
+    dsb::cce_designb_kernel<<<DSB_GRID, dsb::THREADS, dsb::SMEM, s>>>(tX, tY1, tY2, P);
   }
   return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
@@ -394,8 +419,13 @@ cce_status cce_create(cce_handle** out, const cce_config* cfg) {
        (cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD))))
     return CCE_ERR_UNSUPPORTED;
   const uint32_t known = CCE_FLAG_GRAD_FP32 | CCE_FLAG_ACCUMULATE | CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD |
-                         CCE_FLAG_P2P_COMBINE;
+                         CCE_FLAG_P2P_COMBINE | CCE_FLAG_DESIGN_B;
   if (cfg->flags & ~known) return CCE_ERR_INVALID_VALUE;
+  // design B: one unsharded GPU, the plain cross-entropy (its U is the dH of exactly that loss)
+  if ((cfg->flags & CCE_FLAG_DESIGN_B) &&
+      (cfg->world != 1 || cfg->nccl_comm || cfg->label_smoothing != 0.f || cfg->z_loss != 0.f ||
+       (cfg->flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_DH_SEQ_SHARD | CCE_FLAG_P2P_COMBINE))))
+    return CCE_ERR_UNSUPPORTED;
   if (cfg->vocab_total > 0x7fffffffLL) return CCE_ERR_UNSUPPORTED;
   if (!(cfg->label_smoothing >= 0.f && cfg->label_smoothing < 1.f) || !(cfg->z_loss >= 0.f && cfg->z_loss < 1e30f))
     return CCE_ERR_INVALID_VALUE;
@@ -556,8 +586,41 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
           at<__nv_bfloat16>(ws, L.Hc)); }
   }
 
+  const bool dB = (h->cfg.flags & CCE_FLAG_DESIGN_B) != 0;
+  if (dB && D > dsb::D_MAX) return CCE_ERR_UNSUPPORTED;
+  float4* stats = at<float4>(ws, L.stats);
+  if (dB) {
+    // design B (rows a1-a4 with a3): logits, online softmax and the dH numerator O' in one
+    // kernel, then the merge of the per-CTA partials into (m, d, z_y) and U
+    if (N > 0 && V_local > 0) {
+      CUtensorMap tX, tY1, tY2;
+      if (!make_map_colblocks(&tX, at<void>(ws, L.Hc), D, L.Npad, D, dsb::NX, (uint32_t)(D / 64)) ||
+          !make_map_colblocks(&tY1, W, D, V_local, ldw, dsb::YM, 1) ||
+          !make_map_colblocks(&tY2, W, D, V_local, ldw, 64, 2))
+        return CCE_ERR_CUDA;
+      dsb::Params bp{};
+      bp.mode = 0;
+      bp.D = (int)D; bp.V_local = (int)V_local; bp.vocab_offset = (int)h->cfg.vocab_offset; bp.Npad = (int)L.Npad;
+      bp.n_valid = nvp;
+      bp.labels_c = at<int>(ws, L.labels_c);
+      bp.maxseg = (int)L.b_maxseg;
+      bp.opart = at<float>(ws, L.b_opart);
+      bp.spart = at<float4>(ws, L.b_spart);
+      cce_status st = launch_designb(h, tX, tY1, tY2, bp, s, 0);
+      if (st != CCE_OK) return st;
+    }
+    if (N > 0) {
+      ProfScope ps(h, s, 4);
+      if (V_local > 0) {
+        dsb::k_merge_designb<<<(unsigned)((L.Npad + 7) / 8), 256, 0, s>>>(
+            at<float>(ws, L.b_opart), at<float4>(ws, L.b_spart), (int)L.b_maxseg, DSB_GRID, (int)V_local,
+            (int)h->cfg.vocab_offset, (int)D, nvp, at<int>(ws, L.labels_c), static_cast<const __nv_bfloat16*>(W), ldw,
+            stats, at<float>(ws, L.b_U));
+      }
+    }
+  }
   // a1 + a2: tcgen05 logit tiles with the online-softmax epilogue
-  if (N > 0 && V_local > 0) {
+  if (!dB && N > 0 && V_local > 0) {
     GemmParams p{};
     p.D = (int)D;
     p.V_local = (int)V_local;
@@ -590,8 +653,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   }
 
   // a4: merge tiles -> per-rank stats; a9: allgather across vocabulary shards
-  float4* stats = at<float4>(ws, L.stats);
-  if (N > 0) {
+  if (!dB && N > 0) {
     // an empty shard (V_local == 0) merges zero tiles: (m=-inf, d=0, z_y=0) for every row
     ProfScope ps(h, s, 4);
     StatsPush push{};
@@ -782,7 +844,41 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
   int* nvp = at<int>(ws, L.scal);
   float* dH32 = at<float>(ws, L.dH32);
 
-  if (V_local > 0 && N > 0) {
+  const bool dB = (h->cfg.flags & CCE_FLAG_DESIGN_B) != 0;
+  if (dB && opt) return CCE_ERR_UNSUPPORTED;
+  if (dB && V_local > 0 && N > 0) {
+    // design B backward (rows a5-a7 with a6 on chip): S recompute, G in shared memory, dW;
+    // dH = s U (the forward's numerator), scaled into dH32 for the common tail below
+    const float* dloss_c = nullptr;
+    if (h->cfg.reduction == CCE_REDUCTION_NONE) {
+      ProfScope ps(h, s, 4);
+      k_gather_dloss<<<grid_for(L.Npad, 256, 2 * h->num_sms), 256, 0, s>>>(dloss, at<int>(ws, L.idx), nvp,
+                                                                           (int)L.Npad, at<float>(ws, L.dloss_c));
+      dloss_c = at<float>(ws, L.dloss_c);
+    }
+    void* Hc = at<void>(ws, L.Hc);
+    CUtensorMap tX, tY1, tY2;
+    if (!make_map_colblocks(&tX, h->W, D, V_local, h->ldw, dsb::NX, (uint32_t)(D / 64)) ||
+        !make_map_colblocks(&tY1, Hc, D, L.Npad, D, dsb::YM, 1) || !make_map_colblocks(&tY2, Hc, D, L.Npad, D, 64, 2))
+      return CCE_ERR_CUDA;
+    dsb::Params bp{};
+    bp.mode = 1;
+    bp.D = (int)D; bp.V_local = (int)V_local; bp.vocab_offset = (int)h->cfg.vocab_offset; bp.Npad = (int)L.Npad;
+    bp.n_valid = nvp;
+    bp.labels_c = at<int>(ws, L.labels_c);
+    bp.lse_c = at<float>(ws, L.lse_c);
+    bp.dloss = dloss;
+    bp.dloss_c = dloss_c;
+    bp.reduction = h->cfg.reduction;
+    bp.dW = dW;
+    bp.dw_fp32 = (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0;
+    bp.dw_accumulate = (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0;
+    cce_status st = launch_designb(h, tX, tY1, tY2, bp, s, 1);
+    if (st != CCE_OK) return st;
+    ProfScope ps(h, s, 4);
+    dsb::k_scale_rows<<<grid_for(L.Npad * D, 256, 8 * h->num_sms), 256, 0, s>>>(
+        at<float>(ws, L.b_U), dH32, (int)D, nvp, dloss, dloss_c, h->cfg.reduction);
+  } else if (V_local > 0 && N > 0) {
     void* Hc = at<void>(ws, L.Hc);
     void* G = at<void>(ws, L.gbuf);
     GemmParams p{};
