@@ -242,7 +242,7 @@ struct Layout {
   int64_t n_chunks, sched_ints;
   size_t scal, pos, idx, labels_c, Hc, part, zs_part, zy_c, stats, stats_all, lse_c, loss_rows, dloss_c, gbuf,
       dH32, sched, rstd_c, gpart, dHo, p2p_flags, p2p_ready, p2p_done, dHred, b_opart, b_spart, b_U, total;
-  int64_t b_maxseg;  // CCE_FLAG_DESIGN_B: partial slots per CTA
+  int64_t b_maxseg;  // CCE_FLAG_DESIGN_B: forward partial slots (units k tiles + t)
   int64_t p2p_tmax;  // dH tiles the P2P flag arrays hold: ceil(D/256) x Npad/256
   int64_t seq_slice;  // CCE_FLAG_DH_SEQ_SHARD: rows per rank of the original-order dH (0 otherwise)
 };
@@ -307,9 +307,9 @@ Layout layout(int64_t N, int64_t D, int64_t V_local, int world, int64_t chunk, i
   // CCE_FLAG_DESIGN_B: per-CTA O' / (m, d_nt, z_y) partials of the forward, U [Npad][D] fp32
   const bool db = (flags & CCE_FLAG_DESIGN_B) != 0;
   const int64_t btiles = (L.Npad + dsb::NX - 1) / dsb::NX;
-  L.b_maxseg = db ? (btiles + DSB_GRID - 1) / DSB_GRID + 2 : 0;
-  L.b_opart = take(db ? (size_t)DSB_GRID * L.b_maxseg * dsb::NX * D * 4 : 0);
-  L.b_spart = take(db ? (size_t)DSB_GRID * L.b_maxseg * dsb::NX * 16 : 0);
+  L.b_maxseg = db ? dsb::fwd_slots_max(btiles, DSB_GRID) : 0;  // forward partial slots
+  L.b_opart = take(db ? (size_t)L.b_maxseg * dsb::NX * D * 4 : 0);
+  L.b_spart = take(db ? (size_t)L.b_maxseg * dsb::NX * 16 : 0);
   L.b_U = take(db ? (size_t)L.Npad * D * 4 : 0);
   L.total = o;
   return L;
@@ -603,7 +603,6 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
       bp.D = (int)D; bp.V_local = (int)V_local; bp.vocab_offset = (int)h->cfg.vocab_offset; bp.Npad = (int)L.Npad;
       bp.n_valid = nvp;
       bp.labels_c = at<int>(ws, L.labels_c);
-      bp.maxseg = (int)L.b_maxseg;
       bp.opart = at<float>(ws, L.b_opart);
       bp.spart = at<float4>(ws, L.b_spart);
       cce_status st = launch_designb(h, tX, tY1, tY2, bp, s, 0);
@@ -613,7 +612,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
       ProfScope ps(h, s, 4);
       if (V_local > 0) {
         dsb::k_merge_designb<<<(unsigned)((L.Npad + 7) / 8), 256, 0, s>>>(
-            at<float>(ws, L.b_opart), at<float4>(ws, L.b_spart), (int)L.b_maxseg, DSB_GRID, (int)V_local,
+            at<float>(ws, L.b_opart), at<float4>(ws, L.b_spart), DSB_GRID, (int)V_local,
             (int)h->cfg.vocab_offset, (int)D, nvp, at<int>(ws, L.labels_c), static_cast<const __nv_bfloat16*>(W), ldw,
             stats, at<float>(ws, L.b_U));
       }

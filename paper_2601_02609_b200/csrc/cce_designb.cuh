@@ -57,9 +57,8 @@ struct Params {
   int D, V_local, vocab_offset, Npad;
   const int* n_valid;
   const int* labels_c;
-  int maxseg;          // forward: partial slots per CTA
-  float* opart;        // forward: [grid][maxseg][NX][D] fp32 O' partials
-  float4* spart;       // forward: [grid][maxseg][NX] (m natural, d_nt, z_y, -)
+  float* opart;        // forward: [unit][NX][D] fp32 O' partials (unit = k tiles + t)
+  float4* spart;       // forward: [unit][NX] (m natural, d_nt, z_y, -)
   // backward
   const float* lse_c;
   const float* dloss;  // device scalar
@@ -69,8 +68,29 @@ struct Params {
   int dw_fp32, dw_accumulate;
 };
 
-// forward work split: W = tiles x ns steps over gridDim.x CTAs, contiguous ranges
-__host__ __device__ __forceinline__ long long range_lo(long long W, int p, int P) { return W * p / P; }
+// Forward work split: every token tile's vocabulary sweep is cut into K segments of L steps;
+// units u = k * tiles + t are handed out round-robin (CTA p: u = p, p + G, ...), so in any
+// round the CTAs work on one or two vocabulary segments together and read W through the L2
+// (a contiguous per-CTA split scattered the CTAs over the whole vocabulary: 28.8 GB of DRAM
+// reads per forward, ncu).  K balances the rounds: the smallest K with the best
+// units / (rounds x G) ratio among K tiles <= 6 G.
+constexpr int MAX_ROUNDS = 6;
+__host__ __device__ __forceinline__ int fwd_splits(int tiles, int ns, int G) {
+  if (tiles <= 0) return 1;
+  int best = 1;
+  float best_eff = -1.f;
+  for (int k = 1; k <= ns && (long long)k * tiles <= (long long)MAX_ROUNDS * G; ++k) {
+    const int u = k * tiles;
+    const int rounds = (u + G - 1) / G;
+    const float eff = (float)u / (float)(rounds * G);
+    if (eff > best_eff + 1e-3f) { best_eff = eff; best = k; }
+  }
+  return best;
+}
+// forward partial slots the workspace must hold for up to `tiles_max` token tiles
+__host__ __forceinline__ long long fwd_slots_max(long long tiles_max, int G) {
+  return (long long)MAX_ROUNDS * G + tiles_max;
+}
 
 __device__ __forceinline__ int fkey(float f) {  // order-preserving float -> int
   const int i = __float_as_int(f);
@@ -127,32 +147,32 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;   // S: columns [0, 64); O' / dW^T block b: [64 + 64 b, 128 + 64 b)
 
   // ---- the unit sequence (identical in every role) ----
-  // forward: this CTA's contiguous range of the (tile, step) work; a unit is one tile's part
+  // forward: units u = k * tiles + t (segment k of token tile t), round-robin over the CTAs
   const int ns_f = (P.V_local + YM - 1) / YM;
   const int tiles = (nv + NX - 1) / NX;
-  const long long Wf = (long long)tiles * ns_f;
-  const long long lo = P.mode == 0 ? range_lo(Wf, blockIdx.x, gridDim.x) : 0;
-  const long long hi = P.mode == 0 ? range_lo(Wf, blockIdx.x + 1, gridDim.x) : 0;
+  const int Kf = fwd_splits(tiles, ns_f, gridDim.x);
+  const int Lf = (ns_f + Kf - 1) / Kf;
+  const int uf = tiles * Kf;
   // backward: vocabulary tiles u = blockIdx.x, blockIdx.x + grid, ...; steps over the valid rows
   const int n_vt = (P.V_local + NX - 1) / NX;
   const int ns_b = (nv + YM - 1) / YM;
-  int n_units;
-  if (P.mode == 0) n_units = hi > lo ? (int)((hi - 1) / ns_f - lo / ns_f + 1) : 0;
-  else n_units = n_vt > (int)blockIdx.x ? (n_vt - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int n_all = P.mode == 0 ? uf : n_vt;
+  const int n_units = n_all > (int)blockIdx.x ? (n_all - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   // backward with no valid rows: no pipeline; the epilogue writes dW = 0 (kept when accumulating)
   const bool empty_bwd = P.mode == 1 && ns_b == 0;
   const int n_pipe = empty_bwd ? 0 : n_units;
-  // unit u: stationary rows x0 (token tile / vocabulary tile), steps [s0, s1) (step s covers
-  // streamed rows [s YM, s YM + YM))
-  auto unit = [&](int u, int& x0, int& s0, int& s1) {
+  // unit i of this CTA (global unit u = blockIdx.x + i G): stationary rows x0 (token tile /
+  // vocabulary tile), steps [s0, s1) (step s covers streamed rows [s YM, s YM + YM)); a forward
+  // segment past the vocabulary (K L > ns) is empty and skipped by every role
+  auto unit = [&](int i, int& x0, int& s0, int& s1) {
+    const int u = (int)blockIdx.x + i * (int)gridDim.x;
     if (P.mode == 0) {
-      const int t = (int)(lo / ns_f) + u;
+      const int t = u % tiles, k = u / tiles;
       x0 = t * NX;
-      const long long a = max(lo, (long long)t * ns_f), b = min(hi, (long long)(t + 1) * ns_f);
-      s0 = (int)(a - (long long)t * ns_f);
-      s1 = (int)(b - (long long)t * ns_f);
+      s0 = min(k * Lf, ns_f);
+      s1 = min(s0 + Lf, ns_f);
     } else {
-      x0 = ((int)blockIdx.x + u * (int)gridDim.x) * NX;
+      x0 = u * NX;
       s0 = 0;
       s1 = ns_b;
     }
@@ -168,10 +188,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_3d(m, &full[st], sR + st * STG, 0, c1, c2);
         if (++st == NSTG) { st = 0; ph ^= 1; }
       };
+      int xu = 0;   // units loaded so far
       for (int u = 0; u < n_pipe; ++u) {
         int x0, s0, s1;
         unit(u, x0, s0, s1);
-        if (u > 0) mbar_wait(x_empty, (u - 1) & 1);
+        if (s1 == s0) continue;
+        if (xu > 0) mbar_wait(x_empty, (xu - 1) & 1);
+        ++xu;
         mbar_arrive_expect_tx(x_full, NX * D * 2);
         tma_load_3d(&tmX, x_full, sX, 0, x0, 0);
         for (int j = s0; j <= s1; ++j) {
@@ -190,10 +213,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t idesc1 = idesc_bf16_f32(128, NX, 0, 0);   // A K-major (Y), B K-major (X)
     const uint32_t idesc2 = idesc_bf16_f32(128, NX, 1, 1);   // A MN-major (Y^T), B MN-major (B2)
     const uint32_t xa = smem_u32(sX), ra = smem_u32(sR), b2a = smem_u32(sB2);
+    int xu = 0;
     for (int u = 0; u < n_pipe; ++u) {
       int x0, s0, s1;
       unit(u, x0, s0, s1);
-      mbar_wait(x_full, u & 1);
+      if (s1 == s0) continue;
+      const int uu = xu++;
+      mbar_wait(x_full, uu & 1);
       for (int j = s0; j <= s1; ++j) {
         if (j < s1) {
           mbar_wait(s_empty, (g1 & 1) ^ 1);   // the epilogue has read S of the previous step
@@ -220,7 +246,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (j > s0) {
           const int bb = g2 & 1;
           mbar_wait(&b2_full[bb], (g2 >> 1) & 1);
-          if (j - 1 == s0) mbar_wait(a2_empty, (u & 1) ^ 1);   // previous unit's accumulator drained
+          if (j - 1 == s0) mbar_wait(a2_empty, (uu & 1) ^ 1);   // previous unit's accumulator drained
           tc_fence_after();
           for (int b = 0; b < nb; ++b) {
             for (int kh = 0; kh < 2; ++kh) {
@@ -260,7 +286,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (P.mode == 1 && nv > 0 && P.reduction != 2) scale_all = P.reduction == 1 ? *P.dloss : (*P.dloss) / (float)nv;
     if (empty_bwd && !P.dw_accumulate) {
       for (int u = 0; u < n_units; ++u) {
-        const int x0 = ((int)blockIdx.x + u * (int)gridDim.x) * NX;
+        int x0, s0, s1;
+        unit(u, x0, s0, s1);
         for (int i = threadIdx.x - 128; i < NX * D; i += ebar_n) {
           const int v = x0 + i / D;
           if (v >= P.V_local) break;
@@ -269,9 +296,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    int xu = 0;
     for (int u = 0; u < n_pipe; ++u) {
       int x0, s0, s1;
       unit(u, x0, s0, s1);
+      if (s1 == s0) continue;
+      const int uu = xu++;
       float dpart[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) dpart[c] = 0.f;
@@ -286,7 +316,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         named_bar_sync(1, ebar_n);
       }
-      const int slot = blockIdx.x * P.maxseg + u;
+      const int slot = (int)blockIdx.x + u * (int)gridDim.x;   // the global unit index
       for (int j = s0; j < s1; ++j) {
         mbar_wait(s_full, g1 & 1);
         tc_fence_after();
@@ -402,7 +432,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         ++g2;
       }
       // ---- unit end: drain the O' / dW^T accumulator
-      mbar_wait(a2_full, u & 1);
+      mbar_wait(a2_full, uu & 1);
       tc_fence_after();
       if (P.mode == 0) {
         // per-token d_nt of this CTA: warp sums, then the 4 quarters in order
@@ -481,12 +511,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, TMEM_COLS);
 }
 
-// a4 for design B: one warp per valid row; the row's partials in CTA order (fixed ->
-// deterministic), the online-softmax merge of (m, d_nt, O'), then
+// a4 for design B: one warp per valid row; the row's K partials (units k tiles + t) in
+// segment order (fixed -> deterministic), the online-softmax merge of
+// (m, d_nt, O'), then
 //   stats = (m_f, d, z_y, 0) with d = d_nt e^{m - m_f} + e^{z_y - m_f}   (forward_tail's input)
-//   U     = (O' e^{m - m_f} - d_nt e^{m - m_f} W_y) / d                    (written over dH32)
+//   U     = (O' e^{m - m_f} - d_nt e^{m - m_f} W_y) / d
 __global__ void __launch_bounds__(256) k_merge_designb(const float* __restrict__ opart, const float4* __restrict__ spart,
-                                                       int maxseg, int grid, int V_local, int vocab_offset, int D,
+                                                       int grid, int V_local, int vocab_offset, int D,
                                                        const int* __restrict__ n_valid,
                                                        const int* __restrict__ labels_c,
                                                        const __nv_bfloat16* __restrict__ W, long long ldw,
@@ -497,35 +528,27 @@ __global__ void __launch_bounds__(256) k_merge_designb(const float* __restrict__
   if (row >= nv) return;
   const int ns = (V_local + YM - 1) / YM;
   const int tiles = (nv + NX - 1) / NX;
-  const long long Wf = (long long)tiles * ns;
+  const int K = fwd_splits(tiles, ns, grid);
+  const int L = (ns + K - 1) / K;
   const int t = row / NX, col = row % NX;
   const int yl = labels_c[row] - vocab_offset;
   // pass 1: the partials' maxima; the target's logit from the segment covering its row
   float m = -INFINITY, zy = 0.f;
   bool have_y = false;
-  for (int p = 0; p < grid; ++p) {
-    const long long lo = range_lo(Wf, p, grid), hi = range_lo(Wf, p + 1, grid);
-    const long long a = max(lo, (long long)t * ns), b = min(hi, (long long)(t + 1) * ns);
-    if (a >= b) continue;
-    const int k = t - (int)(lo / ns);
-    const float4 sp = spart[((size_t)p * maxseg + k) * NX + col];
+  for (int k = 0; k < K && k * L < ns; ++k) {
+    const float4 sp = spart[((size_t)k * tiles + t) * NX + col];
     m = fmaxf(m, sp.x);
-    const long long v0 = (a - (long long)t * ns) * YM, v1 = (b - (long long)t * ns) * YM;
-    if (yl >= v0 && yl < v1) { zy = sp.z; have_y = true; }
+    if (yl >= k * L * YM && yl < min((k + 1) * L, ns) * YM) { zy = sp.z; have_y = true; }
   }
   const float mf = have_y ? fmaxf(m, zy) : m;
-  // pass 2: d_nt and O' in CTA order
+  // pass 2: d_nt and O' in segment order
   constexpr int PER = D_MAX / 32;  // hidden elements per lane
   float o[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) o[i] = 0.f;
   float dn = 0.f;
-  for (int p = 0; p < grid; ++p) {
-    const long long lo = range_lo(Wf, p, grid), hi = range_lo(Wf, p + 1, grid);
-    const long long a = max(lo, (long long)t * ns), b = min(hi, (long long)(t + 1) * ns);
-    if (a >= b) continue;
-    const int k = t - (int)(lo / ns);
-    const size_t s = (size_t)p * maxseg + k;
+  for (int k = 0; k < K && k * L < ns; ++k) {
+    const size_t s = (size_t)k * tiles + t;
     const float4 sp = spart[s * NX + col];
     if (sp.x == -INFINITY) continue;   // only masked / target entries in this segment
     const float f = __expf(sp.x - mf);
