@@ -238,8 +238,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="extra cce_config.flags bits (e.g. 64 = float32 gradients)")
-    ap.add_argument("--combine", default="nccl", choices=["nccl", "p2p"],
-                    help="N > 1: the sharded exchange through NCCL or over peer memory (CCE_FLAG_P2P_COMBINE)")
+    ap.add_argument("--combine", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N > 1: the sharded exchange over peer memory fused into the kernels (CCE_FLAG_P2P_COMBINE; "
+                         "'auto' when every GPU pair has peer access) or through NCCL")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -285,6 +286,12 @@ def main():
     y = torch.from_numpy(p["labels"]).to(dev)
 
     comm = None
+    if args.combine == "auto":
+        n_dev = torch.cuda.device_count()
+        peers = world > 1 and not one_gpu and all(
+            torch.cuda.can_device_access_peer(a, b) for a in range(min(world, n_dev)) for b in range(min(world, n_dev))
+            if a != b)
+        args.combine = "p2p" if (peers or one_gpu) else "nccl"
     p2p = world > 1 and args.combine == "p2p"
     if world > 1 and not p2p:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)

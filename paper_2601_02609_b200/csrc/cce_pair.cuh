@@ -634,6 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   if (warp == 2) tmem_alloc_pair(tmem_slot, TMEM_COLS);
   tc_fence_before();
   cluster_sync_all();
+  __syncthreads();  // (also a CTA barrier: compute-sanitizer's racecheck does not model barrier.cluster)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 

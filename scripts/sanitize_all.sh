@@ -1,0 +1,20 @@
+#!/usr/bin/env bash
+# compute-sanitizer memcheck / racecheck / synccheck over the pair kernels (tiny config and a
+# 6-chunk problem), the design-B kernels, and the peer-memory path with 2 processes.
+# Run on the GPU box:  bash scripts/sanitize_all.sh  -> gpurun_out/sanitize_*.txt
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+CS=compute-sanitizer
+run() {  # name tool cmd...
+  local name=$1 tool=$2; shift 2
+  timeout 1500 $CS --tool $tool --error-exitcode 9 --print-limit 50 "$@" > gpurun_out/sanitize_${name}_${tool}.txt 2>&1
+  echo "${name} ${tool} rc=$?" | tee -a gpurun_out/sanitize_summary.txt
+}
+: > gpurun_out/sanitize_summary.txt
+for tool in memcheck racecheck synccheck; do
+  run tiny $tool python scripts/sanitize_case.py 64 64 1000
+  run chunks6 $tool python scripts/sanitize_case.py 1000 128 41000
+  run designb $tool python scripts/sanitize_case.py 300 256 3000 2048
+done
+# peer-memory exchange fused into the kernels: 2 processes sharing the GPU (tests/test_gpu_p2p.py)
+run p2p memcheck --target-processes all python -m pytest tests/test_gpu_p2p.py -x -q -k "between_processes and 2"

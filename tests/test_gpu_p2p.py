@@ -49,6 +49,20 @@ dist.all_gather_object(allh, mine)
 cce.cce_p2p_attach(h.h, ws, N, D, [a[0] for a in allh], [a[1] for a in allh])
 dist.barrier()
 one = torch.ones((), dtype=torch.float32, device=dev)
+if mode == "fwdonly":
+    # forward-only loop (evaluation): consecutive forwards with different labels and no
+    # backward in between -- the stats exchange must not let step e+1 overwrite what a peer
+    # still reads for step e (double-buffered by step parity)
+    losses = []
+    for step in range(4):
+        loss, lse, nv = h.forward(H, Wr, torch.roll(y, step))
+        losses.append(loss)
+    torch.cuda.synchronize()
+    np.savez(out, losses=np.array([l.item() for l in losses]), err=cce.cce_get_error(h.h))
+    dist.barrier()
+    h.close()
+    dist.destroy_process_group()
+    sys.exit(0)
 for step in range(0 if rank == absent else 2):
     dH = torch.empty_like(H)
     dW = torch.empty_like(Wr)
@@ -151,3 +165,14 @@ def test_p2p_exchange_with_regularised_loss_and_rmsnorm(tmp_path, mode):
     assert abs(float(res[0]["loss"]) - ref["loss"]) <= TOL_LOSS
     assert rel_fro(f(res[0]["dH"]), dref) <= TOL_GRAD
     assert rel_fro(np.concatenate([f(r["dW"]) for r in res]), ref["dW"]) <= TOL_GRAD
+
+
+def test_p2p_forward_only_loop(tmp_path):
+    """back-to-back forwards without a backward (evaluation loops) over peer memory."""
+    p = workload.make_problem(700, 128, 3000, seed=606, ignore="bern40")
+    res = _run(tmp_path, 2, mode="fwdonly")
+    for step in range(4):
+        ref = oracle.cce(p["H"], p["W"], np.roll(p["labels"], step))
+        for r in res:
+            assert int(r["err"]) == 0
+            assert abs(float(r["losses"][step]) - ref["loss"]) <= TOL_LOSS, (step, float(r["losses"][step]), ref["loss"])
