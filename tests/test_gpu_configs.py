@@ -10,7 +10,12 @@ of every shard's work).  The fp64 oracle cannot afford these problems whole, so 
 GPU's per-row LSE, target logit and dH rows are compared on sampled rows the oracle
 computes one by one (oracle.rows), and the properties that hold at any size are
 checked on the whole output (sum_v dW[v,:] = 0, P:254-258; finite non-zero grads;
-ignored / valid masks)."""
+ignored / valid masks).  With the committed oracle golden of the config (every valid row's
+fp64 LSE and target logit) the mean loss, every row's LSE and sampled dW rows are compared
+too."""
+import hashlib
+import os
+
 import numpy as np
 import pytest
 
@@ -49,7 +54,6 @@ def test_full_size_config(name):
     assert rel.max() <= TOL_LSE, rel.max()
     dH_g = dH[torch.from_numpy(pick).to(dev)].float().cpu().numpy().astype(np.float64)
     assert rel_fro(dH_g, dH_ref) <= TOL_GRAD
-    # the loss is the mean of the per-row (lse - z_y): bounded below by the sampled rows' spread
     l = float(loss.item())
     assert np.isfinite(l) and l > 0
     # properties on the whole output
@@ -57,6 +61,25 @@ def test_full_size_config(name):
     assert torch.isfinite(dWf).all() and dWf.abs().sum().item() > 0
     assert (dWf.double().sum(0).norm() <= 1e-2 * dWf.double().norm()).item()
     assert torch.isfinite(dH.float()).all()
+    # with the oracle golden (scripts/make_golden_configs.py: fp64 LSE and z_y of EVERY valid
+    # row, inputs hashed): every row's LSE, the mean loss, and sampled dW rows (each needs
+    # every row's LSE: dW[v] = s sum_n (exp(z_nv - lse_n) - 1[v = y_n]) h_n)
+    gpath = os.path.join(os.path.dirname(__file__), "golden", f"{name}_seed42.npz")
+    if os.path.exists(gpath):
+        g = np.load(gpath)
+        assert str(g["H_sha256"]) == hashlib.sha256(p["H"].tobytes()).hexdigest()
+        assert str(g["W_sha256"]) == hashlib.sha256(p["W"].tobytes()).hexdigest()
+        grows = g["valid_rows"].astype(np.int64)
+        assert np.array_equal(grows, rows)
+        relg = np.abs(lse_g[grows] - g["lse"]) / np.maximum(np.abs(g["lse"]), 1.0)
+        assert relg.max() <= TOL_LSE, relg.max()
+        assert abs(l - float(np.mean(g["lse"] - g["zy"]))) <= 2e-3
+        lse_full = np.zeros(N)
+        lse_full[grows] = g["lse"]
+        vr = np.unique(np.array([0, 1, 2, 100, V // 3, V // 2, V - 2, V - 1]))
+        dW_ref = oracle.dW_rows(p["H"], p["W"], p["labels"], lse_full, 1.0 / n_valid, vr)
+        dW_g = dW[torch.from_numpy(vr).to(dev)].double().cpu().numpy()
+        assert rel_fro(dW_g, dW_ref) <= TOL_GRAD, rel_fro(dW_g, dW_ref)
     h.close()
     del H, W, y, dH, dW, dWf
     torch.cuda.empty_cache()
