@@ -63,6 +63,10 @@ struct cce_handle {
   int64_t ldx = 0;
   const void* gamma = nullptr;
   int64_t launches = 0;
+  // NCCL backward: side stream for the dH all-reduce overlapping the last chunk's dW items
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  bool dH_reduced = false;  // this backward's all-reduce was already issued (split launch)
   void* trace = nullptr;  // cce_debug_trace: per-item records of the backward
   size_t trace_bytes = 0;
   void* fwd_trace = nullptr;  // ... and of the forward (second half of the buffer)
@@ -332,7 +336,7 @@ int grid_for(long long work, int threads, int cap) {
 cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                        const CUtensorMap& m3, const CUtensorMap& m4, const CUtensorMap& m5, const CUtensorMap& m6,
                        const pairk::PairParams& pp, cudaStream_t s, int prof_class, const CUtensorMap* m7 = nullptr,
-                       const CUtensorMap* m8 = nullptr, const CUtensorMap* m9 = nullptr) {
+                       const CUtensorMap* m8 = nullptr, const CUtensorMap* m9 = nullptr, int pairs = 0) {
   const CUtensorMap& x7 = m7 ? *m7 : m3;
   const CUtensorMap& x8 = m8 ? *m8 : m5;
   const CUtensorMap& x9 = m9 ? *m9 : m4;
@@ -343,7 +347,7 @@ cce_status launch_pair(cce_handle* h, const CUtensorMap& m0, const CUtensorMap& 
       cudaFuncSetAttribute(pairk::cce_pair_kernel<1, 0>, a, pairk::PSMEM) != cudaSuccess ||
       cudaFuncSetAttribute(pairk::cce_pair_kernel<0, 1>, a, pairk::PSMEM) != cudaSuccess)
     return CCE_ERR_CUDA;
-  const int grid = (h->num_sms / 2) * 2;  // whole CTA pairs
+  const int grid = pairs > 0 ? 2 * pairs : (h->num_sms / 2) * 2;  // whole CTA pairs
   {
     ProfScope ps(h, s, prof_class);
     if (pp.g.adamw)
@@ -451,6 +455,9 @@ cce_status cce_destroy(cce_handle* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : h->pool) cudaEventDestroy(e);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_a) cudaEventDestroy(h->ev_a);
+  if (h->ev_b) cudaEventDestroy(h->ev_b);
   for (auto& e : h->stages)
     if (e.consumed) cudaEventDestroy(e.consumed);
   if (h->ev_copied) cudaEventDestroy(h->ev_copied);
@@ -842,6 +849,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
   void* ws = h->ws;
   int* nvp = at<int>(ws, L.scal);
   float* dH32 = at<float>(ws, L.dH32);
+  h->dH_reduced = false;
 
   const bool dB = (h->cfg.flags & CCE_FLAG_DESIGN_B) != 0;
   if (dB && opt) return CCE_ERR_UNSUPPORTED;
@@ -961,8 +969,37 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       pp.dHred_off = L.dHred;
       pp.err = nvp + 1;
     }
-    cce_status st = launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, &mHcMN3, &mWMN3, &mGst);
-    if (st != CCE_OK) return st;
+    // NCCL dH all-reduce (a10) overlapped with the last chunk's dW items: the backward queue
+    // runs as two launches; after the first (every dH tile final) the all-reduce starts on a
+    // side stream while the second launch, on 8 fewer CTA pairs so NCCL's kernels find free
+    // SMs, finishes dW
+    const bool split = h->cfg.nccl_comm != nullptr && !(h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) && !norm;
+    cce_status st;
+    if (!split) {
+      st = launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, &mHcMN3, &mWMN3, &mGst);
+      if (st != CCE_OK) return st;
+    } else {
+      if (!h->side && (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+                       cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+                       cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming) != cudaSuccess))
+        return CCE_ERR_CUDA;
+      pp.part = 1;
+      st = launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, &mHcMN3, &mWMN3, &mGst);
+      if (st != CCE_OK) return st;
+      if (cudaEventRecord(h->ev_a, s) != cudaSuccess || cudaStreamWaitEvent(h->side, h->ev_a, 0) != cudaSuccess)
+        return CCE_ERR_CUDA;
+      Nccl& n = nccl();
+      if (!n.ok) return CCE_ERR_NCCL;
+      if (n.allreduce(dH32, dH32, (size_t)L.Npad * D, kNcclFloat32, kNcclSum, h->cfg.nccl_comm, h->side) != 0)
+        return CCE_ERR_NCCL;
+      if (cudaEventRecord(h->ev_b, h->side) != cudaSuccess) return CCE_ERR_CUDA;
+      pp.part = 2;
+      st = launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, &mHcMN3, &mWMN3, &mGst,
+                       std::max(1, h->num_sms / 2 - 8));
+      if (st != CCE_OK) return st;
+      if (cudaStreamWaitEvent(s, h->ev_b, 0) != cudaSuccess) return CCE_ERR_CUDA;
+      h->dH_reduced = true;
+    }
   } else if (V_local > 0 && N == 0 && opt) {
     // no rows: zero gradient, the optimizer step still applies (decay, moment decay)
     if (h->ldw != D) return CCE_ERR_UNSUPPORTED;
@@ -1005,7 +1042,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
       k_p2p_wait_tiles<<<1, 256, 0, s>>>(at<int>(ws, L.p2p_done), nvp, (int)D, h->epoch, nvp + 1);
       dH32 = at<float>(ws, L.dHred);
     }
-    if (h->cfg.nccl_comm) {
+    if (h->cfg.nccl_comm && !h->dH_reduced) {
       // a10: dH partials summed over the vocabulary shards (all-reduce), or reduce-scattered
       // by sequence slice (CCE_FLAG_DH_SEQ_SHARD; in place: rank r's slice at r x slice rows)
       Nccl& n = nccl();

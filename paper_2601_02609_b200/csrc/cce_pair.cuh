@@ -77,6 +77,9 @@ struct PairParams {
   GemmParams g;
   int mode;        // 0 = forward queue, 1 = backward queue
   int n_chunks;
+  int part;        // backward: 0 the whole queue; 1 every item but the last chunk's DW items;
+                   // 2 only those (the NCCL dH all-reduce runs between the two launches, on a
+                   // side stream, overlapping part 2)
   int slots;       // Gbuf ring slots
   int lookahead;   // backward queue: G of chunk block b + lookahead is queued before W of block b
   int qblock;      // chunks per block of the backward queue ((lookahead + 1) * qblock <= slots)
@@ -91,7 +94,7 @@ struct PairParams {
   unsigned long long ready_off, done_off;    // int flag arrays in every workspace
   unsigned long long dH32_off, dHred_off;    // partial / reduced dH in every workspace
   int* err;                                  // error word (bit 2: a peer never signalled)
-  int* sched;      // zeroed: [0] head [1] done | g_done[n] | w_done[n] | dh_flag[n_dt * t256]
+  int* sched;      // zeroed: [0] head [1] head of part 2 | g_done[n] | w_done[n] | dh_flag[n_dt * t256]
   TraceRec* trace;
   int trace_cap;
 };
@@ -610,7 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   int* head = P.sched;
-  int* done_total = P.sched + 1;
+  int* head2 = P.sched + 1;
   int* g_done = P.sched + 2;
   int* w_done = P.sched + 2 + P.n_chunks;
   int* dh_flag = P.sched + 2 + 2 * P.n_chunks;
@@ -650,9 +653,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       // ===== scheduler (leader): dequeue items and publish them into both CTAs' rings,
       // up to PRING items ahead of the consumers (hides the atomic and DSMEM latency).
       uint32_t rs = 0, rph = 0;
+      // split backward (NCCL): the last chunk's DW items are the queue's last p_n_dw items
+      int q_split = 0;
+      if (P.part != 0) {
+        int total = 0;
+        for (int c = 0; c < P.n_chunks; ++c) {
+          const int w = p_chunk_width(g, c);
+          total += p_n_g(k, w) + k.n_dh + p_n_dw(k, w);
+        }
+        q_split = total - p_n_dw(k, p_chunk_width(g, P.n_chunks - 1));
+      }
       while (true) {
-        const int q = atomicAdd(head, 1);
+        const int q = P.part == 2 ? q_split + atomicAdd(head2, 1) : atomicAdd(head, 1);
         PItem it = decode(P, k, q);
+        if (P.part == 1 && q >= q_split) it = make_item(PT_END, 0, 0, 0, 0, 0, 0, q);
         if (P.trace) it.t_deq = gtimer();
         mbar_wait(&rempty_l[rs], rph ^ 1);
         mbar_wait(&rempty_p[rs], rph ^ 1);
@@ -889,7 +903,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
             }
             atomicAdd(&w_done[it.c], 1);
           }
-          atomicAdd(done_total, 1);
         }
       }
     }
