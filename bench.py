@@ -455,7 +455,8 @@ def main():
                "sync_value": sync_value,
                "note": "cce_step_host_async: per step pinned H + labels H2D on a copy stream (double-buffered "
                        "staging, overlapping the previous step's compute), fwd+bwd, loss D2H to pinned memory; "
-                       "wall clock around all steps + final sync; W resident (a parameter).  sync_value: "
+                       "wall clock around all steps + final sync; W resident (a parameter); dH / dW stay on the "
+                       "device, as a training step keeps them.  sync_value: "
                        "cce_step_host, one synchronised step at a time"}
 
     cpu = None
