@@ -2,11 +2,11 @@
 """A/B timing of kernel variants on the bench workload, interleaved in one process
 so that box-to-box and clock drift affect every variant alike.
 
-  python scripts/ab.py name=flags[:ENV=VAL,...] ... [--rounds 3] [--steps 20] [--config qwen05b]
+  python scripts/ab.py name=flags[@path/to/libcce.so] ... [--rounds 3] [--steps 20] [--config qwen05b]
 
-Each variant gets its own handle (env vars are applied while its handle makes its
-first launch, which is when the library reads them).  Prints per-variant median
-step / forward / backward times in ms.
+Each variant gets its own handle, optionally on another build of libcce.so (the library
+reads no environment: compile-time variants are separate builds).  Prints per-variant
+median step / forward / backward times in ms.
 """
 from __future__ import annotations
 

@@ -13,7 +13,7 @@ ref = oracle.cce(p["H"], p["W"], p["labels"])
 for trial in range(3):
     got = run_gpu(H, W, y, flags=flags)
     print("trial", trial, "loss", got["loss"], ref["loss"], "dH", rel_fro(got["dH"], ref["dH"]), "dW", rel_fro(got["dW"], ref["dW"]))
-    C = int(os.environ.get("CCE_CHUNK", "8192"))
+    C = 8192  # the library's backward chunk (compile-time CCE_CHUNK)
     for c0 in range(0, V, C):
         sl = slice(c0, min(V, c0 + C))
         print("   chunk", c0 // C, "dW relF", rel_fro(got["dW"][sl], ref["dW"][sl]))
