@@ -602,8 +602,8 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     if (N > 0 && V_local > 0) {
       CUtensorMap tX, tY1, tY2;
       if (!make_map_colblocks(&tX, at<void>(ws, L.Hc), D, L.Npad, D, dsb::NX, (uint32_t)(D / 64)) ||
-          !make_map_colblocks(&tY1, W, D, V_local, ldw, dsb::YM, 1) ||
-          !make_map_colblocks(&tY2, W, D, V_local, ldw, 64, 2))
+          !make_map_colblocks(&tY1, W, D, V_local, ldw, dsb::YM, 2) ||
+          !make_map_colblocks(&tY2, W, D, V_local, ldw, dsb::YM, 2))
         return CCE_ERR_CUDA;
       dsb::Params bp{};
       bp.mode = 0;
@@ -866,7 +866,7 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
     void* Hc = at<void>(ws, L.Hc);
     CUtensorMap tX, tY1, tY2;
     if (!make_map_colblocks(&tX, h->W, D, V_local, h->ldw, dsb::NX, (uint32_t)(D / 64)) ||
-        !make_map_colblocks(&tY1, Hc, D, L.Npad, D, dsb::YM, 1) || !make_map_colblocks(&tY2, Hc, D, L.Npad, D, 64, 2))
+        !make_map_colblocks(&tY1, Hc, D, L.Npad, D, dsb::YM, 2) || !make_map_colblocks(&tY2, Hc, D, L.Npad, D, dsb::YM, 2))
       return CCE_ERR_CUDA;
     dsb::Params bp{};
     bp.mode = 1;

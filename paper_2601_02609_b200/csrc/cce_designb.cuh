@@ -42,13 +42,18 @@ constexpr int NX = 64;                 // stationary rows per CTA (tokens / voca
 constexpr int YM = 128;                // streamed rows per step
 constexpr int NB_MAX = 7;              // D <= 896: 7 blocks of 128 hidden rows
 constexpr int D_MAX = NB_MAX * 128;
-constexpr int STG = 16384;             // ring stage: one 128 x 64 K-major k-block, or 128 d x 64 rows MN-major
-constexpr int NSTG = 4;
+// ring stage: 128 streamed rows x two 64-wide hidden blocks (32 KB, one 3-D TMA box): two
+// K-major k-blocks of GEMM1 or one 128-row hidden block of GEMM2 -- 8 MMAs per commit (a
+// commit per 4 MMAs cost ~145 cycles per MMA at N = 64, ~100 at 8; scripts/ubench_narrow_n.cu)
+constexpr int STG = 32768;
+constexpr int NSTG = 3;
 constexpr int XBYTES = NX * D_MAX * 2;         // 112 KB
-constexpr int B2BYTES = YM * NX * 2;           // 16 KB per buffer
+constexpr int B2BYTES = YM * NX * 2;           // 16 KB, single buffer (GEMM2_{j-1} reads it
+                                               // while GEMM1_{j+1} runs; P'_j is written after)
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
-constexpr int SMEM = XBYTES + 2 * B2BYTES + NSTG * STG + 1024 /*align*/ + 2048 /*barriers, scratch*/;
+constexpr int SCRATCH = 128 /*barriers*/ + 3 * 64 * 4 /*m2, fsc, ytile*/ + 4 * 64 * 4 /*wmax / dsum*/;
+constexpr int SMEM = XBYTES + B2BYTES + NSTG * STG + SCRATCH + 1024 /*align*/;
 static_assert(SMEM <= 232448, "design-B shared memory");
 constexpr float THRESH = 16.f;         // log2 headroom before the reference max moves (P' <= 2^16)
 
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sX = smem;
   uint8_t* sB2 = smem + XBYTES;
-  uint8_t* sR = sB2 + 2 * B2BYTES;
+  uint8_t* sR = sB2 + B2BYTES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sR + NSTG * STG);
   uint64_t* full = bar;                 // [NSTG]
   uint64_t* empty = bar + NSTG;         // [NSTG]
@@ -113,21 +118,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* x_empty = x_full + 1;
   uint64_t* s_full = x_full + 2;
   uint64_t* s_empty = x_full + 3;
-  uint64_t* b2_full = x_full + 4;       // [2]
-  uint64_t* b2_empty = x_full + 6;      // [2]
-  uint64_t* a2_full = x_full + 8;
-  uint64_t* a2_empty = x_full + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 10);
-  float* m2 = reinterpret_cast<float*>(sR + NSTG * STG + 256);   // [NX] running reference (log2)
+  uint64_t* b2_full = x_full + 4;
+  uint64_t* b2_empty = x_full + 5;
+  uint64_t* a2_full = x_full + 6;
+  uint64_t* a2_empty = x_full + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 8);
+  float* m2 = reinterpret_cast<float*>(sR + NSTG * STG + 128);   // [NX] running reference (log2)
   float* fsc = m2 + NX;                 // [NX] rescale factors of the current step
   int* ytile = reinterpret_cast<int*>(fsc + NX);   // [NX] local target ids of the unit's tokens
-  int* wmax = ytile + NX;               // [4][NX] per-quarter column maxima (fkey)
-  float* dsum = reinterpret_cast<float*>(wmax + 4 * NX);  // [4][NX] per-quarter d_nt sums
+  int* wmax = ytile + NX;               // [4][NX] per-quarter column maxima (fkey), rescale path
+  float* dsum = reinterpret_cast<float*>(wmax);  // [4][NX] per-quarter d_nt sums, unit end (same space)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int D = P.D;
-  const int nkb = D / BK;               // k-blocks (GEMM1 stages)
+  const int nkb = D / BK;               // k-blocks of GEMM1 (two per stage)
+  const int ns1 = (nkb + 1) / 2;        // GEMM1 stages
   const int nb = (D + 127) / 128;       // hidden blocks of GEMM2 (2 stages each)
   const int nv = *P.n_valid;
 
@@ -136,7 +142,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < NSTG; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(x_full, 1); mbar_init(x_empty, 1);
     mbar_init(s_full, 1); mbar_init(s_empty, EPI_WARPS);
-    for (int b = 0; b < 2; ++b) { mbar_init(&b2_full[b], EPI_WARPS); mbar_init(&b2_empty[b], 1); }
+    mbar_init(b2_full, EPI_WARPS);
+    mbar_init(b2_empty, 1);
     mbar_init(a2_full, 1); mbar_init(a2_empty, EPI_WARPS);
     fence_barrier_init();
   }
@@ -199,10 +206,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_3d(&tmX, x_full, sX, 0, x0, 0);
         for (int j = s0; j <= s1; ++j) {
           if (j < s1)
-            for (int k = 0; k < nkb; ++k) ring(&tmY1, j * YM, k);                 // GEMM1_j
+            for (int k2 = 0; k2 < ns1; ++k2) ring(&tmY1, j * YM, 2 * k2);          // GEMM1_j: k-blocks 2 k2, 2 k2 + 1
           if (j > s0)
-            for (int b = 0; b < nb; ++b)
-              for (int kh = 0; kh < 2; ++kh) ring(&tmY2, (j - 1) * YM + 64 * kh, 2 * b);  // GEMM2_{j-1}
+            for (int b = 0; b < nb; ++b) ring(&tmY2, (j - 1) * YM, 2 * b);     // GEMM2_{j-1}: hidden block b
         }
       }
     }
@@ -224,16 +230,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (j < s1) {
           mbar_wait(s_empty, (g1 & 1) ^ 1);   // the epilogue has read S of the previous step
           tc_fence_after();
-          for (int k = 0; k < nkb; ++k) {
+          for (int k2 = 0; k2 < ns1; ++k2) {
             mbar_wait(&full[st], ph);
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk)
-                umma_bf16(tmem, sdesc_sw128(ra + st * STG + kk * 32, 16, 1024),
-                          sdesc_sw128(xa + k * (NX * 128) + kk * 32, 16, 1024), idesc1, (k | kk) ? 1u : 0u);
+              for (int kh = 0; kh < 2; ++kh) {
+                const int k = 2 * k2 + kh;
+                if (k < nkb) {
+#pragma unroll
+                  for (int kk = 0; kk < BK / 16; ++kk)
+                    umma_bf16(tmem, sdesc_sw128(ra + st * STG + kh * (YM * 128) + kk * 32, 16, 1024),
+                              sdesc_sw128(xa + k * (NX * 128) + kk * 32, 16, 1024), idesc1, (k | kk) ? 1u : 0u);
+                }
+              }
               umma_commit(&empty[st]);
-              if (k == nkb - 1) {
+              if (k2 == ns1 - 1) {
                 if (j == s1 - 1) umma_commit(x_empty);
                 umma_commit(s_full);
               }
@@ -244,32 +256,29 @@ __global__ void __launch_bounds__(THREADS, 1)
           ++g1;
         }
         if (j > s0) {
-          const int bb = g2 & 1;
-          mbar_wait(&b2_full[bb], (g2 >> 1) & 1);
+          mbar_wait(b2_full, g2 & 1);
           if (j - 1 == s0) mbar_wait(a2_empty, (uu & 1) ^ 1);   // previous unit's accumulator drained
           tc_fence_after();
           for (int b = 0; b < nb; ++b) {
-            for (int kh = 0; kh < 2; ++kh) {
-              mbar_wait(&full[st], ph);
-              tc_fence_after();
-              if (elect_one()) {
+            mbar_wait(&full[st], ph);
+            tc_fence_after();
+            if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                  // A: 128 hidden rows (two 64-wide MN atoms, 8 KB apart) x 16 streamed rows;
-                  // B: 16 K-rows of the [128 x 64] interleaved P' / G tile
-                  const uint64_t ad = sdesc_sw128(ra + st * STG + kk * 2048, 8192, 1024);
-                  const uint64_t bd = sdesc_none(b2a + bb * B2BYTES + (kh * 8 + kk * 2) * 128, 128, 2048);
-                  umma_bf16(tmem + 64 + 64 * b, ad, bd, idesc2, (j - 1 > s0 || kh || kk) ? 1u : 0u);
-                }
-                umma_commit(&empty[st]);
-                if (b == nb - 1 && kh == 1) {
-                  umma_commit(&b2_empty[bb]);
-                  if (j == s1) umma_commit(a2_full);
-                }
+              for (int kk = 0; kk < YM / 16; ++kk) {
+                // A: 128 hidden rows (two 64-wide MN atoms, 16 KB apart) x 16 streamed rows;
+                // B: 16 K-rows of the [128 x 64] interleaved P' / G tile
+                const uint64_t ad = sdesc_sw128(ra + st * STG + kk * 2048, YM * 128, 1024);
+                const uint64_t bd = sdesc_none(b2a + kk * 2 * 128, 128, 2048);
+                umma_bf16(tmem + 64 + 64 * b, ad, bd, idesc2, (j - 1 > s0 || kk) ? 1u : 0u);
               }
-              __syncwarp();
-              if (++st == NSTG) { st = 0; ph ^= 1; }
+              umma_commit(&empty[st]);
+              if (b == nb - 1) {
+                umma_commit(b2_empty);
+                if (j == s1) umma_commit(a2_full);
+              }
             }
+            __syncwarp();
+            if (++st == NSTG) { st = 0; ph ^= 1; }
           }
           ++g2;
         }
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             named_bar_sync(1, ebar_n);
             if (j > s0) {
               // O' holds GEMM2 of steps s0 .. j-1: wait for the last of them, scale in place
-              mbar_wait(&b2_empty[(g2 - 1) & 1], ((g2 - 1) >> 1) & 1);
+              mbar_wait(b2_empty, (g2 - 1) & 1);
               tc_fence_after();
               for (int b = 0; b < nb; ++b) {
 #pragma unroll
@@ -417,9 +426,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         // P' / G -> the interleaved MN-major B tile: element (k = r, n = 32 h + c) at
         // (n / 8) * 2048 + (r / 8) * 128 + (r % 8) * 16 + (n % 8) * 2
-        const int bb = g2 & 1;
-        mbar_wait(&b2_empty[bb], ((g2 >> 1) & 1) ^ 1);   // GEMM2 of two steps ago is done with it
-        uint8_t* dst = sB2 + bb * B2BYTES + (r >> 3) * 128 + (r & 7) * 16;
+        mbar_wait(b2_empty, (g2 & 1) ^ 1);   // GEMM2 of the previous step is done with the tile
+        uint8_t* dst = sB2 + (r >> 3) * 128 + (r & 7) * 16;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           *reinterpret_cast<uint4*>(dst + (4 * h + i) * 2048) =
@@ -428,7 +436,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         fence_proxy_async_shared();
         tc_fence_before();   // orders this thread's earlier TMEM stores (rescale) before the arrive
         __syncwarp();
-        if (lane == 0) mbar_arrive(&b2_full[bb]);
+        if (lane == 0) mbar_arrive(b2_full);
         ++g2;
       }
       // ---- unit end: drain the O' / dW^T accumulator
