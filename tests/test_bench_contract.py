@@ -35,3 +35,26 @@ def test_committed_gpu_bench_line_has_the_contract_keys():
     assert r["bound"] == "tensor" and 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["gpu_launches"] > 0 and d["memory"]["no_NxV_buffer"] is True
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+
+
+def test_self_launch_builds_a_torchrun_command(monkeypatch):
+    """`bench.py --gpus N` without WORLD_SIZE re-launches itself through torch.distributed.run,
+    one process per GPU, rendezvous on 127.0.0.1, passing its own arguments through."""
+    sys.path.insert(0, ROOT)
+    import bench
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "7"])
+    assert bench._self_launch(4) == 0 or "cmd" in seen
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "7"]
+
+
+def test_committed_r02_lines_carry_in_bench_parity():
+    """Round-2 bench lines carry the in-bench oracle-golden check."""
+    for f in ("r02_bench_default_same_box.json", "r02_bench_designb.json", "r02_bench_long_200steps.json"):
+        d = json.loads(open(os.path.join(ROOT, "profiles", f)).read().strip().splitlines()[-1])
+        assert d["parity"]["ok"] is True and d["parity"]["rows_checked"] == 4915, f
+        assert d["parity"]["lse_max_rel_err"] <= 1e-3 and d["parity"]["loss_abs_err"] <= 2e-3
