@@ -110,8 +110,8 @@ typedef enum {
  * U_n = E_p[W] - W_{y_n} (online-rescaled like the FlashAttention output accumulator,
  * P:1220-1226, target excluded: (O' - d_nt W_y) / d) and the backward recomputes the logits,
  * keeps the dlogits in shared memory only and contracts them into dW; dH = s U.  Same
- * results as the default path within the stated tolerances; measured SLOWER on B200 (its
- * GEMMs are N = 64 wide).  D <= 896 (else CCE_ERR_UNSUPPORTED from
+ * results as the default path within the stated tolerances; measured 1.58x SLOWER on B200
+ * (its GEMMs are N = 64 wide).  D <= 896 (else CCE_ERR_UNSUPPORTED from
  * cce_forward), world 1, no label smoothing / z-loss, not with cce_backward_adamw
  * (CCE_ERR_UNSUPPORTED). */
 #define CCE_FLAG_DESIGN_B 2048u
