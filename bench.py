@@ -122,6 +122,20 @@ class ClockSampler:
                 "samples_under_load": len(load), "power_w_max": max(pw) if pw else None}
 
 
+def _all_host_cores():
+    """torch.distributed.run sets OMP_NUM_THREADS=1 in every rank; the CPU baseline is defined
+    on all host cores, so rank 0 raises the OpenMP thread count of the oracle's runtime."""
+    import ctypes
+    try:
+        n = len(os.sched_getaffinity(0))
+    except Exception:
+        n = os.cpu_count() or 1
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(ctypes.c_int(n))
+    except OSError:
+        pass
+
+
 def cpu_baseline(p, n_tokens_target_s=15.0):
     """The oracle as it stands (fp64, OpenMP on all host cores) on a bounded
     sample of the same workload: the first n tokens of the batch at full V, D."""
@@ -129,6 +143,7 @@ def cpu_baseline(p, n_tokens_target_s=15.0):
 
     import oracle
     oracle.build()
+    _all_host_cores()
     lab = p["labels"]
 
     def run(n):
@@ -160,6 +175,7 @@ def reference_arm(args):
     c = workload.CONFIGS[args.config]
     p = workload.make_config(args.config, seed=args.seed)
     oracle.build()
+    _all_host_cores()
     # size one step to ~3 s of CPU work
     t = time.perf_counter()
     oracle.cce(p["H"][:16], p["W"], p["labels"][:16])
@@ -293,20 +309,36 @@ def main():
             if a != b)
         args.combine = "p2p" if (peers or one_gpu) else "nccl"
     p2p = world > 1 and args.combine == "p2p"
+    h = None
+    if p2p:  # map every rank's workspace into every other rank (CUDA IPC), then a barrier
+        ok = 1
+        try:
+            h = cce.CCEHandle(vocab_total=c.V, vocab_offset=lo, rank=rank, world=world,
+                              flags=args.flags | cce.FLAG_P2P_COMBINE)
+            ws = h.workspace(c.N, c.D, hi - lo, dev)
+            allh = [None] * world
+            dist.all_gather_object(allh, cce.cce_p2p_export(ws))
+            cce.cce_p2p_attach(h.h, ws, c.N, c.D, [a[0] for a in allh], [a[1] for a in allh])
+        except Exception as ex:  # e.g. no IPC / peer access: every rank falls back to NCCL together
+            print(f"[bench rank {rank}] peer-memory exchange unavailable ({ex}); using NCCL", file=sys.stderr)
+            ok = 0
+        okt = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if int(okt.item()) == 0 and not one_gpu:
+            p2p, args.combine = False, "nccl"
+            if h is not None:
+                h.close()
+                h = None
+        dist.barrier()
     if world > 1 and not p2p:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(cce.cce_nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         comm = cce.cce_nccl_comm_init(world, bytes(uid.cpu().numpy().tobytes()), rank)
-    h = cce.CCEHandle(vocab_total=c.V, vocab_offset=lo, rank=rank, world=world, nccl_comm=comm,
-                      flags=args.flags | (cce.FLAG_P2P_COMBINE if p2p else 0))
-    ws = h.workspace(c.N, c.D, hi - lo, dev)
-    if p2p:  # map every rank's workspace into every other rank (CUDA IPC), then a barrier
-        allh = [None] * world
-        dist.all_gather_object(allh, cce.cce_p2p_export(ws))
-        cce.cce_p2p_attach(h.h, ws, c.N, c.D, [a[0] for a in allh], [a[1] for a in allh])
-        dist.barrier()
+    if h is None:
+        h = cce.CCEHandle(vocab_total=c.V, vocab_offset=lo, rank=rank, world=world, nccl_comm=comm, flags=args.flags)
+        ws = h.workspace(c.N, c.D, hi - lo, dev)
     loss = torch.empty((), dtype=torch.float32, device=dev)
     lse = torch.empty(c.N, dtype=torch.float32, device=dev)
     nvt = torch.empty((), dtype=torch.int32, device=dev)
