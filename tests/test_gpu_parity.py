@@ -367,3 +367,21 @@ def test_rmsnorm_eps_must_be_positive(dev):
         h.forward_rmsnorm(X, g, 0.0, W, y)
     assert ei.value.status == 1
     h.close()
+
+
+@pytest.mark.parametrize("flags", [0, 2048], ids=["default", "design_b"])
+def test_row_strided_inputs(dev, flags):
+    """H and W as column slices of wider buffers (ldh = D + 64, ldw = D + 128, the padding
+    columns NaN): the row strides reach the TMA maps and the padding is never read."""
+    import torch
+    p = workload.make_problem(500, 192, 7000, seed=51, ignore="bern40")
+    H, W, y = to_dev(p, dev)
+    Hb = torch.full((500, 192 + 64), float("nan"), dtype=torch.bfloat16, device=dev)
+    Wb = torch.full((7000, 192 + 128), float("nan"), dtype=torch.bfloat16, device=dev)
+    Hb[:, :192] = H
+    Wb[:, :192] = W
+    Hs, Ws = Hb[:, :192], Wb[:, :192]
+    assert Hs.stride(0) == 256 and Ws.stride(0) == 320
+    got = run_gpu(Hs, Ws, y, flags=flags)
+    ref = oracle.cce(p["H"], p["W"], p["labels"])
+    assert_parity(got, ref, p["labels"])
