@@ -274,19 +274,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # CCE_BENCH_ONE_GPU=1 (testing the N > 1 plumbing on a one-GPU box): every rank on cuda:0,
-    # gloo for the host-side process group, --combine p2p for the exchange (NCCL refuses two
-    # ranks on one GPU).  The timings of such a run are time-sliced, not a scaling result.
-    one_gpu = os.environ.get("CCE_BENCH_ONE_GPU") == "1"
-    if one_gpu:
-        local = 0
+    # one process per GPU: ranks whose kernels wait on one another (the exchange) must not be
+    # time-sliced on one GPU (B200_PROFILING.md: Xid 109); the one-GPU emulation of the
+    # exchange is tests/test_gpu_p2p_emulated.py, not a bench run
+    if world > torch.cuda.device_count():
+        print(json.dumps({"error": f"--gpus {world} needs {world} visible GPUs, found {torch.cuda.device_count()}"}))
+        return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        if one_gpu:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("nccl", device_id=dev)
     if rank == 0:
         cce_build.build()
     if world > 1:
@@ -304,10 +301,10 @@ def main():
     comm = None
     if args.combine == "auto":
         n_dev = torch.cuda.device_count()
-        peers = world > 1 and not one_gpu and all(
+        peers = world > 1 and all(
             torch.cuda.can_device_access_peer(a, b) for a in range(min(world, n_dev)) for b in range(min(world, n_dev))
             if a != b)
-        args.combine = "p2p" if (peers or one_gpu) else "nccl"
+        args.combine = "p2p" if peers else "nccl"
     p2p = world > 1 and args.combine == "p2p"
     h = None
     if p2p:  # map every rank's workspace into every other rank (CUDA IPC), then a barrier
@@ -324,7 +321,7 @@ def main():
             ok = 0
         okt = torch.tensor([ok], dtype=torch.int32, device=dev)
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-        if int(okt.item()) == 0 and not one_gpu:
+        if int(okt.item()) == 0:
             p2p, args.combine = False, "nccl"
             if h is not None:
                 h.close()

@@ -371,6 +371,23 @@ cce_status cce_p2p_export(const void *dev_ptr, void *handle_out, int64_t *offset
 cce_status cce_p2p_attach(cce_handle *h, void *workspace, int64_t N, int64_t D, const void *handles,
                           const int64_t *offsets);
 
+/*
+ * One-GPU emulation of the peer-memory exchange, for testing where there are fewer GPUs than
+ * ranks: `world` handles (CCE_FLAG_P2P_COMBINE, cfg.rank == index, cfg.world == world) in ONE
+ * process on ONE device, hs[r] using workspaces[r] (device pointers; no IPC).  Ranks whose
+ * kernels wait on one another must not be separate launches time-sliced on one GPU (nothing
+ * makes them run at the same time; B200_PROFILING.md reports Xid 109 for such processes), so
+ * the group defers: cce_forward on ranks 0 .. world-2 pushes and signals only, and the last
+ * rank's cce_forward runs every rank's wait + finalize; cce_backward on ranks 0 .. world-2
+ * prepares the launch only, and the last rank's cce_backward issues ONE backward launch in
+ * which CTA pairs [r p, (r + 1) p) run rank r's queue (p = (SMs / 2) / world; the RED items
+ * reduce across the co-resident rank groups), then every rank's tail.  So call the forwards of
+ * ranks 0 .. world-1 in order on one stream, then the backwards in order on the same stream
+ * (CCE_ERR_NO_FORWARD otherwise).  Same kernels and arithmetic as cce_p2p_attach; the
+ * handles must outlive one another's use (destroy them together).
+ */
+cce_status cce_p2p_attach_group(cce_handle *const *hs, void *const *workspaces, int32_t world, int64_t N, int64_t D);
+
 /* NCCL plumbing for world > 1 (NCCL is resolved at run time with dlopen; the
  * library does not link it).  The 128-byte unique id is produced on rank 0 and
  * broadcast by the caller (e.g. over torch.distributed). */

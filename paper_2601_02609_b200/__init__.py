@@ -30,7 +30,8 @@ EXPORTS = ["cce_config_default", "cce_create", "cce_destroy", "cce_workspace_byt
            "cce_nccl_comm_destroy", "cce_status_string", "cce_kernel_launches", "cce_build_info",
            "cce_profile_enable", "cce_profile_read", "cce_debug_trace", "cce_backward_adamw", "cce_adamw_step",
            "cce_forward_rmsnorm", "cce_backward_rmsnorm", "cce_combine_offsets", "cce_forward_finish",
-           "cce_backward_finish", "cce_step_host_async", "cce_p2p_export", "cce_p2p_attach"]
+           "cce_backward_finish", "cce_step_host_async", "cce_p2p_export", "cce_p2p_attach",
+           "cce_p2p_attach_group"]
 PROF_CLASSES = ("fwd_logits_lse", "bwd", "bwd_dW", "bwd_dH", "aux")
 # "bwd" is the persistent backward kernel (recompute + dlogits + dW + dH)
 FLAG_GRAD_FP32 = 64
@@ -113,6 +114,8 @@ def lib():
         L.cce_p2p_export.restype = st
         L.cce_p2p_attach.argtypes = [p, p, i64, i64, p, p]
         L.cce_p2p_attach.restype = st
+        L.cce_p2p_attach_group.argtypes = [p, p, i32, i64, i64]
+        L.cce_p2p_attach_group.restype = st
         L.cce_step_host_async.argtypes = [p, p, i64, i64, p, p, i64, i64, p, p, p, p, sz, p, sz, p, p]
         L.cce_step_host_async.restype = st
         L.cce_nccl_unique_id.argtypes = [p]
@@ -311,6 +314,16 @@ def cce_p2p_attach(h, workspace, N: int, D: int, handles, offsets):
     blob = ctypes.create_string_buffer(b"".join(bytes(x) for x in handles), 64 * len(handles))
     offs = (ctypes.c_int64 * len(offsets))(*offsets)
     _check(lib().cce_p2p_attach(h, _ptr(workspace), N, D, blob, offs), "cce_p2p_attach")
+
+
+def cce_p2p_attach_group(handles, workspaces, N: int, D: int):
+    """One-GPU emulation of the peer-memory exchange (cce.h): handles[r] / workspaces[r] of
+    ranks 0 .. world-1 in one process.  Then call every rank's forward in rank order, then every
+    rank's backward in rank order, on one stream."""
+    world = len(handles)
+    hs = (ctypes.c_void_p * world)(*[h.value if isinstance(h, ctypes.c_void_p) else h for h in handles])
+    ws = (ctypes.c_void_p * world)(*[w.data_ptr() for w in workspaces])
+    _check(lib().cce_p2p_attach_group(hs, ws, world, N, D), "cce_p2p_attach_group")
 
 
 def cce_kernel_launches(h) -> int:

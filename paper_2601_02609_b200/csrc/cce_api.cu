@@ -59,6 +59,19 @@ struct cce_handle {
   bool p2p_attached = false;
   int epoch = 0;
   int64_t p2p_N = 0, p2p_D = 0;  // the problem size the P2P flag arrays were laid out for
+  // cce_p2p_attach_group (one-GPU emulation of `group_n` ranks in one process): the group's
+  // handles in rank order; each rank's forward tail and backward launch + tail are deferred
+  // until the group's last rank calls, which issues them for every rank (one backward launch)
+  cce_handle* group[P2P_MAX] = {};
+  int group_n = 0;
+  bool grp_fwd_pending = false, grp_bwd_pending = false;
+  cudaStream_t grp_stream = nullptr;
+  pairk::PairLaunch grp_launch;             // this rank's prepared backward launch (host copy)
+  bool grp_has_launch = false;
+  void* grp_dH = nullptr;
+  void* grp_dgamma = nullptr;
+  bool grp_norm = false;
+  pairk::PairLaunch* grp_launch_dev = nullptr;  // last rank: every rank's launch, device copy
   const void* nX = nullptr;
   int64_t ldx = 0;
   const void* gamma = nullptr;
@@ -463,6 +476,7 @@ cce_status cce_destroy(cce_handle* h) {
   if (h->ev_copied) cudaEventDestroy(h->ev_copied);
   for (auto p : h->opened)
     if (p) cudaIpcCloseMemHandle(p);
+  if (h->grp_launch_dev) cudaFree(h->grp_launch_dev);
   delete h;
   return CCE_OK;
 }
@@ -691,6 +705,30 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     const int epoch = ++h->epoch;  // (the merge above already stored the stats into every rank)
     k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_STATS, h->cfg.rank, h->cfg.world,
                                   epoch);
+    if (h->group_n) {
+      // one-GPU group emulation: every rank pushes and signals before any rank waits
+      h->grp_fwd_pending = true;
+      h->grp_stream = s;
+      h->p_loss = loss;
+      h->p_lse = lse;
+      h->p_nv = n_valid;
+      if (h->cfg.rank + 1 < h->group_n) return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+      for (int q = 0; q < h->group_n; ++q) {
+        cce_handle* g = h->group[q];
+        if (!g->grp_fwd_pending || g->epoch != epoch || g->grp_stream != s) return CCE_ERR_NO_FORWARD;
+      }
+      for (int q = 0; q < h->group_n; ++q) {
+        cce_handle* g = h->group[q];
+        g->grp_fwd_pending = false;
+        const Layout Lq = layout(g->N, g->D, g->V_local, g->cfg.world, g->chunk, g->slots, g->cfg.flags);
+        k_p2p_wait<<<1, 32, 0, s>>>(at<int>(g->ws, Lq.p2p_flags), P2P_STATS, g->cfg.world, epoch,
+                                    at<int>(g->ws, Lq.scal) + 1);
+        const cce_status st = forward_tail(g, at<float4>(g->ws, Lq.stats_all) + (size_t)(epoch & 1) * g->cfg.world * Lq.Npad,
+                                           g->p_loss, g->p_lse, g->p_nv, s);
+        if (st != CCE_OK) return st;
+      }
+      return CCE_OK;
+    }
     k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_STATS, h->cfg.world, epoch, errp);
     return forward_tail(h, at<float4>(ws, L.stats_all) + (size_t)(epoch & 1) * h->cfg.world * L.Npad, loss, lse,
                         n_valid, s);
@@ -792,6 +830,8 @@ static bool adamw_aligned(const cce_adamw_params* o) {
 
 static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, void* dW, const cce_adamw_params* opt,
                                 void* stream, void* dgamma = nullptr, bool norm = false);
+static cce_status backward_tail(cce_handle* h, void* dH, void* dgamma, bool norm, cudaStream_t s);
+static cce_status group_backward(cce_handle* h, void* dH, void* dgamma, bool norm, cudaStream_t s);
 
 cce_status cce_backward_rmsnorm(cce_handle* h, const float* dloss, void* dX, void* dgamma, void* dW, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
@@ -975,7 +1015,13 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
     // SMs, finishes dW
     const bool split = h->cfg.nccl_comm != nullptr && !(h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) && !norm;
     cce_status st;
-    if (!split) {
+    if (h->group_n) {
+      // one-GPU group emulation: the launch is issued for every rank at once by the last rank
+      const CUtensorMap* ms[10] = {&mHcK, &mWK, &mGMN, &mHcMN, &mGK, &mWMN, &mDH, &mHcMN3, &mWMN3, &mGst};
+      for (int i = 0; i < 10; ++i) h->grp_launch.m[i] = *ms[i];
+      h->grp_launch.P = pp;
+      h->grp_has_launch = true;
+    } else if (!split) {
       st = launch_pair(h, mHcK, mWK, mGMN, mHcMN, mGK, mWMN, mDH, pp, s, 1, &mHcMN3, &mWMN3, &mGst);
       if (st != CCE_OK) return st;
     } else {
@@ -1015,6 +1061,18 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
         cudaMemsetAsync(dW, 0, (size_t)V_local * D * ((h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 4 : 2), s) != cudaSuccess)
       return CCE_ERR_CUDA;
   }
+  if (h->group_n) return group_backward(h, dH, dgamma, norm, s);
+  return backward_tail(h, dH, dgamma, norm, s);
+}
+
+// Everything after the backward kernel: the dH exchange (a10), the scatter to the original
+// rows (or the RMSNorm backward / the sequence-sharded slice).
+static cce_status backward_tail(cce_handle* h, void* dH, void* dgamma, bool norm, cudaStream_t s) {
+  const int64_t N = h->N, D = h->D, V_local = h->V_local;
+  const Layout L = layout(N, D, V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
+  void* ws = h->ws;
+  int* nvp = at<int>(ws, L.scal);
+  float* dH32 = at<float>(ws, L.dH32);
   const bool seq = (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0;
   float* dHo = seq ? at<float>(ws, L.dHo) : nullptr;
   if (N > 0) {
@@ -1092,6 +1150,63 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
   return CCE_OK;
 }
 
+// One-GPU group emulation (cce_p2p_attach_group): ranks 0 .. n-2 only record their launch and
+// tail; the last rank issues ONE backward launch holding every rank's queue on its own CTA
+// pairs (co-resident by construction, cooperative when the driver accepts it), then every
+// rank's tail in rank order.
+static cce_status group_backward(cce_handle* h, void* dH, void* dgamma, bool norm, cudaStream_t s) {
+  h->grp_bwd_pending = true;
+  h->grp_dH = dH;
+  h->grp_dgamma = dgamma;
+  h->grp_norm = norm;
+  h->grp_stream = s;
+  const int n = h->group_n;
+  if (h->cfg.rank + 1 < n) return cudaGetLastError() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
+  int with_kernel = 0;
+  for (int q = 0; q < n; ++q) {
+    const cce_handle* g = h->group[q];
+    if (!g->grp_bwd_pending || g->grp_stream != s || g->epoch != h->epoch) return CCE_ERR_NO_FORWARD;
+    with_kernel += g->grp_has_launch ? 1 : 0;
+  }
+  if (with_kernel != 0 && with_kernel != n) return CCE_ERR_UNSUPPORTED;  // (empty shards are refused in P2P mode)
+  if (with_kernel == n) {
+    std::vector<pairk::PairLaunch> all(n);
+    for (int q = 0; q < n; ++q) all[q] = h->group[q]->grp_launch;
+    if (cudaMemcpyAsync(h->grp_launch_dev, all.data(), sizeof(pairk::PairLaunch) * n, cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+      return CCE_ERR_CUDA;
+    if (cudaFuncSetAttribute(pairk::cce_pair_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             pairk::PSMEM) != cudaSuccess)
+      return CCE_ERR_CUDA;
+    const int ppr = (h->num_sms / 2) / n;  // CTA pairs per rank
+    ProfScope ps(h, s, 1);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(2 * ppr * n);
+    lc.blockDim = dim3(pairk::PTHREADS);
+    lc.dynamicSmemBytes = pairk::PSMEM;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    const pairk::PairLaunch* dev = h->grp_launch_dev;
+    if (cudaLaunchKernelEx(&lc, pairk::cce_pair_group_kernel, dev, ppr) != cudaSuccess) {
+      (void)cudaGetLastError();  // cooperative + cluster launch refused: a plain launch of the same grid
+      lc.numAttrs = 0;
+      if (cudaLaunchKernelEx(&lc, pairk::cce_pair_group_kernel, dev, ppr) != cudaSuccess) return CCE_ERR_CUDA;
+    }
+  }
+  for (int q = 0; q < n; ++q) {
+    cce_handle* g = h->group[q];
+    g->grp_bwd_pending = false;
+    g->grp_has_launch = false;
+    const cce_status st = backward_tail(g, g->grp_dH, g->grp_dgamma, g->grp_norm, s);
+    if (st != CCE_OK) return st;
+  }
+  return CCE_OK;
+}
+
 cce_status cce_backward_finish(cce_handle* h, void* stream) {
   if (!h) return CCE_ERR_INVALID_VALUE;
   if (!h->bwd_pending) return CCE_ERR_NO_FORWARD;
@@ -1157,6 +1272,39 @@ cce_status cce_p2p_attach(cce_handle* h, void* workspace, int64_t N, int64_t D, 
   h->p2p_attached = true;
   h->epoch = 0;
   return CCE_OK;
+}
+
+cce_status cce_p2p_attach_group(cce_handle* const* hs, void* const* workspaces, int32_t world, int64_t N, int64_t D) {
+  if (!hs || !workspaces || world < 2 || world > P2P_MAX || N < 0 || D <= 0) return CCE_ERR_INVALID_VALUE;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return CCE_ERR_CUDA;
+  for (int r = 0; r < world; ++r) {
+    const cce_handle* h = hs[r];
+    if (!h || !workspaces[r] || !(h->cfg.flags & CCE_FLAG_P2P_COMBINE) || h->p2p_attached || h->cfg.world != world ||
+        h->cfg.rank != r || h->device != dev)
+      return CCE_ERR_INVALID_VALUE;
+    if (!aligned16(workspaces[r])) return CCE_ERR_UNSUPPORTED;
+    for (int q = 0; q < r; ++q)
+      if (hs[q] == h) return CCE_ERR_INVALID_VALUE;
+  }
+  cce_handle* last = hs[world - 1];
+  if (cudaMalloc(&last->grp_launch_dev, sizeof(pairk::PairLaunch) * world) != cudaSuccess) return CCE_ERR_CUDA;
+  const Layout L = layout(N, D, 0, world, last->chunk, last->slots, last->cfg.flags);
+  for (int r = 0; r < world; ++r) {
+    cce_handle* h = hs[r];
+    for (int q = 0; q < world; ++q) {
+      h->peers.ws[q] = static_cast<char*>(workspaces[q]);
+      h->group[q] = hs[q];
+    }
+    h->group_n = world;
+    if (cudaMemset(workspaces[r], 0, L.stats_all) != cudaSuccess) return CCE_ERR_CUDA;  // flags start at 0
+    h->p2p_N = N;
+    h->p2p_D = D;
+    h->p2p_ws = workspaces[r];
+    h->p2p_attached = true;
+    h->epoch = 0;
+  }
+  return cudaDeviceSynchronize() == cudaSuccess ? CCE_OK : CCE_ERR_CUDA;
 }
 
 cce_status cce_get_error(cce_handle* h, void* stream) {

@@ -582,16 +582,13 @@ __device__ __forceinline__ void mma_item_k2(const PItem& it, uint64_t* full_bar,
 }
 
 // ------------------------------------------------------------------ kernel
-// ADAMW = 1: the backward queue with AdamW fused into the dW epilogue (cce_backward_adamw);
-// a separate instantiation so its epilogue's register demand leaves the default kernel alone.
+// The kernel body, shared by the launch kinds below: the tensor maps are generic pointers
+// (kernel parameters for cce_pair_kernel, a global-memory array for cce_pair_group_kernel).
 template <int ADAMW, int P2P>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
-    cce_pair_kernel(const __grid_constant__ CUtensorMap tmHcK, const __grid_constant__ CUtensorMap tmWK,
-                    const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
-                    const __grid_constant__ CUtensorMap tmGK, const __grid_constant__ CUtensorMap tmWMN,
-                    const __grid_constant__ CUtensorMap tmDH, const __grid_constant__ CUtensorMap tmHcMN3,
-                    const __grid_constant__ CUtensorMap tmWMN3, const __grid_constant__ CUtensorMap tmGst,
-                    const PairParams P) {
+__device__ __forceinline__ void pair_body(const CUtensorMap* tmHcK, const CUtensorMap* tmWK, const CUtensorMap* tmGMN,
+                                          const CUtensorMap* tmHcMN, const CUtensorMap* tmGK, const CUtensorMap* tmWMN,
+                                          const CUtensorMap* tmDH, const CUtensorMap* tmHcMN3,
+                                          const CUtensorMap* tmWMN3, const CUtensorMap* tmGst, const PairParams& P) {
   const GemmParams& g = P.g;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -619,11 +616,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   int* dh_flag = P.sched + 2 + 2 * P.n_chunks;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmHcK); tma_prefetch_desc(&tmWK);
+    tma_prefetch_desc(tmHcK); tma_prefetch_desc(tmWK);
     if (P.mode == 1) {
-      tma_prefetch_desc(&tmGMN); tma_prefetch_desc(&tmHcMN); tma_prefetch_desc(&tmGK); tma_prefetch_desc(&tmWMN);
-      tma_prefetch_desc(&tmDH);
-      tma_prefetch_desc(&tmHcMN3); tma_prefetch_desc(&tmWMN3); tma_prefetch_desc(&tmGst);
+      tma_prefetch_desc(tmGMN); tma_prefetch_desc(tmHcMN); tma_prefetch_desc(tmGK); tma_prefetch_desc(tmWMN);
+      tma_prefetch_desc(tmDH);
+      tma_prefetch_desc(tmHcMN3); tma_prefetch_desc(tmWMN3); tma_prefetch_desc(tmGst);
     }
     for (int s = 0; s < KSTAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull_bar[b], 1); mbar_init(&tempty_bar[b], 2 * PEPI_WARPS); }
@@ -727,16 +724,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           const int kb0 = KPS * st;
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * KPS * (PA_BYTES + b_bytes));
           if (it.type == PT_FWD || it.type == PT_G) {
-            tma_load_3d_pair(&tmHcK, fb, a, 0, it.m0 + hr, kb0);
-            tma_load_3d_pair(&tmWK, fb, b, 0, it.n0 + hn, kb0);
+            tma_load_3d_pair(tmHcK, fb, a, 0, it.m0 + hr, kb0);
+            tma_load_3d_pair(tmWK, fb, b, 0, it.n0 + hn, kb0);
           } else if (it.type == PT_DW) {
-            tma_load_3d_pair(&tmGMN, fb, a, 0, kb0 * BK, slot_blk0 + (it.m0 + hr) / 64);
-            if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmHcMN3, fb, b, 0, kb0 * BK, (it.n0 + hn) / 64);
-            else tma_load_2d_pair(&tmHcMN, fb, b, it.n0 + hn, kb0 * BK);
+            tma_load_3d_pair(tmGMN, fb, a, 0, kb0 * BK, slot_blk0 + (it.m0 + hr) / 64);
+            if (it.N / 2 / 64 == 2) tma_load_3d_pair(tmHcMN3, fb, b, 0, kb0 * BK, (it.n0 + hn) / 64);
+            else tma_load_2d_pair(tmHcMN, fb, b, it.n0 + hn, kb0 * BK);
           } else {  // PT_DH
-            tma_load_3d_pair(&tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb0);
-            if (it.N / 2 / 64 == 2) tma_load_3d_pair(&tmWMN3, fb, b, 0, c0 + kb0 * BK, (it.n0 + hn) / 64);
-            else tma_load_2d_pair(&tmWMN, fb, b, it.n0 + hn, c0 + kb0 * BK);
+            tma_load_3d_pair(tmGK, fb, a, 0, it.m0 + hr, slot_blk0 + kb0);
+            if (it.N / 2 / 64 == 2) tma_load_3d_pair(tmWMN3, fb, b, 0, c0 + kb0 * BK, (it.n0 + hn) / 64);
+            else tma_load_2d_pair(tmWMN, fb, b, it.n0 + hn, c0 + kb0 * BK);
           }
           if (++stage == KSTAGES) { stage = 0; phase ^= 1; }
         }
@@ -826,7 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       if (it.type == PT_FWD) {
         if constexpr (!ADAMW) epi_fwd(g, taddr, e, it, k.nv);
       } else if (it.type == PT_G) {
-        epi_g(g, taddr, e, it, k.nv, scale, &tmGst, (it.c % P.slots) * (g.C / 64));
+        epi_g(g, taddr, e, it, k.nv, scale, tmGst, (it.c % P.slots) * (g.C / 64));
       } else if (it.type == PT_RED) {
         if constexpr (P2P) epi_reduce(P, e, it, k.nv, leader);
       } else if (it.type == PT_DW) {
@@ -847,7 +844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         if (leader) wait_ge(&dh_flag[it.tile_id], 2 * it.c);
         named_bar_sync(2, PEPI_THREADS);
         fence_proxy_async_global();  // the acquired flag orders the TMA reduce below
-        epi_dh_tma(&tmDH, taddr, e, it);
+        epi_dh_tma(tmDH, taddr, e, it);
       }
       if (have_acc) {
         tc_fence_before();
@@ -913,6 +910,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair(tmem_base, TMEM_COLS);
+}
+
+
+// ADAMW = 1: the backward queue with AdamW fused into the dW epilogue (cce_backward_adamw);
+// a separate instantiation so its epilogue's register demand leaves the default kernel alone.
+template <int ADAMW, int P2P>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
+    cce_pair_kernel(const __grid_constant__ CUtensorMap tmHcK, const __grid_constant__ CUtensorMap tmWK,
+                    const __grid_constant__ CUtensorMap tmGMN, const __grid_constant__ CUtensorMap tmHcMN,
+                    const __grid_constant__ CUtensorMap tmGK, const __grid_constant__ CUtensorMap tmWMN,
+                    const __grid_constant__ CUtensorMap tmDH, const __grid_constant__ CUtensorMap tmHcMN3,
+                    const __grid_constant__ CUtensorMap tmWMN3, const __grid_constant__ CUtensorMap tmGst,
+                    const PairParams P) {
+  pair_body<ADAMW, P2P>(&tmHcK, &tmWK, &tmGMN, &tmHcMN, &tmGK, &tmWMN, &tmDH, &tmHcMN3, &tmWMN3, &tmGst, P);
+}
+
+// One rank's launch of the backward queue, as the group kernel below reads it.
+struct alignas(64) PairLaunch {
+  CUtensorMap m[10];  // HcK, WK, GMN, HcMN, GK, WMN, DH, HcMN3, WMN3, Gst
+  PairParams P;
+};
+
+// One-GPU emulation of `world` ranks exchanging over peer memory (cce_p2p_attach_group):
+// ONE launch holds every rank's backward queue, CTA pairs [r ppr, (r + 1) ppr) serving rank
+// r, so the ranks' kernels are co-resident by construction -- ranks whose kernels wait on one
+// another are never separate launches time-sliced on one GPU.  Same body as the P2P kernel.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
+    cce_pair_group_kernel(const PairLaunch* __restrict__ L, int pairs_per_rank) {
+  const PairLaunch& R = L[(blockIdx.x >> 1) / pairs_per_rank];
+  pair_body<0, 1>(&R.m[0], &R.m[1], &R.m[2], &R.m[3], &R.m[4], &R.m[5], &R.m[6], &R.m[7], &R.m[8], &R.m[9], R.P);
 }
 
 }  // namespace pairk

@@ -1,6 +1,7 @@
 #!/usr/bin/env bash
 # compute-sanitizer memcheck / racecheck / synccheck over the pair kernels (tiny config and a
-# 6-chunk problem), the design-B kernels, and the peer-memory path with 2 processes.
+# 6-chunk problem), the design-B kernels, and the peer-memory path (one-GPU group emulation:
+# 2 ranks in one process, one backward launch; never ranks time-sliced as processes).
 # Run on the GPU box:  bash scripts/sanitize_all.sh  -> gpurun_out/sanitize_*.txt
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
@@ -16,5 +17,5 @@ for tool in memcheck racecheck synccheck; do
   run chunks6 $tool python scripts/sanitize_case.py 1000 128 41000
   run designb $tool python scripts/sanitize_case.py 300 256 3000 2048
 done
-# peer-memory exchange fused into the kernels: 2 processes sharing the GPU (tests/test_gpu_p2p.py)
-run p2p memcheck --target-processes all python -m pytest tests/test_gpu_p2p.py -x -q -k "between_processes and 2"
+# peer-memory exchange fused into the kernels (tests/test_gpu_p2p_emulated.py, world 2)
+run p2p memcheck python -m pytest tests/test_gpu_p2p_emulated.py -x -q -k "matches_oracle and 2"

@@ -21,7 +21,12 @@ dev = torch.device("cuda:0")
 c = workload.CONFIGS[cfg]
 p = workload.make_config(cfg, seed=42)
 H, W, y = to_dev(p, dev)
-h = cce.CCEHandle(vocab_total=c.V, flags=int(os.environ.get("CCE_FLAGS", "0")))
+V = c.V
+if os.environ.get("CCE_VSLICE"):  # the kernels of one vocabulary shard: the first n rows of W
+    V = int(os.environ["CCE_VSLICE"])
+    W = W[:V].contiguous()
+    y = torch.where(y >= 0, y % V, y)
+h = cce.CCEHandle(vocab_total=V, flags=int(os.environ.get("CCE_FLAGS", "0")))
 dH = torch.empty(H.shape, dtype=torch.bfloat16, device=dev)
 dW = torch.empty(W.shape, dtype=torch.bfloat16, device=dev)
 one = torch.ones((), dtype=torch.float32, device=dev)
@@ -80,3 +85,14 @@ for name, rec in (("forward", allrec[1]), ("backward", allrec[0])):
               f"mma_end->epi0 {np.mean(ep0[m]-m1[m]):6.2f} | epi {np.mean(ep1[m]-ep0[m]):6.2f} | dep-wait {np.mean(rdy[m]-deq[m]):6.2f} | "
               f"per-kb {np.mean((m1[m]-m0[m])/np.maximum(kb[m],1)):.3f} us, {np.mean(cyc[m]/np.maximum(kb[m],1)):.0f} cyc"
               f" (clock {np.sum(cyc[m])/np.sum((m1[m]-m0[m])*1e3):.2f} GHz) | issue->full {np.mean(lat[m]/np.maximum(kb[m],1)):.0f} cyc")
+    # per CTA pair (leader SM): MMA-window occupancy, idle before the first and after the last item
+    sm = rec[:, 1].astype(np.int64)
+    busy, head, tail = [], [], []
+    for s_ in np.unique(sm):
+        m = sm == s_
+        busy.append(np.sum(m1[m] - m0[m]) / ep1.max())
+        head.append(m0[m].min())
+        tail.append(ep1.max() - m1[m].max())
+    print(f"   per pair: MMA window {np.mean(busy)*100:.1f}% of the span (min {np.min(busy)*100:.1f}%), "
+          f"first MMA at {np.mean(head):.1f} us (max {np.max(head):.1f}), idle after the last MMA {np.mean(tail):.1f} us "
+          f"(max {np.max(tail):.1f})")

@@ -1,9 +1,10 @@
 """The vocabulary-sharded exchange over peer memory (CCE_FLAG_P2P_COMBINE, SURVEY 8(f)
-NEXT #4): two PROCESSES, one rank each, on the same GPU (this run has one GPU), their
-workspaces mapped into each other with CUDA IPC.  The stats are pushed by the merge
-kernel and the dH slices are reduced and broadcast by k_p2p_reduce_dH across the two
-processes; both ranks must match the unsharded oracle and each other bit for bit, over two
-consecutive steps (the per-step flag epochs)."""
+NEXT #4): 2 or 3 PROCESSES, one rank per GPU, their workspaces mapped into each other with
+CUDA IPC.  The stats are pushed by the merge kernel and the dH tiles are reduced and broadcast
+by the backward kernel's RED items across the processes; every rank must match the unsharded
+oracle and the others bit for bit, over two consecutive steps (the per-step flag epochs).
+Skipped with fewer GPUs than ranks (see _need_gpus); on one GPU the same kernels run as
+co-resident rank groups of ONE launch (tests/test_gpu_p2p_emulated.py)."""
 import os
 import socket
 import subprocess
@@ -17,6 +18,17 @@ import workload
 from cce_testutil import TOL_GRAD, TOL_LOSS, TOL_LSE, rel_fro
 
 pytestmark = pytest.mark.gpu
+
+
+def _need_gpus(world):
+    """Ranks whose kernels wait on one another must run on their own GPUs: several such
+    processes time-sliced on ONE GPU can raise Xid 109 (context-switch timeout) on this
+    driver (B200_PROFILING.md), so with fewer GPUs than ranks these tests are skipped; the
+    exchange's arithmetic is covered on one GPU by test_gpu_sharded.py (split-phase) and the
+    host logic by tests/test_multiproc.py (gloo)."""
+    import torch
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs (one process per GPU); {torch.cuda.device_count()} visible")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 WORKER = r'''
@@ -28,7 +40,8 @@ from cce_testutil import to_dev
 rank, world, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
 absent = int(os.environ.get("CCE_ABSENT", "-1"))   # a rank that attaches but never steps
 dist.init_process_group("gloo", init_method="tcp://127.0.0.1:" + os.environ["CCE_PORT"], rank=rank, world_size=world)
-dev = torch.device("cuda:0")
+dev = torch.device("cuda", rank)
+torch.cuda.set_device(dev)
 p = workload.make_problem(700, 128, 3000, seed=606, ignore="bern40")
 H, W, y = to_dev(p, dev)
 N, D = H.shape
@@ -96,6 +109,7 @@ def _free_port():
 
 
 def _run(tmp_path, world, absent=-1, mode="plain"):
+    _need_gpus(world)
     import __graft_entry__
     __graft_entry__.build()
     script = tmp_path / "worker.py"

@@ -1,0 +1,173 @@
+"""The vocabulary-sharded exchange over peer memory (CCE_FLAG_P2P_COMBINE, SURVEY 8(f)
+NEXT #4; rows a9 / a10) on ONE GPU: `world` ranks as handles of one process, attached with
+cce_p2p_attach_group.  The forward's merge kernel pushes each rank's stats into every rank's
+all-ranks array (a9 fused into the kernel that produces them); the backward runs as ONE
+launch in which each rank's queue owns its own CTA pairs, so the RED items reduce every dH
+tile across the co-resident rank groups (a10 fused into the backward kernel) -- the same
+kernels and flags as across GPUs, without time-slicing ranks that wait on one another.
+
+Every rank must match the unsharded fp64 oracle (north_star tolerances) and every other rank
+bit for bit, over consecutive steps (per-step flag epochs, double-buffered stats)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2601_02609_b200 as cce
+import workload
+from cce_testutil import TOL_GRAD, TOL_LOSS, TOL_LSE, rel_fro, to_dev
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+def _bf(b):
+    return (b.astype(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def _group(V, world, N, D, W, **kw):
+    hs, wss, Ws = [], [], []
+    for r in range(world):
+        lo, hi = cce.shard_range(V, r, world)
+        h = cce.CCEHandle(vocab_total=V, vocab_offset=lo, rank=r, world=world, flags=cce.FLAG_P2P_COMBINE, **kw)
+        hs.append(h)
+        wss.append(h.workspace(N, D, hi - lo, DEV))
+        Ws.append(W[lo:hi].contiguous())
+    cce.cce_p2p_attach_group([h.h for h in hs], wss, N, D)
+    return hs, Ws
+
+
+def _step(hs, Ws, H, y, dloss=None):
+    one = torch.ones((), dtype=torch.float32, device=DEV) if dloss is None else dloss
+    fw = [h.forward(H, Wr, y) for h, Wr in zip(hs, Ws)]
+    dHs = [torch.empty_like(H) for _ in hs]
+    dWs = [torch.empty_like(Wr) for Wr in Ws]
+    for h, dH, dW in zip(hs, dHs, dWs):
+        h.backward(one, dH, dW)
+    torch.cuda.synchronize()
+    for h in hs:
+        assert cce.cce_get_error(h.h) == 0
+    return fw, dHs, dWs
+
+
+def _check(p, fw, dHs, dWs, ref, dref=None):
+    valid = p["labels"] != -100
+    loss0, lse0 = fw[0][0].item(), fw[0][1].cpu().numpy()
+    dH0 = dHs[0].view(torch.int16).cpu().numpy()
+    for (loss, lse, nv), dH in zip(fw, dHs):
+        assert loss.item() == loss0
+        assert np.array_equal(lse.cpu().numpy().view(np.int32), lse0.view(np.int32))
+        assert np.array_equal(dH.view(torch.int16).cpu().numpy(), dH0)
+        assert int(nv.item()) == int(valid.sum())
+    assert abs(loss0 - ref["loss"]) <= TOL_LOSS
+    rel = np.abs(lse0[valid] - ref["lse"][valid]) / np.maximum(np.abs(ref["lse"][valid]), 1.0)
+    assert rel.max() <= TOL_LSE
+    assert np.all(lse0[~valid] == 0.0)
+    assert np.all(dH0[~valid] == 0)
+    assert rel_fro(_bf(dH0), ref["dH"] if dref is None else dref) <= TOL_GRAD
+    dW = np.concatenate([_bf(d.view(torch.int16).cpu().numpy()) for d in dWs])
+    assert rel_fro(dW, ref["dW"]) <= TOL_GRAD
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_p2p_group_matches_oracle(world):
+    """2-8 ranks, a ragged vocabulary split (3000 / world) and a ragged row count: several dH
+    tiles and chunks per rank; two consecutive steps (epochs 1, 2)."""
+    p = workload.make_problem(700, 128, 3000, seed=606, ignore="bern40")
+    H, W, y = to_dev(p, DEV)
+    hs, Ws = _group(3000, world, 700, 128, W)
+    ref = oracle.cce(p["H"], p["W"], p["labels"])
+    for _ in range(2):
+        fw, dHs, dWs = _step(hs, Ws, H, y)
+        _check(p, fw, dHs, dWs, ref)
+    for h in hs:
+        h.close()
+
+
+def test_p2p_group_multi_chunk_and_tiles():
+    """A vocabulary shard larger than one backward chunk (8192) on every rank and 2 x 4 dH
+    tiles: the RED items start while other rank groups still run their last chunk's dW items."""
+    p = workload.make_problem(600, 896, 20000, seed=11, ignore="bern40")
+    H, W, y = to_dev(p, DEV)
+    hs, Ws = _group(20000, 2, 600, 896, W)
+    ref = oracle.cce(p["H"], p["W"], p["labels"])
+    fw, dHs, dWs = _step(hs, Ws, H, y)
+    _check(p, fw, dHs, dWs, ref)
+    for h in hs:
+        h.close()
+
+
+@pytest.mark.parametrize("mode", ["ls", "rms"])
+def test_p2p_group_regularised_loss_and_rmsnorm(mode):
+    """The exchange carries the label-smoothing logit sums (4th stat) and feeds the RMSNorm
+    prologue's backward (dH reduced across ranks before dX / dgamma)."""
+    p = workload.make_problem(700, 128, 3000, seed=606, ignore="bern40")
+    H, W, y = to_dev(p, DEV)
+    kw = dict(label_smoothing=0.1, z_loss=1e-4) if mode == "ls" else {}
+    hs, Ws = _group(3000, 2, 700, 128, W, **kw)
+    one = torch.ones((), dtype=torch.float32, device=DEV)
+    if mode == "ls":
+        ref = oracle.cce(p["H"], p["W"], p["labels"], label_smoothing=0.1, z_loss=1e-4)
+        fw, dHs, dWs = _step(hs, Ws, H, y)
+        _check(p, fw, dHs, dWs, ref)
+    else:
+        Xb, gb = workload.make_rmsnorm_inputs(606, 700, 128)
+        X = torch.from_numpy(Xb.view(np.int16)).view(torch.bfloat16).to(DEV)
+        g = torch.from_numpy(gb.view(np.int16)).view(torch.bfloat16).to(DEV)
+        ref = oracle.cce_rmsnorm(Xb, gb, p["W"], p["labels"], eps=1e-6)
+        fw = [h.forward_rmsnorm(X, g, 1e-6, Wr, y) for h, Wr in zip(hs, Ws)]
+        dXs = [torch.empty_like(X) for _ in hs]
+        dgs = [torch.empty_like(g) for _ in hs]
+        dWs = [torch.empty_like(Wr) for Wr in Ws]
+        for h, dX, dg, dW in zip(hs, dXs, dgs, dWs):
+            h.backward_rmsnorm(one, dX, dg, dW)
+        torch.cuda.synchronize()
+        for h in hs:
+            assert cce.cce_get_error(h.h) == 0
+        assert abs(fw[0][0].item() - ref["loss"]) <= TOL_LOSS
+        for dX in dXs:
+            assert torch.equal(dX.view(torch.int16), dXs[0].view(torch.int16))
+        assert rel_fro(_bf(dXs[0].view(torch.int16).cpu().numpy()), ref["dX"]) <= TOL_GRAD
+        assert rel_fro(np.concatenate([_bf(d.view(torch.int16).cpu().numpy()) for d in dWs]), ref["dW"]) <= TOL_GRAD
+    for h in hs:
+        h.close()
+
+
+def test_p2p_group_forward_only_loop():
+    """Back-to-back forwards without a backward (evaluation): the double-buffered stats
+    exchange keeps step e + 1 from overwriting what a rank still reads for step e."""
+    p = workload.make_problem(700, 128, 3000, seed=606, ignore="bern40")
+    H, W, y = to_dev(p, DEV)
+    hs, Ws = _group(3000, 3, 700, 128, W)
+    losses = []
+    for step in range(4):
+        yr = torch.roll(y, step)
+        fw = [h.forward(H, Wr, yr) for h, Wr in zip(hs, Ws)]
+        losses.append([f[0] for f in fw])
+    torch.cuda.synchronize()
+    for step in range(4):
+        ref = oracle.cce(p["H"], p["W"], np.roll(p["labels"], step))
+        for l in losses[step]:
+            assert abs(l.item() - ref["loss"]) <= TOL_LOSS
+    for h in hs:
+        assert cce.cce_get_error(h.h) == 0
+        h.close()
+
+
+def test_p2p_group_out_of_order_calls_are_refused():
+    """The group defers each rank's tail to the last rank's call: a backward before the
+    group's forward is complete is refused, and a group with a foreign handle is rejected."""
+    p = workload.make_problem(300, 64, 1000, seed=3, ignore="bern40")
+    H, W, y = to_dev(p, DEV)
+    hs, Ws = _group(1000, 2, 300, 64, W)
+    hs[0].forward(H, Ws[0], y)     # rank 1 has not run its forward: nothing is finalised yet
+    with pytest.raises(cce.CCEError):
+        hs[0].backward(torch.ones((), device=DEV), torch.empty_like(H), torch.empty_like(Ws[0]))
+    hs[1].forward(H, Ws[1], y)
+    fw, dHs, dWs = _step(hs, Ws, H, y)
+    _check(p, fw, dHs, dWs, oracle.cce(p["H"], p["W"], p["labels"]))
+    lone = cce.CCEHandle(vocab_total=1000, rank=0, world=2, flags=cce.FLAG_P2P_COMBINE)
+    with pytest.raises(cce.CCEError):
+        cce.cce_p2p_attach_group([lone.h, hs[1].h], [lone.workspace(300, 64, 500, DEV), hs[1]._ws], 300, 64)
+    for h in hs + [lone]:
+        h.close()
