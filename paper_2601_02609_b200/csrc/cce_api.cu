@@ -22,6 +22,16 @@
 
 using namespace cce;
 
+#ifndef CCE_JIT_TAIL
+// the last CCE_JIT_TAIL queue items are claimed just in time (pairk::PairParams::jit_tail):
+// measured (interleaved A/B, profiles/r02b_ab_jit_tail.txt) 6% faster on a 1/8 vocabulary shard
+// (0.556 -> 0.524 ms per step), neutral on the whole vocabulary; claiming EVERY item just in
+// time starves the pipeline (+20%)
+#define CCE_JIT_TAIL 400
+#endif
+#ifndef CCE_LOOKAHEAD
+#define CCE_LOOKAHEAD 1  // backward queue: G of chunk c + LOOKAHEAD is queued before W of chunk c
+#endif
 #ifndef CCE_CHUNK
 #define CCE_CHUNK 8192  // vocabulary rows per backward chunk (Gbuf = Npad x CCE_CHUNK bf16)
 #endif
@@ -665,6 +675,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     pp.mode = 0;
     pp.n_chunks = 0;
     pp.slots = h->slots;
+    pp.jit_tail = CCE_JIT_TAIL;
     pp.sched = at<int>(ws, L.sched);
     pp.trace = static_cast<TraceRec*>(h->fwd_trace);
     pp.trace_cap = (int)(h->fwd_trace_bytes / sizeof(TraceRec));
@@ -673,6 +684,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   }
 
   // a4: merge tiles -> per-rank stats; a9: allgather across vocabulary shards
+  bool merged_final = false;
   if (!dB && N > 0) {
     // an empty shard (V_local == 0) merges zero tiles: (m=-inf, d=0, z_y=0) for every row
     ProfScope ps(h, s, 4);
@@ -683,9 +695,32 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
         push.dst[r] = reinterpret_cast<float4*>(h->peers.ws[r] + L.stats_all) + half + (size_t)h->cfg.rank * L.Npad;
       push.n = h->cfg.world;
     }
+    // one rank, no exchange: the finalize (lse, row losses, the deterministic loss reduction)
+    // runs in the merge kernel's tail
+    MergeFinalize fin{};
+    if (h->cfg.world == 1 && !h->cfg.nccl_comm && !(h->cfg.flags & (CCE_FLAG_EXTERNAL_COMBINE | CCE_FLAG_P2P_COMBINE))) {
+      const bool none = h->cfg.reduction == CCE_REDUCTION_NONE;
+      fin.on = 1;
+      fin.pos = at<int>(ws, L.pos);
+      fin.idx = at<int>(ws, L.idx);
+      fin.N = (int)N;
+      fin.lse_out = lse;
+      fin.lse_c = at<float>(ws, L.lse_c);
+      fin.loss_rows = at<float>(ws, L.loss_rows);
+      fin.loss_tok = none ? loss : nullptr;
+      fin.ls_eps = h->cfg.label_smoothing;
+      fin.z_loss = h->cfg.z_loss;
+      fin.inv_vtotal = (float)(1.0 / (double)h->cfg.vocab_total);
+      fin.err = errp;
+      fin.loss = none ? nullptr : loss;
+      fin.n_valid_out = n_valid;
+      fin.sum = h->cfg.reduction == CCE_REDUCTION_SUM ? 1 : 0;
+      fin.counter = nvp + 2;
+      merged_final = true;
+    }
     k_merge_tiles<<<(unsigned)((L.Npad + 31) / 32), 32 * MERGE_SL, 0, s>>>(
         at<float2>(ws, L.part), V_local > 0 ? (int)L.Tv : 0, (int)L.Npad, at<float>(ws, L.zy_c), nvp,
-        (h->cfg.label_smoothing > 0.f && V_local > 0) ? at<float>(ws, L.zs_part) : nullptr, stats, push);
+        (h->cfg.label_smoothing > 0.f && V_local > 0) ? at<float>(ws, L.zs_part) : nullptr, stats, push, fin);
   }
   h->have_fwd = false;
   h->norm = norm != nullptr;
@@ -750,6 +785,11 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     if (n.allgather(stats, at<float4>(ws, L.stats_all), (size_t)L.Npad * 4, kNcclFloat32, h->cfg.nccl_comm, s) != 0)
       return CCE_ERR_NCCL;
     stats_all = at<float4>(ws, L.stats_all);
+  }
+  if (merged_final) {
+    if (cudaGetLastError() != cudaSuccess) return CCE_ERR_CUDA;
+    h->have_fwd = true;
+    return CCE_OK;
   }
   return forward_tail(h, stats_all, loss, lse, n_valid, s);
 }
@@ -990,10 +1030,11 @@ static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, voi
     pp.mode = 1;
     pp.n_chunks = (int)L.n_chunks;
     pp.slots = slots;
+    pp.jit_tail = CCE_JIT_TAIL;
     // queue order: G of chunk c + 1 is queued before W of chunk c (deadlock-free iff
     // (lookahead + 1) * qblock <= slots; measured: larger blocks / lookaheads are equal)
     pp.qblock = 1;
-    pp.lookahead = 1;
+    pp.lookahead = CCE_LOOKAHEAD;
     pp.sched = at<int>(ws, L.sched);
     pp.trace = static_cast<TraceRec*>(h->trace);
     pp.trace_cap = (int)(h->trace_bytes / sizeof(TraceRec));

@@ -103,6 +103,76 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ H, long long ldh
   }
 }
 
+// The last block to arrive (threadfence + counter) sums loss_rows[0, nv) in a fixed order:
+// threads 0-255 each keep eight independent partial sums (loads in flight), then a fixed
+// shuffle tree and warp order -- the same order whatever the launch's block size, so the
+// loss is bit-identical between the kernels that end with it.  Resets the counter.
+__device__ __forceinline__ void loss_reduce_last_block(const float* __restrict__ loss_rows,
+                                                       const int* __restrict__ n_valid, const int* __restrict__ err,
+                                                       float* __restrict__ loss, int32_t* __restrict__ n_valid_out,
+                                                       int sum, int* __restrict__ counter) {
+  constexpr int RT = 256;  // reducing threads
+  __shared__ int am_last;
+  __shared__ float red[RT / 32];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) am_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  const int nv = *n_valid;
+  if (threadIdx.x < RT) {
+    float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int i0 = threadIdx.x; i0 < nv; i0 += 8 * RT) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * RT;
+        if (i < nv) a8[u] += __ldcg(loss_rows + i);
+      }
+    }
+    float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int k = 0; k < RT / 32; ++k) t += red[k];
+    float l = sum ? t : (nv > 0 ? t / (float)nv : 0.f);
+    if (*err) l = __int_as_float(0x7fc00000);
+    if (loss) *loss = l;
+    if (n_valid_out) *n_valid_out = nv;
+    *counter = 0;
+  }
+}
+
+// Per-row loss from the row's global (lse, z_y, sum z):, with label smoothing eps /
+// z-loss lambda (1 - eps)(lse - z_y) + eps (lse - sum_v z_v / V_total) + lambda lse^2.
+__device__ __forceinline__ float row_loss(float lse, float zy, float zs, float ls_eps, float z_loss, float inv_vtotal) {
+  float l = lse - zy;
+  if (ls_eps != 0.f || z_loss != 0.f) l = (1.f - ls_eps) * l + ls_eps * (lse - zs * inv_vtotal) + z_loss * lse * lse;
+  return l;
+}
+
+// world == 1 (no exchange): the finalize fused into the merge kernel (one launch less).
+struct MergeFinalize {
+  int on;
+  const int* pos;    // [N] original -> compact (-1: ignored)
+  const int* idx;    // [Npad] compact -> original
+  int N;
+  float* lse_out;    // [N] or nullptr
+  float* lse_c;      // [Npad]
+  float* loss_rows;  // [Npad]
+  float* loss_tok;   // [N] (reduction "none") or nullptr
+  float ls_eps, z_loss, inv_vtotal;
+  const int* err;
+  float* loss;       // scalar or nullptr
+  int32_t* n_valid_out;
+  int sum;
+  int* counter;
+};
+
 // CCE_FLAG_P2P_COMBINE: the merged stats also go straight into every rank's all-ranks array
 // (slot of this rank, peer memory), so the exchange needs no separate kernel (a9 fused).
 struct StatsPush {
@@ -122,7 +192,7 @@ constexpr int MERGE_SL = 16;  // tile slices per merge block (512 threads: two b
 __global__ void __launch_bounds__(32 * MERGE_SL) k_merge_tiles(const float2* __restrict__ part, int Tv, int Npad,
                                                       const float* __restrict__ zy_c, const int* __restrict__ n_valid,
                                                       const float* __restrict__ zs_part, float4* __restrict__ stats,
-                                                      const StatsPush push) {
+                                                      const StatsPush push, const MergeFinalize fin) {
   __shared__ float2 red[MERGE_SL][33];
   __shared__ float redz[MERGE_SL][33];
   const int nv = *n_valid;
@@ -184,8 +254,25 @@ __global__ void __launch_bounds__(32 * MERGE_SL) k_merge_tiles(const float2* __r
     const float4 st = make_float4(M, S, zy_c[i], Z);
     stats[i] = st;
     for (int k = 0; k < push.n; ++k) push.dst[k][i] = st;
+    if (fin.on) {  // = k_finalize_loss at world 1: m = M, d = S exp(M - M) = S
+      const float lse = M + logf(S);
+      fin.lse_c[i] = lse;
+      const float l = row_loss(lse, st.z, Z, fin.ls_eps, fin.z_loss, fin.inv_vtotal);
+      fin.loss_rows[i] = l;
+      const int n = fin.idx[i];
+      if (fin.loss_tok) fin.loss_tok[n] = l;
+      if (fin.lse_out) fin.lse_out[n] = lse;
+    }
   }
   if (push.n) __threadfence_system();  // the peer stores are visible before the flag (next kernel)
+  if (fin.on) {
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < fin.N; n += gridDim.x * blockDim.x)
+      if (fin.pos[n] < 0) {  // ignored rows: lse = 0 (reading R4), per-token loss 0
+        if (fin.lse_out) fin.lse_out[n] = 0.f;
+        if (fin.loss_tok) fin.loss_tok[n] = 0.f;
+      }
+    loss_reduce_last_block(fin.loss_rows, n_valid, fin.err, fin.loss, fin.n_valid_out, fin.sum, fin.counter);
+  }
 }
 
 
@@ -225,45 +312,12 @@ __global__ void __launch_bounds__(256) k_finalize_loss(
     }
     const float lse = m + logf(d);
     lse_c[i] = lse;
-    float l = lse - zy;
-    if (ls_eps != 0.f || z_loss != 0.f)
-      l = (1.f - ls_eps) * l + ls_eps * (lse - zs * inv_vtotal) + z_loss * lse * lse;
+    const float l = row_loss(lse, zy, zs, ls_eps, z_loss, inv_vtotal);
     loss_rows[i] = l;
     if (loss_tok) loss_tok[n] = l;
     if (lse_out) lse_out[n] = lse;
   }
-  __shared__ int am_last;
-  __shared__ float red[8];
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) am_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  const int nv = *n_valid;
-  // eight independent partial sums per thread (loads in flight), combined in a fixed order
-  float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int i0 = threadIdx.x; i0 < nv; i0 += 8 * blockDim.x) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i < nv) a8[u] += __ldcg(loss_rows + i);
-    }
-  }
-  float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
-    float l = sum ? t : (nv > 0 ? t / (float)nv : 0.f);
-    if (*err) l = __int_as_float(0x7fc00000);
-    if (loss) *loss = l;
-    if (n_valid_out) *n_valid_out = nv;
-    *counter = 0;
-  }
+  loss_reduce_last_block(loss_rows, n_valid, err, loss, n_valid_out, sum, counter);
 }
 
 // Mean loss over the valid rows in a fixed reduction order (deterministic).

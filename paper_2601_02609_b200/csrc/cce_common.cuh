@@ -21,7 +21,10 @@ namespace cce {
 constexpr int BN = 256;          // vocabulary tile of the forward partials (Tv = ceil(V / BN))
 constexpr int BK = 64;           // k-block (one 128-byte swizzle atom of bf16)
 constexpr int TMEM_COLS = 512;
-constexpr int GBUF_SLOTS = 3;    // ring of chunk dlogits buffers: G(c) reuses the slot of chunk c-3
+#ifndef CCE_SLOTS
+#define CCE_SLOTS 3
+#endif
+constexpr int GBUF_SLOTS = CCE_SLOTS;  // ring of chunk dlogits buffers: G(c) reuses the slot of chunk c-SLOTS
 constexpr float LOG2E = 1.4426950408889634f;
 
 struct GemmParams {

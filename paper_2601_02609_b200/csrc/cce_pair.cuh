@@ -94,6 +94,10 @@ struct PairParams {
   unsigned long long ready_off, done_off;    // int flag arrays in every workspace
   unsigned long long dH32_off, dHred_off;    // partial / reduced dH in every workspace
   int* err;                                  // error word (bit 2: a peer never signalled)
+  // the last jit_tail items of the queue are dequeued just in time: the scheduler claims the
+  // next item only once this pair's producer has reached the last stage of the previous one,
+  // so no pair holds claimed-but-unstarted items while others run out of work (the tail)
+  int jit_tail;
   int* sched;      // zeroed: [0] head [1] head of part 2 | g_done[n] | w_done[n] | dh_flag[n_dt * t256]
   TraceRec* trace;
   int trace_cap;
@@ -175,6 +179,18 @@ __device__ PItem decode(const PairParams& P, const PCounts& k, int q) {
     }
   }
   return make_item(PT_END, 0, 0, 0, 0, 0, 0, q);
+}
+
+// Queue positions [0, total): every item before PT_END (the P2P RED items included).
+__device__ __forceinline__ int queue_total(const PairParams& P, const PCounts& k) {
+  if (P.mode == 0) return k.t256 * k.tv;
+  int total = 0;
+  for (int c = 0; c < P.n_chunks; ++c) {
+    const int w = p_chunk_width(P.g, c);
+    total += p_n_g(k, w) + k.n_dh + p_n_dw(k, w);
+  }
+  if (P.world > 1 && P.peers.ws[0] != nullptr && k.n_dh > P.prank) total += (k.n_dh - P.prank + P.world - 1) / P.world;
+  return total;
 }
 
 // ------------------------------------------------------------------ epilogues (per CTA)
@@ -603,6 +619,7 @@ __device__ __forceinline__ void pair_body(const CUtensorMap* tmHcK, const CUtens
   uint64_t* rempty_p = rempty_l + PRING;    // leader: peer consumers (producer + epilogue warps)
   PItem* ring = reinterpret_cast<PItem*>(rempty_p + PRING);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + PRING);
+  volatile int* prod_cnt = reinterpret_cast<volatile int*>(tmem_slot + 1);  // leader: items whose last stage the producer reached
   float* xchg = reinterpret_cast<float*>(smem + PSTAGES * PSTAGE_BYTES + 1024);
   uint8_t* stage_base = smem + PSTAGES * PSTAGE_BYTES + 2048;
 
@@ -629,6 +646,7 @@ __device__ __forceinline__ void pair_body(const CUtensorMap* tmHcK, const CUtens
       mbar_init(&rempty_l[r], 2 + PEPI_WARPS);  // leader producer + MMA + epilogue warps
       mbar_init(&rempty_p[r], 1 + PEPI_WARPS);  // peer producer + epilogue warps
     }
+    *prod_cnt = 0;
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_pair(tmem_slot, TMEM_COLS);
@@ -651,17 +669,15 @@ __device__ __forceinline__ void pair_body(const CUtensorMap* tmHcK, const CUtens
       // up to PRING items ahead of the consumers (hides the atomic and DSMEM latency).
       uint32_t rs = 0, rph = 0;
       // split backward (NCCL): the last chunk's DW items are the queue's last p_n_dw items
-      int q_split = 0;
-      if (P.part != 0) {
-        int total = 0;
-        for (int c = 0; c < P.n_chunks; ++c) {
-          const int w = p_chunk_width(g, c);
-          total += p_n_g(k, w) + k.n_dh + p_n_dw(k, w);
-        }
-        q_split = total - p_n_dw(k, p_chunk_width(g, P.n_chunks - 1));
-      }
+      const int total = queue_total(P, k);
+      const int q_split = P.part != 0 ? total - p_n_dw(k, p_chunk_width(g, P.n_chunks - 1)) : 0;
+      const int jit_from = (P.part == 1 ? q_split : total) - P.jit_tail;
+      int published = 0, q_last = -1;
       while (true) {
+        if (q_last >= jit_from && published > 0)
+          while (*prod_cnt < published) __nanosleep(32);  // just in time: the producer is on its last stage
         const int q = P.part == 2 ? q_split + atomicAdd(head2, 1) : atomicAdd(head, 1);
+        q_last = q;
         PItem it = decode(P, k, q);
         if (P.part == 1 && q >= q_split) it = make_item(PT_END, 0, 0, 0, 0, 0, 0, q);
         if (P.trace) it.t_deq = gtimer();
@@ -676,12 +692,14 @@ __device__ __forceinline__ void pair_body(const CUtensorMap* tmHcK, const CUtens
         mbar_arrive_cluster(mapa_shared(smem_u32(&rfull_bar[rs]), 1));
         if (++rs == PRING) { rs = 0; rph ^= 1; }
         if (it.type == PT_END) break;
+        ++published;
       }
     }
   } else if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer (both CTAs): next item from the local ring, dependencies, loads
       uint32_t stage = 0, phase = 0, rs = 0, rph = 0;
+      int n_started = 0;
       const uint32_t full_leader0 = mapa_shared(smem_u32(&full_bar[0]), 0);
       while (true) {
         if (rank == 0) mbar_wait(&rfull_bar[rs], rph);
@@ -715,7 +733,9 @@ __device__ __forceinline__ void pair_body(const CUtensorMap* tmHcK, const CUtens
         // one 3-D box per operand per stage (KPS k-blocks); a ragged last stage: the k-blocks
         // past num_kb are zero-filled (OOB) or zero rows / columns and their MMAs are skipped
         const int ns = (it.num_kb + KPS - 1) / KPS;
+        if (ns == 0 && rank == 0) *prod_cnt = ++n_started;
         for (int st = 0; st < ns; ++st) {
+          if (st == ns - 1 && rank == 0) *prod_cnt = ++n_started;  // the scheduler may claim the next item
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if (P.trace && st == 0) tl0 = gtimer();
           uint8_t* a = sA + stage * KA_BYTES;

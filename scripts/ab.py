@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="qwen05b")
+    ap.add_argument("--vslice", type=int, default=0, help="time one vocabulary shard: the first n rows of W")
     ap.add_argument("--sample-ms", type=int, default=20)
     ap.add_argument("--rest", type=float, default=1.0, help="idle seconds before each measurement")
     args = ap.parse_args()
@@ -44,11 +45,16 @@ def main():
     H = torch.from_numpy(p["H"].view(np.int16)).view(torch.bfloat16).to(dev)
     W = torch.from_numpy(p["W"].view(np.int16)).view(torch.bfloat16).to(dev)
     y = torch.from_numpy(p["labels"]).to(dev)
+    V = c.V
+    if args.vslice:
+        V = args.vslice
+        W = W[:V].contiguous()
+        y = torch.where(y >= 0, y % V, y)
     loss = torch.empty((), dtype=torch.float32, device=dev)
     lse = torch.empty(c.N, dtype=torch.float32, device=dev)
     nvt = torch.empty((), dtype=torch.int32, device=dev)
     dH = torch.empty((c.N, c.D), dtype=torch.bfloat16, device=dev)
-    dW = torch.empty((c.V, c.D), dtype=torch.bfloat16, device=dev)
+    dW = torch.empty((V, c.D), dtype=torch.bfloat16, device=dev)
     one = torch.ones((), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -75,17 +81,17 @@ def main():
         cce._lib = libs[name]
         old = {k: os.environ.get(k) for k in env}
         os.environ.update(env)
-        h = cce.CCEHandle(vocab_total=c.V, flags=flags)
+        h = cce.CCEHandle(vocab_total=V, flags=flags)
         # WSOFF=<bytes>: place the workspace at this offset from a 2 MiB-aligned base
         off = int(env.get("WSOFF", "-1"))
         if off >= 0:
-            need = cce.cce_workspace_bytes(h.h, c.N, c.D, c.V)
+            need = cce.cce_workspace_bytes(h.h, c.N, c.D, V)
             raw = torch.empty(need + off + (4 << 20), dtype=torch.uint8, device=dev)
             base = (-raw.data_ptr()) % (2 << 20)
             ws = raw[base + off: base + off + need]
             h._ws_keep = raw
         else:
-            ws = h.workspace(c.N, c.D, c.V, dev)
+            ws = h.workspace(c.N, c.D, V, dev)
         cce.cce_forward(h.h, H, W, y, loss, lse, nvt, ws, stream)
         cce.cce_backward(h.h, one, dH, dW, stream)
         torch.cuda.synchronize()
