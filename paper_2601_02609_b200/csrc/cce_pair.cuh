@@ -105,7 +105,31 @@ struct PairParams {
 
 struct PCounts {
   int nv, t256, n_dt, n_dh, tv;
+  int rg;  // row tiles per L2 group (the FWD / G items of a group share its Hc rows through L2)
 };
+
+// Hc rows of one L2 group: the forward and G items sweep the vocabulary tiles over a group of
+// row tiles whose Hc block stays L2-resident, then move to the next group.  Sweeping ALL rows
+// per vocabulary tile re-reads Hc from DRAM once per vocabulary tile when Hc exceeds the L2
+// (configs[4] shard: N = 32768, D = 3584, Hc = 235 MB -> 17.8 GB of DRAM reads per forward);
+// grouping re-reads only the (vocabulary) operand once per group instead.  At D = 896 every
+// row tile fits one group: the order is unchanged.
+constexpr long long L2_GROUP_BYTES = 48ll << 20;
+__device__ __forceinline__ int l2_group_rows(int t256, int D) {
+  const long long per_tile = (long long)PM * D * 2;
+  const int rg = (int)(L2_GROUP_BYTES / per_tile);
+  return rg < 1 ? 1 : (rg > t256 ? t256 : rg);
+}
+
+// item index i of a (row tiles x vocabulary tiles) block swept group by group: vocabulary
+// tile outer, row tile inner within a group of rg row tiles
+__device__ __forceinline__ void grouped_tile(int i, int t256, int rg, int ntv, int& row_tile, int& vtile) {
+  const int per_group = rg * ntv;
+  const int grp = i / per_group, ii = i - grp * per_group;
+  const int rows_in = min(rg, t256 - grp * rg);
+  vtile = ii / rows_in;
+  row_tile = grp * rg + (ii - vtile * rows_in);
+}
 
 __device__ __forceinline__ int dtile_N(int D, int dt) {
   const int rem = D - dt * PN;
@@ -131,7 +155,11 @@ __device__ __forceinline__ int p_n_dw(const PCounts& k, int w) { return ((w + PM
 __device__ PItem decode(const PairParams& P, const PCounts& k, int q) {
   const GemmParams& g = P.g;
   if (P.mode == 0) {
-    if (q < k.t256 * k.tv) return make_item(PT_FWD, 0, (q % k.t256) * PM, (q / k.t256) * PN, PN, g.D / BK, 0, q);
+    if (q < k.t256 * k.tv) {
+      int rt, vt;
+      grouped_tile(q, k.t256, k.rg, k.tv, rt, vt);
+      return make_item(PT_FWD, 0, rt * PM, vt * PN, PN, g.D / BK, 0, q);
+    }
     return make_item(PT_END, 0, 0, 0, 0, 0, 0, q);
   }
   // chunk blocks of B = P.qblock chunks: G(blocks 0 .. L-1), then for each block b:
@@ -154,7 +182,11 @@ __device__ PItem decode(const PairParams& P, const PCounts& k, int q) {
     const int c0 = c * g.C;
     if (isG) {
       const int cnt = p_n_g(k, w);
-      if (r < cnt) return make_item(PT_G, c, (r % k.t256) * PM, c0 + (r / k.t256) * PN, PN, g.D / BK, 0, q);
+      if (r < cnt) {
+        int rt, vt;
+        grouped_tile(r, k.t256, k.rg, (w + PN - 1) / PN, rt, vt);
+        return make_item(PT_G, c, rt * PM, c0 + vt * PN, PN, g.D / BK, 0, q);
+      }
       r -= cnt;
     } else {
       if (r < k.n_dh) {
@@ -662,6 +694,7 @@ __device__ __forceinline__ void pair_body(const CUtensorMap* tmHcK, const CUtens
   k.n_dt = (g.D + PN - 1) / PN;
   k.n_dh = k.t256 * k.n_dt;
   k.tv = (g.V_local + PN - 1) / PN;
+  k.rg = l2_group_rows(k.t256, g.D);
 
   if (warp == 3) {
     if (lane == 0 && rank == 0) {
