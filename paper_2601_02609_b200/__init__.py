@@ -114,8 +114,9 @@ def lib():
         L.cce_p2p_export.restype = st
         L.cce_p2p_attach.argtypes = [p, p, i64, i64, p, p]
         L.cce_p2p_attach.restype = st
-        L.cce_p2p_attach_group.argtypes = [p, p, i32, i64, i64]
-        L.cce_p2p_attach_group.restype = st
+        if hasattr(L, "cce_p2p_attach_group"):  # (older builds, loaded by scripts/ab.py, lack it)
+            L.cce_p2p_attach_group.argtypes = [p, p, i32, i64, i64]
+            L.cce_p2p_attach_group.restype = st
         L.cce_step_host_async.argtypes = [p, p, i64, i64, p, p, i64, i64, p, p, p, p, sz, p, sz, p, p]
         L.cce_step_host_async.restype = st
         L.cce_nccl_unique_id.argtypes = [p]

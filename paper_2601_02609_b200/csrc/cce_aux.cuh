@@ -11,9 +11,11 @@ namespace cce {
 
 // a0: range check + stable compaction of the non-ignored rows (P:2076-2079:
 // rows with y == ignore_index are skipped; the mean divides by their count,
-// P:899).  One block of 1024 threads walks the labels in tiles of 1024 (thread t owns
-// label n0 + t: coalesced), ranks the valid ones with a warp ballot + block scan and
-// carries the running count, so the compact order equals the original row order.
+// P:899).  One block of 1024 threads; per pass over 8192 labels every thread owns 8
+// CONSECUTIVE labels (two 16-byte loads), counts its valid ones, and one block-wide exclusive
+// scan of the per-thread counts (warp shuffles + a 32-entry warp scan) gives each thread its
+// first compact position, so the compact order equals the original row order.  (The earlier
+// form scanned 8 tiles of 1024 one after another: 16 block barriers per 8192 labels.)
 // Out-of-range labels set err and are treated as ignored.
 // The same launch also resets the per-forward state the later kernels accumulate into
 // (saves three memsets): the target logits zy_c [Npad] (written only by the tile that owns
@@ -32,51 +34,65 @@ __global__ void __launch_bounds__(1024) k_label_scan(const int32_t* __restrict__
     sched2[1] = 0;
     *fin_counter = 0;
   }
+  constexpr int PT = 8;  // labels per thread per pass
+  const bool vec = (reinterpret_cast<uintptr_t>(labels) & 15u) == 0;
   int base = 0, bad = 0;
-  constexpr int ST = 8;  // tiles per super-tile: all its labels are loaded before the scans
-  for (int s0 = 0; s0 < N; s0 += ST * 1024) {
-    int ys[ST];
+  for (int s0 = 0; s0 < N; s0 += PT * 1024) {
+    const int n0 = s0 + PT * t;
+    int ys[PT];
+    if (vec && n0 + PT <= N) {
+      const int4 a = *reinterpret_cast<const int4*>(labels + n0);
+      const int4 b = *reinterpret_cast<const int4*>(labels + n0 + 4);
+      ys[0] = a.x; ys[1] = a.y; ys[2] = a.z; ys[3] = a.w; ys[4] = b.x; ys[5] = b.y; ys[6] = b.z; ys[7] = b.w;
+    } else {
 #pragma unroll
-    for (int k = 0; k < ST; ++k) {
-      const int n = s0 + k * 1024 + t;
-      ys[k] = n < N ? labels[n] : ignore_index;
+      for (int k = 0; k < PT; ++k) ys[k] = n0 + k < N ? labels[n0 + k] : ignore_index;
     }
-#pragma unroll 1
-  for (int k = 0; k < ST; ++k) {
-    const int n = s0 + k * 1024 + t;
-    const int y = ys[k];
-    bool v = false;
-    if (n < N && y != ignore_index) {
-      if (y < 0 || (long long)y >= vocab_total) bad = 1;
-      else v = true;
+    unsigned vmask = 0;
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int y = ys[k];
+      if (n0 + k < N && y != ignore_index) {
+        if (y < 0 || (long long)y >= vocab_total) bad = 1;
+        else vmask |= 1u << k;
+      }
     }
-    const unsigned m = __ballot_sync(0xffffffffu, v);
-    const int wpre = __popc(m & ((1u << lane) - 1u));
-    if (lane == 0) warp_tot[w] = __popc(m);
+    const int cnt = __popc(vmask);
+    int incl = cnt;  // inclusive scan of the counts within the warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_tot[w] = incl;
     __syncthreads();
     if (w == 0) {
-      int s = warp_tot[lane];
+      int v = warp_tot[lane];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += u;
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
       }
-      warp_tot[lane] = s;  // inclusive over warps
+      warp_tot[lane] = v;  // inclusive over warps
     }
     __syncthreads();
-    if (n < N) {
-      if (v) {
-        const int off = base + (w > 0 ? warp_tot[w - 1] : 0) + wpre;
-        pos[n] = off;
-        idx[off] = n;
-        labels_c[off] = y;
-      } else {
-        pos[n] = -1;
+    int off = base + (w > 0 ? warp_tot[w - 1] : 0) + incl - cnt;
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      const int n = n0 + k;
+      if (n < N) {
+        if (vmask >> k & 1u) {
+          pos[n] = off;
+          idx[off] = n;
+          labels_c[off] = ys[k];
+          ++off;
+        } else {
+          pos[n] = -1;
+        }
       }
     }
     base += warp_tot[31];
-    __syncthreads();  // warp_tot is rewritten by the next tile
-  }
+    __syncthreads();  // warp_tot is rewritten by the next pass
   }
   const int any_bad = __syncthreads_or(bad);
   if (t == 0) {
@@ -95,11 +111,33 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ H, long long ldh
   const int rows = min(Npad, ((nv + 127) / 128) * 128);
   const int vec_per_row = D / 8;
   const long long total = (long long)rows * vec_per_row;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / vec_per_row), c = (int)(i % vec_per_row);
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < nv) v = *reinterpret_cast<const uint4*>(H + (long long)idx[r] * ldh + c * 8);
-    *reinterpret_cast<uint4*>(Hc + (long long)r * D + c * 8) = v;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // four 16-byte copies per thread in flight (the row-index loads first, then the data loads,
+  // then the stores): the kernel is latency-bound at this size otherwise
+  constexpr int U = 4;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += U * stride) {
+    int src[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      const int r = (int)(i / vec_per_row);
+      src[u] = (i < total && r < nv) ? idx[r] : -1;
+    }
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      const int c = (int)(i % vec_per_row);
+      v[u] = src[u] >= 0 ? *reinterpret_cast<const uint4*>(H + (long long)src[u] * ldh + c * 8) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < total) {
+        const int r = (int)(i / vec_per_row), c = (int)(i % vec_per_row);
+        *reinterpret_cast<uint4*>(Hc + (long long)r * D + c * 8) = v[u];
+      }
+    }
   }
 }
 

@@ -133,13 +133,15 @@ def main():
             ck = smp.stop()
             if ck and ck["sm_mhz"]:
                 res[name]["mhz"].append((ck["sm_mhz"], ck.get("power_w_max"), ck.get("reasons")))
+            res[name].setdefault("rounds", []).append(statistics.median([a.elapsed_time(c_) for a, b, c_ in ev]))
             res[name]["step"] += [a.elapsed_time(c_) for a, b, c_ in ev]
             res[name]["fwd"] += [a.elapsed_time(b) for a, b, c_ in ev]
             res[name]["bwd"] += [b.elapsed_time(c_) for a, b, c_ in ev]
     for name, _, _ in vs:
         d = res[name]
         print(f"{name:24s} step {statistics.median(d['step']):7.3f} ms  fwd {statistics.median(d['fwd']):7.3f}"
-              f"  bwd {statistics.median(d['bwd']):7.3f}  (min step {min(d['step']):.3f})  sm MHz {d['mhz']}", flush=True)
+              f"  bwd {statistics.median(d['bwd']):7.3f}  (min step {min(d['step']):.3f})  per-round medians "
+              f"{[round(x, 3) for x in d['rounds']]}  sm MHz {d['mhz']}", flush=True)
     for name, (h, _) in handles.items():
         cce._lib = libs[name]
         h.close()
