@@ -25,6 +25,8 @@ def main():
     import __graft_entry__
     import paper_2601_02609_b200 as cce
     import workload
+    if os.environ.get("CCE_LIB"):  # time another build of libcce.so
+        cce.LIB_PATH = os.environ["CCE_LIB"]
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)

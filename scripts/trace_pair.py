@@ -62,7 +62,7 @@ cce.cce_debug_trace(h.h, None)
 allrec = buf.view(torch.int64).view(2, CAP, 16).cpu().numpy().astype(np.uint64)
 np.savez(out, bwd=allrec[0], fwd=allrec[1])
 print(f"{cfg}: fwd {ev[0].elapsed_time(ev[1]):.3f} ms, bwd {ev[1].elapsed_time(ev[2]):.3f} ms")
-NAMES = {0: "FWD", 1: "G", 2: "DW", 3: "DH"}
+NAMES = {0: "FWD", 1: "G", 2: "DW", 3: "DH", 5: "RED", 6: "OPT"}
 for name, rec in (("forward", allrec[1]), ("backward", allrec[0])):
     rec = rec[rec[:, 5] > 0]
     if len(rec) == 0:
