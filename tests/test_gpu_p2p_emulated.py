@@ -171,3 +171,46 @@ def test_p2p_group_out_of_order_calls_are_refused():
         cce.cce_p2p_attach_group([lone.h, hs[1].h], [lone.workspace(300, 64, 500, DEV), hs[1]._ws], 300, 64)
     for h in hs + [lone]:
         h.close()
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_p2p_group_full_size_bench_config(world):
+    """The bench configuration (Qwen2.5-0.5B head, N = 8192, V = 151,936 split `world` ways,
+    40% packed padding): every rank's loss and every valid row's LSE against the fp64 oracle
+    golden, sampled dW rows of every shard against the oracle, bit-identical ranks."""
+    import hashlib
+    import os
+    gold = os.path.join(os.path.dirname(__file__), "golden", "qwen05b_seed42.npz")
+    if not os.path.exists(gold):
+        pytest.skip("golden file missing (scripts/make_golden.py)")
+    g = np.load(gold)
+    p = workload.make_config("qwen05b", seed=42)
+    assert hashlib.sha256(p["W"].tobytes()).hexdigest() == str(g["W_sha256"])
+    H, W, y = to_dev(p, DEV)
+    N, D = H.shape
+    V = W.shape[0]
+    hs, Ws = _group(V, world, N, D, W)
+    fw, dHs, dWs = _step(hs, Ws, H, y)
+    valid = p["labels"] != -100
+    ref_loss = float(np.mean(g["lse"] - g["zy"]))
+    lse0 = fw[0][1].cpu().numpy()
+    for (loss, lse, nv), dH in zip(fw, dHs):
+        assert abs(loss.item() - ref_loss) <= TOL_LOSS
+        assert np.array_equal(lse.cpu().numpy().view(np.int32), lse0.view(np.int32))
+        assert torch.equal(dH.view(torch.int16), dHs[0].view(torch.int16))
+    rel = np.abs(lse0[valid] - g["lse"]) / np.maximum(np.abs(g["lse"]), 1.0)
+    assert rel.max() <= TOL_LSE
+    lse_all = np.zeros(N)
+    lse_all[g["valid_rows"]] = g["lse"]
+    for r in range(world):
+        lo, hi = cce.shard_range(V, r, world)
+        pick = np.unique(np.array([lo, lo + 1, (lo + hi) // 2, hi - 1]))
+        ref = oracle.dW_rows(p["H"], p["W"], p["labels"], lse_all, 1.0 / len(g["valid_rows"]), pick)
+        got = _bf(dWs[r].view(torch.int16).cpu().numpy()[pick - lo])
+        assert rel_fro(got, ref) <= TOL_GRAD, r
+    rows = g["valid_rows"]
+    pick = rows[np.linspace(0, len(rows) - 1, 8).astype(int)]
+    _, _, dH_ref = oracle.rows(p["H"], p["W"], p["labels"], pick, scale=1.0 / len(rows))
+    assert rel_fro(_bf(dHs[0].view(torch.int16).cpu().numpy()[pick]), dH_ref) <= TOL_GRAD
+    for h in hs:
+        h.close()

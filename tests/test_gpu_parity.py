@@ -53,6 +53,10 @@ def test_multi_tile_shapes(dev, N, D, V, ign):
     (700, 3584, 6100, "bern40"),   # configs[4] hidden size (Qwen2.5-7B head), 14 x 256 hidden tiles
     (260, 8192, 2300, "bern40"),   # Llama-3-70B-class hidden size: 128 k-blocks per logit tile, 32 hidden tiles
     (333, 5120, 4100, "none"),     # 5120 = 20 hidden tiles, ragged rows / vocabulary
+    # L2 row groups (cce_pair.cuh l2_group_rows, 48 MB of Hc per group): 12 row tiles per group
+    # at D = 8192 -> 13 tiles = a full group + a ragged group of ONE tile; 6 per group at D = 16384
+    (3300, 8192, 1000, "none"),
+    (2100, 16384, 700, "none"),
 ])
 def test_large_hidden_sizes(dev, N, D, V, ign):
     """The wide-hidden configurations: D = 2048 / 3584 / 4096 (8 / 14 / 16 hidden tiles
