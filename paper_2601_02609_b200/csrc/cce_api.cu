@@ -550,7 +550,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
                                int32_t* n_valid, void* workspace, size_t workspace_bytes, void* stream,
                                const NormArgs* norm);
 static cce_status forward_tail(cce_handle* h, const float4* stats_all, float* loss, float* lse, int32_t* n_valid,
-                               cudaStream_t s);
+                               cudaStream_t s, const int* wait_flags = nullptr);
 
 cce_status cce_forward(cce_handle* h, const void* H, int64_t N, int64_t D, int64_t ldh, const void* W,
                        int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
@@ -691,9 +691,13 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
     StatsPush push{};
     if (h->cfg.flags & CCE_FLAG_P2P_COMBINE) {  // a9 fused: every rank's slot `rank`, including ours
       const size_t half = (size_t)((h->epoch + 1) & 1) * h->cfg.world * L.Npad;  // this step's half
-      for (int r = 0; r < h->cfg.world; ++r)
+      for (int r = 0; r < h->cfg.world; ++r) {
         push.dst[r] = reinterpret_cast<float4*>(h->peers.ws[r] + L.stats_all) + half + (size_t)h->cfg.rank * L.Npad;
+        push.flag[r] = reinterpret_cast<int*>(h->peers.ws[r] + L.p2p_flags) + P2P_STATS * P2P_MAX + h->cfg.rank;
+      }
       push.n = h->cfg.world;
+      push.epoch = h->epoch + 1;  // this forward's epoch (incremented below)
+      push.counter = nvp + 3;
     }
     // one rank, no exchange: the finalize (lse, row losses, the deterministic loss reduction)
     // runs in the merge kernel's tail
@@ -737,9 +741,11 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
   if (h->cfg.flags & CCE_FLAG_P2P_COMBINE) {
     // a9 over peer memory: push this rank's stats into every rank's all-ranks array, raise
     // the flag, wait for every rank's
-    const int epoch = ++h->epoch;  // (the merge above already stored the stats into every rank)
-    k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_STATS, h->cfg.rank, h->cfg.world,
-                                  epoch);
+    // (the merge above stored the stats into every rank and raised this rank's flag everywhere)
+    const int epoch = ++h->epoch;
+    if (N == 0)
+      k_p2p_signal<<<1, 32, 0, s>>>(h->peers, (unsigned long long)L.p2p_flags, P2P_STATS, h->cfg.rank, h->cfg.world,
+                                    epoch);
     if (h->group_n) {
       // one-GPU group emulation: every rank pushes and signals before any rank waits
       h->grp_fwd_pending = true;
@@ -756,17 +762,14 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
         cce_handle* g = h->group[q];
         g->grp_fwd_pending = false;
         const Layout Lq = layout(g->N, g->D, g->V_local, g->cfg.world, g->chunk, g->slots, g->cfg.flags);
-        k_p2p_wait<<<1, 32, 0, s>>>(at<int>(g->ws, Lq.p2p_flags), P2P_STATS, g->cfg.world, epoch,
-                                    at<int>(g->ws, Lq.scal) + 1);
         const cce_status st = forward_tail(g, at<float4>(g->ws, Lq.stats_all) + (size_t)(epoch & 1) * g->cfg.world * Lq.Npad,
-                                           g->p_loss, g->p_lse, g->p_nv, s);
+                                           g->p_loss, g->p_lse, g->p_nv, s, at<int>(g->ws, Lq.p2p_flags) + P2P_STATS * P2P_MAX);
         if (st != CCE_OK) return st;
       }
       return CCE_OK;
     }
-    k_p2p_wait<<<1, 32, 0, s>>>(at<int>(ws, L.p2p_flags), P2P_STATS, h->cfg.world, epoch, errp);
     return forward_tail(h, at<float4>(ws, L.stats_all) + (size_t)(epoch & 1) * h->cfg.world * L.Npad, loss, lse,
-                        n_valid, s);
+                        n_valid, s, at<int>(ws, L.p2p_flags) + P2P_STATS * P2P_MAX);  // the wait runs in the finalize
   }
   if (h->cfg.flags & CCE_FLAG_EXTERNAL_COMBINE) {
     // a9 done by the caller: it gathers every rank's `stats` into `stats_all`, then calls
@@ -796,7 +799,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
 
 // a4 (global) + loss: per-row LSE / loss from the (gathered) per-rank stats.
 static cce_status forward_tail(cce_handle* h, const float4* stats_all, float* loss, float* lse, int32_t* n_valid,
-                               cudaStream_t s) {
+                               cudaStream_t s, const int* wait_flags) {
   const int64_t N = h->N;
   const Layout L = layout(N, h->D, h->V_local, h->cfg.world, h->chunk, h->slots, h->cfg.flags);
   void* ws = h->ws;
@@ -810,7 +813,7 @@ static cce_status forward_tail(cce_handle* h, const float4* stats_all, float* lo
         at<float>(ws, L.loss_rows), h->cfg.label_smoothing, h->cfg.z_loss, (float)(1.0 / (double)h->cfg.vocab_total),
         h->cfg.reduction == CCE_REDUCTION_NONE ? loss : nullptr, nvp, errp,
         h->cfg.reduction == CCE_REDUCTION_NONE ? nullptr : loss, n_valid, h->cfg.reduction == CCE_REDUCTION_SUM ? 1 : 0,
-        nvp + 2);
+        nvp + 2, wait_flags, h->epoch, errp);
   } else {
     ProfScope ps(h, s, 4);
     k_loss<<<1, 1024, 0, s>>>(at<float>(ws, L.loss_rows), nvp, errp,
@@ -1116,6 +1119,7 @@ static cce_status backward_tail(cce_handle* h, void* dH, void* dgamma, bool norm
   float* dH32 = at<float>(ws, L.dH32);
   const bool seq = (h->cfg.flags & CCE_FLAG_DH_SEQ_SHARD) != 0;
   float* dHo = seq ? at<float>(ws, L.dHo) : nullptr;
+  const int* p2p_done = nullptr;  // peer-memory exchange: the scatter waits for the reduced tiles
   if (N > 0) {
     if (V_local == 0 && cudaMemsetAsync(dH32, 0, (size_t)L.Npad * D * 4, s) != cudaSuccess) return CCE_ERR_CUDA;
     if (seq) {
@@ -1138,7 +1142,10 @@ static cce_status backward_tail(cce_handle* h, void* dH, void* dgamma, bool norm
     if ((h->cfg.flags & CCE_FLAG_P2P_COMBINE) && h->cfg.world > 1) {
       // a10 over peer memory, fused into the backward kernel (RED items, tile by tile): here
       // only wait until every tile's reduced dH has arrived in this rank's reduced array
-      k_p2p_wait_tiles<<<1, 256, 0, s>>>(at<int>(ws, L.p2p_done), nvp, (int)D, h->epoch, nvp + 1);
+      // (the dH scatter below waits for every tile's done flags itself; the RMSNorm backward
+      // reads the reduced dH from its own kernel, so a wait launch precedes it)
+      if (norm) k_p2p_wait_tiles<<<1, 256, 0, s>>>(at<int>(ws, L.p2p_done), nvp, (int)D, h->epoch, nvp + 1);
+      else p2p_done = at<int>(ws, L.p2p_done);
       dH32 = at<float>(ws, L.dHred);
     }
     if (h->cfg.nccl_comm && !h->dH_reduced) {
@@ -1178,10 +1185,9 @@ static cce_status backward_tail(cce_handle* h, void* dH, void* dgamma, bool norm
       return CCE_OK;
     }
     ProfScope ps(h, s, 4);
-    k_scatter_dH<<<grid_for((long long)N * D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(dH32, at<int>(ws, L.pos), (int)N,
-                                                                                     (int)D, dH,
-                                                                                     (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0,
-                                                                                     (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0);
+    k_scatter_dH<<<grid_for((long long)N * D / 8, 256, 8 * h->num_sms), 256, 0, s>>>(
+        dH32, at<int>(ws, L.pos), (int)N, (int)D, dH, (h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 1 : 0,
+        (h->cfg.flags & CCE_FLAG_ACCUMULATE) ? 1 : 0, p2p_done, nvp, h->epoch, nvp + 1);
   } else if (norm && !(h->cfg.flags & CCE_FLAG_ACCUMULATE)) {
     // no rows: dgamma = 0
     if (cudaMemsetAsync(dgamma, 0, (size_t)D * ((h->cfg.flags & CCE_FLAG_GRAD_FP32) ? 4 : 2), s) != cudaSuccess)

@@ -9,6 +9,17 @@
 
 namespace cce {
 
+__device__ __forceinline__ int ld_acquire_sys_i(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // a0: range check + stable compaction of the non-ignored rows (P:2076-2079:
 // rows with y == ignore_index are skipped; the mean divides by their count,
 // P:899).  One block of 1024 threads; per pass over 8192 labels every thread owns 8
@@ -32,7 +43,8 @@ __global__ void __launch_bounds__(1024) k_label_scan(const int32_t* __restrict__
   if (t == 0) {
     sched2[0] = 0;
     sched2[1] = 0;
-    *fin_counter = 0;
+    fin_counter[0] = 0;  // the finalize's last-block counter
+    fin_counter[1] = 0;  // the merge kernel's (peer-memory signal)
   }
   constexpr int PT = 8;  // labels per thread per pass
   const bool vec = (reinterpret_cast<uintptr_t>(labels) & 15u) == 0;
@@ -216,6 +228,12 @@ struct MergeFinalize {
 struct StatsPush {
   float4* dst[8];  // every rank's stats_all + rank * Npad (peer memory), or unused
   int n;           // number of destinations (0: no push)
+  // the flag (kind P2P_STATS, this rank) in every rank, raised to `epoch` by the last block to
+  // finish (counter: last-block pattern) after a system-scope fence -- the signal fused into
+  // the kernel that produced the stats
+  int* flag[8];
+  int epoch;
+  int* counter;
 };
 
 constexpr int MERGE_SL = 16;  // tile slices per merge block (512 threads: two blocks per SM, one wave)
@@ -302,7 +320,16 @@ __global__ void __launch_bounds__(32 * MERGE_SL) k_merge_tiles(const float2* __r
       if (fin.lse_out) fin.lse_out[n] = lse;
     }
   }
-  if (push.n) __threadfence_system();  // the peer stores are visible before the flag (next kernel)
+  if (push.n) {
+    __threadfence_system();  // this block's peer stores are visible before the flag
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(push.counter, 1) == (int)gridDim.x - 1) {
+      *push.counter = 0;
+      __threadfence_system();
+      for (int r = 0; r < push.n; ++r)
+        asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(push.flag[r]), "r"(push.epoch) : "memory");
+    }
+  }
   if (fin.on) {
     for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < fin.N; n += gridDim.x * blockDim.x)
       if (fin.pos[n] < 0) {  // ignored rows: lse = 0 (reading R4), per-token loss 0
@@ -328,7 +355,19 @@ __global__ void __launch_bounds__(256) k_finalize_loss(
     float* __restrict__ lse_out, float* __restrict__ lse_c, float* __restrict__ loss_rows, float ls_eps,
     float z_loss, float inv_vtotal, float* __restrict__ loss_tok, const int* __restrict__ n_valid,
     const int* __restrict__ err, float* __restrict__ loss, int32_t* __restrict__ n_valid_out, int sum,
-    int* __restrict__ counter) {
+    int* __restrict__ counter, const int* __restrict__ wait_flags, int epoch, int* __restrict__ err_w) {
+  if (wait_flags) {
+    // peer-memory exchange: every rank's stats flag (kind P2P_STATS) must show this step's epoch
+    // before the rows are merged; bounded like k_p2p_wait (a missing peer sets err bit 4)
+    if ((int)threadIdx.x < world) {
+      const unsigned long long t0 = gtimer_ns();
+      while (ld_acquire_sys_i(wait_flags + threadIdx.x) < epoch) {
+        if (gtimer_ns() - t0 > 5000000000ull) { atomicOr(err_w, 4); break; }
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
+  }
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     const int i = pos[n];
     if (i < 0) {
@@ -338,14 +377,14 @@ __global__ void __launch_bounds__(256) k_finalize_loss(
     }
     float m = -INFINITY, zy = 0.f, zs = 0.f;
     for (int r = 0; r < world; ++r) {
-      const float4 st = stats_all[(size_t)r * Npad + i];
+      const float4 st = __ldcg(stats_all + (size_t)r * Npad + i);  // written by other kernels / GPUs: L2
       m = fmaxf(m, st.x);
       zy += st.z;
       zs += st.w;
     }
     float d = 0.f;
     for (int r = 0; r < world; ++r) {
-      const float4 st = stats_all[(size_t)r * Npad + i];
+      const float4 st = __ldcg(stats_all + (size_t)r * Npad + i);
       if (st.y > 0.f) d += st.y * expf(st.x - m);
     }
     const float lse = m + logf(d);
@@ -388,7 +427,22 @@ __global__ void __launch_bounds__(1024) k_loss(const float* __restrict__ loss_ro
 // a8: dH rows back to the original positions in bf16; ignored rows are bit-zero.
 // fp32 = 1: dH is float32; accumulate = 1: dH += gradient (ignored rows untouched).
 __global__ void k_scatter_dH(const float* __restrict__ dH32, const int* __restrict__ pos, int N, int D,
-                             void* __restrict__ dH_out, int fp32, int accumulate) {
+                             void* __restrict__ dH_out, int fp32, int accumulate, const int* __restrict__ done = nullptr,
+                             const int* __restrict__ n_valid = nullptr, int epoch = 0, int* __restrict__ err = nullptr) {
+  if (done) {
+    // peer-memory exchange: every dH tile's reduced sum has arrived (the RED items raised
+    // done[tile][cta] = epoch); bounded like k_p2p_wait_tiles
+    const int t256 = (*n_valid + 255) / 256, n_dt = (D + 255) / 256;
+    const int n = 2 * t256 * n_dt;
+    const unsigned long long t0 = gtimer_ns();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      while (ld_acquire_sys_i(done + i) < epoch) {
+        if (gtimer_ns() - t0 > 5000000000ull) { atomicOr(err, 4); break; }
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
+  }
   const int vec_per_row = D / 8;
   const long long total = (long long)N * vec_per_row;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -398,8 +452,8 @@ __global__ void k_scatter_dH(const float* __restrict__ dH32, const int* __restri
       if (accumulate && r < 0) continue;
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
       if (r >= 0) {
-        a = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8);
-        b = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8 + 4);
+        a = __ldcg(reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8));
+        b = __ldcg(reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8 + 4));
       }
       if (fp32) {
         float4* d = reinterpret_cast<float4*>(static_cast<float*>(dH_out) + (long long)n * D + c * 8);
@@ -430,8 +484,8 @@ __global__ void k_scatter_dH(const float* __restrict__ dH32, const int* __restri
     __nv_bfloat16* dH = static_cast<__nv_bfloat16*>(dH_out);
     uint4 out = make_uint4(0, 0, 0, 0);
     if (r >= 0) {
-      const float4 a = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8);
-      const float4 b = *reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8 + 4);
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8));
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(dH32 + (long long)r * D + c * 8 + 4));
       __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y), p1 = __floats2bfloat162_rn(a.z, a.w);
       __nv_bfloat162 p2 = __floats2bfloat162_rn(b.x, b.y), p3 = __floats2bfloat162_rn(b.z, b.w);
       out.x = *reinterpret_cast<uint32_t*>(&p0);

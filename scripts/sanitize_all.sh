@@ -1,4 +1,6 @@
 #!/usr/bin/env bash
+# NOTE: compute-sanitizer has since been closed on the GPU pool (runs under it left GPUs needing a
+# reset); the committed logs in profiles/r02_sanitize/ are from before that.  Do not run this there.
 # compute-sanitizer memcheck / racecheck / synccheck over the pair kernels (tiny config and a
 # 6-chunk problem), the design-B kernels, and the peer-memory path (one-GPU group emulation:
 # 2 ranks in one process, one backward launch; never ranks time-sliced as processes).
