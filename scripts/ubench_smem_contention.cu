@@ -11,9 +11,14 @@
 #include "../paper_2601_02609_b200/csrc/sm100.cuh"
 using namespace cce;
 
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
 template <int AMN, int BMN>
 __global__ void __launch_bounds__(384, 1) kc(int iters, int nw, int mode, unsigned long long* out,
-                                           unsigned long long* bytes_out) {
+                                           unsigned long long* bytes_out, const uint8_t* gsrc, int fill) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar[8];
@@ -30,6 +35,28 @@ __global__ void __launch_bounds__(384, 1) kc(int iters, int nw, int mode, unsign
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = slot;
+  __shared__ uint64_t fbar[2];
+  if (fill && warp == 3 && lane == 0) {
+    // TMA-like operand fills: 32 KB bulk copies from L2-resident global memory into a 64 KB
+    // region (two alternating halves), as the pair kernel's producer loads 32 KB per k-block
+    mbar_init(&fbar[0], 1);
+    mbar_init(&fbar[1], 1);
+    fence_barrier_init();
+    uint32_t ph[2] = {0, 0};
+    unsigned long long nb = 0;
+    const unsigned long long t0 = clock64();
+    const uint32_t dst0 = smem_u32(smem + 131072 + 32768);  // beyond the noise region
+    while (clock64() - t0 < (unsigned long long)iters * 980ull) {  // two 32 KB copies in flight
+      const int hb = (int)(nb & 1);
+      if (nb >= 2) { mbar_wait(&fbar[hb], ph[hb]); ph[hb] ^= 1; }
+      mbar_arrive_expect_tx(&fbar[hb], 32768);
+      bulk_g2s(dst0 + (uint32_t)(hb * 32768), gsrc + ((blockIdx.x * 7 + nb) & 63) * 32768, 32768, smem_u32(&fbar[hb]));
+      ++nb;
+    }
+    for (int hb = 0; hb < 2; ++hb) if (nb > (unsigned long long)hb) mbar_wait(&fbar[hb], ph[hb]);
+    atomicAdd(bytes_out + 296 + blockIdx.x, nb * 32768);
+    atomicAdd(bytes_out + 444 + blockIdx.x, clock64() - t0);
+  }
   if (warp == 0) {
     if (lane == 0 && rank == 0) {
       const uint32_t a = smem_u32(smem), b = smem_u32(smem + 65536);
@@ -107,15 +134,17 @@ __global__ void __launch_bounds__(384, 1) kc(int iters, int nw, int mode, unsign
   if (warp == 1) tmem_dealloc_pair(tmem, 512);
 }
 
+static uint8_t* g_src = nullptr;
 template <int AMN, int BMN>
-void run(int nw, int mode, int iters) {
+void run(int nw, int mode, int iters, int fill = 0) {
   const int grid = 148;
   unsigned long long *d, *bts;
+  if (!g_src) { cudaMalloc(&g_src, 64 * 32768); cudaMemset(g_src, 1, 64 * 32768); }
   cudaMalloc(&d, grid * 8);
-  cudaMalloc(&bts, 2 * grid * 8);
-  cudaMemset(bts, 0, 2 * grid * 8);
+  cudaMalloc(&bts, 4 * grid * 8);
+  cudaMemset(bts, 0, 4 * grid * 8);
   auto k = kc<AMN, BMN>;
-  const int sm = 200 * 1024;
+  const int sm = 228 * 1024 - 2048;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -128,20 +157,20 @@ void run(int nw, int mode, int iters) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k, iters, nw, mode, d, bts);
-  cudaMemset(bts, 0, 2 * grid * 8);
-  cudaLaunchKernelEx(&cfg, k, iters, nw, mode, d, bts);
+  cudaLaunchKernelEx(&cfg, k, iters, nw, mode, d, bts, (const uint8_t*)g_src, fill);
+  cudaMemset(bts, 0, 4 * grid * 8);
+  cudaLaunchKernelEx(&cfg, k, iters, nw, mode, d, bts, (const uint8_t*)g_src, fill);
   cudaError_t err = cudaDeviceSynchronize();
-  unsigned long long h[256], hb[512];
+  unsigned long long h[256], hb[1024];
   cudaMemcpy(h, d, grid * 8, cudaMemcpyDeviceToHost);
-  cudaMemcpy(hb, bts, 2 * grid * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hb, bts, 4 * grid * 8, cudaMemcpyDeviceToHost);
   unsigned long long mx = 0;
   for (int i = 0; i < grid; i += 2) mx = h[i] > mx ? h[i] : mx;
   const double per_kb = (double)mx / iters / 2;
   static const char* names[6] = {"", "st   ", "st+ld", "ffma ", "ex2  ", "sts  "};
-  printf("A_%s B_%s other warps %d mode %s err=%s: cycles per 64-k-block %.1f (floor 512); other-warp smem traffic %.1f B/clk/SM\n",
-         AMN ? "MN" : "K ", BMN ? "MN" : "K ", nw, names[mode], cudaGetErrorString(err), per_kb,
-         nw ? (double)hb[0] / (double)hb[148] : 0.0);
+  printf("A_%s B_%s other warps %d mode %s fill %d err=%s: cycles per 64-k-block %.1f (floor 512); other-warp smem traffic %.1f B/clk/SM; fills %.1f B/clk/SM\n",
+         AMN ? "MN" : "K ", BMN ? "MN" : "K ", nw, names[mode], fill, cudaGetErrorString(err), per_kb,
+         nw && hb[148] ? (double)hb[0] / (double)hb[148] : 0.0, fill && hb[444] ? (double)hb[296] / (double)hb[444] : 0.0);
   cudaFree(d);
   cudaFree(bts);
 }
@@ -155,5 +184,9 @@ int main() {
   // one noise warp on each SMSP (warp 4..7; the MMA issuer is warp 0 = SMSP 0): ALU, MUFU, st.shared
   for (int mode : {3, 4, 5})
     for (int w : {4, 5, 6, 7}) run<0, 0>(w, mode, it);
+  // with TMA-like operand fills streaming into shared memory (warp 3): alone, and with st.shared
+  // bursts from warps on the OTHER SMSPs (not the issuer's)
+  run<0, 0>(0, 1, it, 1);
+  for (int w : {5, 6, 7}) run<0, 0>(w, 5, it, 1);
   return 0;
 }
