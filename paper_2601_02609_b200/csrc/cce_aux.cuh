@@ -22,11 +22,11 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
 
 // a0: range check + stable compaction of the non-ignored rows (P:2076-2079:
 // rows with y == ignore_index are skipped; the mean divides by their count,
-// P:899).  One block of 1024 threads; per pass over 8192 labels every thread owns 8
-// CONSECUTIVE labels (two 16-byte loads), counts its valid ones, and one block-wide exclusive
-// scan of the per-thread counts (warp shuffles + a 32-entry warp scan) gives each thread its
-// first compact position, so the compact order equals the original row order.  (The earlier
-// form scanned 8 tiles of 1024 one after another: 16 block barriers per 8192 labels.)
+// P:899).  One block of 1024 threads; per pass over 8192 labels each warp owns a contiguous
+// block of 256 (lane-strided: coalesced), ranks its valid labels with 8 ballots, and one
+// block-wide scan of the 32 warp counts gives every warp its offset, so the compact order
+// equals the original row order.  (The round-1 form scanned 8 tiles of 1024 one after
+// another: 16 block barriers per 8192 labels.)
 // Out-of-range labels set err and are treated as ignored.
 // The same launch also resets the per-forward state the later kernels accumulate into
 // (saves three memsets): the target logits zy_c [Npad] (written only by the tile that owns
@@ -46,37 +46,29 @@ __global__ void __launch_bounds__(1024) k_label_scan(const int32_t* __restrict__
     fin_counter[0] = 0;  // the finalize's last-block counter
     fin_counter[1] = 0;  // the merge kernel's (peer-memory signal)
   }
-  constexpr int PT = 8;  // labels per thread per pass
-  const bool vec = (reinterpret_cast<uintptr_t>(labels) & 15u) == 0;
+  // per pass of 8192 labels: warp w owns the contiguous block [s0 + 256 w, s0 + 256 (w + 1)),
+  // lane l its labels l + 32 j (j = 0..7: coalesced loads and stores); the compact position of
+  // (j, l) is the warp's offset + the valid labels of sub-blocks j' < j + those of lanes < l
+  constexpr int PT = 8;
   int base = 0, bad = 0;
   for (int s0 = 0; s0 < N; s0 += PT * 1024) {
-    const int n0 = s0 + PT * t;
+    const int b0 = s0 + 256 * w;
     int ys[PT];
-    if (vec && n0 + PT <= N) {
-      const int4 a = *reinterpret_cast<const int4*>(labels + n0);
-      const int4 b = *reinterpret_cast<const int4*>(labels + n0 + 4);
-      ys[0] = a.x; ys[1] = a.y; ys[2] = a.z; ys[3] = a.w; ys[4] = b.x; ys[5] = b.y; ys[6] = b.z; ys[7] = b.w;
-    } else {
+    unsigned mk[PT];
+    int cnt = 0;
 #pragma unroll
-      for (int k = 0; k < PT; ++k) ys[k] = n0 + k < N ? labels[n0 + k] : ignore_index;
-    }
-    unsigned vmask = 0;
-#pragma unroll
-    for (int k = 0; k < PT; ++k) {
-      const int y = ys[k];
-      if (n0 + k < N && y != ignore_index) {
-        if (y < 0 || (long long)y >= vocab_total) bad = 1;
-        else vmask |= 1u << k;
+    for (int j = 0; j < PT; ++j) {
+      const int n = b0 + 32 * j + lane;
+      ys[j] = n < N ? labels[n] : ignore_index;
+      bool v = false;
+      if (n < N && ys[j] != ignore_index) {
+        if (ys[j] < 0 || (long long)ys[j] >= vocab_total) bad = 1;
+        else v = true;
       }
+      mk[j] = __ballot_sync(0xffffffffu, v);
+      cnt += __popc(mk[j]);
     }
-    const int cnt = __popc(vmask);
-    int incl = cnt;  // inclusive scan of the counts within the warp
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += u;
-    }
-    if (lane == 31) warp_tot[w] = incl;
+    if (lane == 0) warp_tot[w] = cnt;
     __syncthreads();
     if (w == 0) {
       int v = warp_tot[lane];
@@ -88,20 +80,22 @@ __global__ void __launch_bounds__(1024) k_label_scan(const int32_t* __restrict__
       warp_tot[lane] = v;  // inclusive over warps
     }
     __syncthreads();
-    int off = base + (w > 0 ? warp_tot[w - 1] : 0) + incl - cnt;
+    int off = base + (w > 0 ? warp_tot[w - 1] : 0);
+    const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int k = 0; k < PT; ++k) {
-      const int n = n0 + k;
+    for (int j = 0; j < PT; ++j) {
+      const int n = b0 + 32 * j + lane;
       if (n < N) {
-        if (vmask >> k & 1u) {
-          pos[n] = off;
-          idx[off] = n;
-          labels_c[off] = ys[k];
-          ++off;
+        if (mk[j] >> lane & 1u) {
+          const int o = off + __popc(mk[j] & lt);
+          pos[n] = o;
+          idx[o] = n;
+          labels_c[o] = ys[j];
         } else {
           pos[n] = -1;
         }
       }
+      off += __popc(mk[j]);
     }
     base += warp_tot[31];
     __syncthreads();  // warp_tot is rewritten by the next pass
@@ -358,7 +352,7 @@ __global__ void __launch_bounds__(256) k_finalize_loss(
     int* __restrict__ counter, const int* __restrict__ wait_flags, int epoch, int* __restrict__ err_w) {
   if (wait_flags) {
     // peer-memory exchange: every rank's stats flag (kind P2P_STATS) must show this step's epoch
-    // before the rows are merged; bounded like k_p2p_wait (a missing peer sets err bit 4)
+    // before the rows are merged; bounded at 5 s (a missing peer sets err bit 4)
     if ((int)threadIdx.x < world) {
       const unsigned long long t0 = gtimer_ns();
       while (ld_acquire_sys_i(wait_flags + threadIdx.x) < epoch) {
@@ -431,7 +425,7 @@ __global__ void k_scatter_dH(const float* __restrict__ dH32, const int* __restri
                              const int* __restrict__ n_valid = nullptr, int epoch = 0, int* __restrict__ err = nullptr) {
   if (done) {
     // peer-memory exchange: every dH tile's reduced sum has arrived (the RED items raised
-    // done[tile][cta] = epoch); bounded like k_p2p_wait_tiles
+    // done[tile][cta] = epoch); bounded at 5 s like k_p2p_wait_tiles
     const int t256 = (*n_valid + 255) / 256, n_dt = (D + 255) / 256;
     const int n = 2 * t256 * n_dt;
     const unsigned long long t0 = gtimer_ns();

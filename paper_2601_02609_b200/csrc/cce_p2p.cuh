@@ -2,13 +2,13 @@
 // (CCE_FLAG_P2P_COMBINE): every rank's workspace is mapped into
 // every other rank (CUDA IPC), and
 //   a9  the merged per-row stats are PUSHED into each rank's all-ranks array by the
-//       kernel that produced them (k_merge_tiles, stores over NVLink), then a release
-//       flag per (kind, source rank) is raised in every peer and waited for;
+//       kernel that produced them (k_merge_tiles, stores over NVLink), whose last block then
+//       raises a release flag per source rank in every peer; k_finalize_loss waits for them;
 //   a10 inside the backward kernel (cce_pair.cuh, RED items): as soon as every rank's
 //       last-chunk dH tile is final, the tile's owner (tile % world) sums it over the ranks
 //       in rank order (loads over NVLink, deterministic) and stores the sum into every
 //       rank's reduced-dH array (a reduce-scatter and an all-gather fused, overlapping the
-//       remaining MMA items tile by tile); k_p2p_wait_tiles gates the scatter on it.
+//       remaining MMA items tile by tile); the dH scatter (k_scatter_dH) waits for it.
 // Flags are epoch counters (one step = one epoch) in each rank's workspace; waits are
 // bounded (a missing peer sets the error word instead of hanging the GPU).
 #pragma once
@@ -49,23 +49,9 @@ __global__ void k_p2p_signal(PeerPtrs peers, unsigned long long flags_off, int k
   }
 }
 
-// Wait until every rank raised (kind) for this epoch; bounded: on timeout set err bit 4.
-__global__ void k_p2p_wait(const int* __restrict__ flags, int kind, int world, int epoch, int* err) {
-  const int r = threadIdx.x;
-  if (r >= world) return;
-  const int* f = flags + kind * P2P_MAX + r;
-  const unsigned long long t0 = p2p_now();
-  while (ld_acquire_sys(f) < epoch) {
-    if (p2p_now() - t0 > P2P_TIMEOUT_NS) {
-      atomicOr(err, 4);
-      return;
-    }
-    __nanosleep(1000);
-  }
-}
-
 // Wait until every tile's RED item raised done[tile][cta] for this epoch (tiles from the
-// device-side n_valid); bounded like k_p2p_wait.
+// device-side n_valid); bounded: on timeout set err bit 4 (used before the RMSNorm backward;
+// the dH scatter waits itself).
 __global__ void k_p2p_wait_tiles(const int* __restrict__ done, const int* __restrict__ n_valid, int D, int epoch,
                                  int* err) {
   const int t256 = (*n_valid + 255) / 256, n_dt = (D + 255) / 256;
