@@ -67,6 +67,7 @@ class ClockSampler:
         self.index = index
         self.period_ms = period_ms
         self.rows = []
+        self.stamped = []
         self.proc = None
 
     def start(self):
@@ -81,17 +82,35 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.stamped.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
-    def stop(self):
+    def wait_first(self, timeout_s: float = 5.0):
+        """nvidia-smi can take a second to print its first sample: wait for it, so that the
+        timed region that follows is covered."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.stamped and time.perf_counter() - t0 < timeout_s:
+            time.sleep(0.01)
+
+    def stop(self, window=None):
+        """window = (t0, t1) perf_counter bounds of the timed region: the statistics use the
+        samples taken inside it (the sampler's output is buffered, so a sample is stamped when
+        read: up to one period late)."""
         if self.proc is None:
             return None
+        time.sleep(2 * self.period_ms / 1000.0)   # the samples of the region's last periods
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
+        self.rows = [r for t, r in self.stamped]
+        inside = None
+        if window is not None:
+            t0, t1 = window
+            inside = [r for t, r in self.stamped if t0 <= t <= t1 + self.period_ms / 1000.0]
+            if inside:
+                self.rows = inside
         if not self.rows:
             return None
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
@@ -119,7 +138,8 @@ class ClockSampler:
                 pass
         return {"sm_mhz": statistics.median(load) if load else (statistics.median(sm) if sm else None),
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(self.rows),
-                "samples_under_load": len(load), "power_w_max": max(pw) if pw else None}
+                "samples_under_load": len(load), "power_w_max": max(pw) if pw else None,
+                "samples_in_timed_region": len(inside) if inside is not None else None}
 
 
 def _all_host_cores():
@@ -387,7 +407,8 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(local, period_ms=10)  # the timed region is ~0.1 s: sample every 10 ms
     sampler.start()
-    time.sleep(0.3)
+    sampler.wait_first()
+    time.sleep(0.05)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -401,8 +422,9 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    wall = time.perf_counter() - wall0
-    clocks = sampler.stop()
+    wall1 = time.perf_counter()
+    wall = wall1 - wall0
+    clocks = sampler.stop(window=(wall0, wall1))
     launches = cce.cce_kernel_launches(h.h) - l0
     prof = cce.cce_profile_read(h.h, reset=True)
     cce.cce_profile_enable(h.h, False)
