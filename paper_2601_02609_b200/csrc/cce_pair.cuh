@@ -109,12 +109,15 @@ struct PCounts {
 };
 
 // Hc rows of one L2 group: the forward and G items sweep the vocabulary tiles over a group of
-// row tiles whose Hc block stays L2-resident, then move to the next group.  Sweeping ALL rows
+// row tiles whose Hc block (32 MB) stays L2-resident, then move to the next group.  Sweeping ALL rows
 // per vocabulary tile re-reads Hc from DRAM once per vocabulary tile when Hc exceeds the L2
 // (configs[4] shard: N = 32768, D = 3584, Hc = 235 MB -> 17.8 GB of DRAM reads per forward);
 // grouping re-reads only the (vocabulary) operand once per group instead.  At D = 896 every
 // row tile fits one group: the order is unchanged.
-constexpr long long L2_GROUP_BYTES = 48ll << 20;
+#ifndef CCE_L2_GROUP_MB
+#define CCE_L2_GROUP_MB 32
+#endif
+constexpr long long L2_GROUP_BYTES = (long long)CCE_L2_GROUP_MB << 20;  // 16 / 32 / 48 / 80 MB A/B: profiles/r02b_l2_group_size.txt
 __device__ __forceinline__ int l2_group_rows(int t256, int D) {
   const long long per_tile = (long long)PM * D * 2;
   const int rg = (int)(L2_GROUP_BYTES / per_tile);

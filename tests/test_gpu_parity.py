@@ -53,8 +53,8 @@ def test_multi_tile_shapes(dev, N, D, V, ign):
     (700, 3584, 6100, "bern40"),   # configs[4] hidden size (Qwen2.5-7B head), 14 x 256 hidden tiles
     (260, 8192, 2300, "bern40"),   # Llama-3-70B-class hidden size: 128 k-blocks per logit tile, 32 hidden tiles
     (333, 5120, 4100, "none"),     # 5120 = 20 hidden tiles, ragged rows / vocabulary
-    # L2 row groups (cce_pair.cuh l2_group_rows, 48 MB of Hc per group): 12 row tiles per group
-    # at D = 8192 -> 13 tiles = a full group + a ragged group of ONE tile; 6 per group at D = 16384
+    # L2 row groups (cce_pair.cuh l2_group_rows, 32 MB of Hc per group): 8 row tiles per group
+    # at D = 8192 -> 13 tiles = 8 + 5; 4 per group at D = 16384 -> 9 tiles = 4 + 4 + a ragged ONE
     (3300, 8192, 1000, "none"),
     (2100, 16384, 700, "none"),
 ])
