@@ -58,3 +58,25 @@ def test_committed_r02_lines_carry_in_bench_parity():
         d = json.loads(open(os.path.join(ROOT, "profiles", f)).read().strip().splitlines()[-1])
         assert d["parity"]["ok"] is True and d["parity"]["rows_checked"] == 4915, f
         assert d["parity"]["lse_max_rel_err"] <= 1e-3 and d["parity"]["loss_abs_err"] <= 2e-3
+
+
+def test_clock_sampler_keeps_the_timed_region_samples():
+    """The clock record covers the timed region: samples are stamped as they arrive and the
+    statistics use the ones inside (t0, t1 + one period); throttle reasons are collected."""
+    sys.path.insert(0, ROOT)
+    import bench
+    s = bench.ClockSampler(0, period_ms=10)
+    s.proc = object()  # (no nvidia-smi on the CPU box: feed rows directly)
+    s.t = type("T", (), {"join": lambda self, timeout=None: None})()
+    s.proc = type("P", (), {"terminate": lambda self: None, "wait": lambda self, timeout=None: 0})()
+    row = lambda mhz, w, cap: ["0", str(mhz), "1965", str(w), "0x0", "Not Active", "Not Active", "Not Active", cap]  # noqa: E731
+    s.stamped = [(0.5, row(1965, 100.0, "Not Active")),      # idle lead-in, outside the window
+                 (1.00, row(1400, 900.0, "Active")), (1.01, row(1380, 950.0, "Active")),
+                 (1.02, row(1390, 920.0, "Not Active")),
+                 (3.0, row(1965, 80.0, "Not Active"))]       # after the window
+    c = s.stop(window=(0.99, 1.02))
+    assert c["samples_in_timed_region"] == 3 and c["samples"] == 3
+    assert c["sm_mhz"] == 1390 and c["reasons"] == ["sw_power_cap"] and c["power_w_max"] == 950.0
+    s.stamped = [(0.5, row(1965, 100.0, "Not Active"))]       # nothing inside: fall back to every sample
+    c = s.stop(window=(0.99, 1.02))
+    assert c["samples"] == 1 and c["samples_in_timed_region"] == 0
