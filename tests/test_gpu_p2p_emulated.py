@@ -214,3 +214,58 @@ def test_p2p_group_full_size_bench_config(world):
     assert rel_fro(_bf(dHs[0].view(torch.int16).cpu().numpy()[pick]), dH_ref) <= TOL_GRAD
     for h in hs:
         h.close()
+
+
+@pytest.mark.parametrize("mode", ["sum", "none", "fp32", "fp32_accumulate"])
+def test_p2p_group_reductions_and_gradient_modes(mode):
+    """The exchange under the other reductions (sum; none with per-row upstream gradients, the
+    per-token losses identical on every rank) and gradient modes (float32 dH / dW, accumulated
+    into existing buffers: the reduced dH is added once, on every rank)."""
+    p = workload.make_problem(700, 256, 9000, seed=21, ignore="bern40")
+    H, W, y = to_dev(p, DEV)
+    world = 3
+    reduction = mode if mode in ("sum", "none") else "mean"
+    flags = cce.FLAG_GRAD_FP32 | (cce.FLAG_ACCUMULATE if mode == "fp32_accumulate" else 0) if mode.startswith("fp32") else 0
+    hs, Ws, wss = [], [], []
+    for r in range(world):
+        lo, hi = cce.shard_range(9000, r, world)
+        h = cce.CCEHandle(vocab_total=9000, vocab_offset=lo, rank=r, world=world, flags=cce.FLAG_P2P_COMBINE | flags,
+                          reduction=reduction)
+        hs.append(h)
+        wss.append(h.workspace(700, 256, hi - lo, DEV))
+        Ws.append(W[lo:hi].contiguous())
+    cce.cce_p2p_attach_group([h.h for h in hs], wss, 700, 256)
+    if reduction == "none":
+        dl_np = np.random.default_rng(3).standard_normal(700).astype(np.float32).astype(np.float64) / 700
+        dloss = torch.tensor(dl_np, dtype=torch.float32, device=DEV)
+    else:
+        dl_np = 0.5 / 420
+        dloss = torch.tensor(dl_np, dtype=torch.float32, device=DEV)
+    ref = oracle.cce(p["H"], p["W"], p["labels"], dloss=dl_np, reduction=reduction)
+    gdt = torch.float32 if flags & cce.FLAG_GRAD_FP32 else torch.bfloat16
+    init = mode == "fp32_accumulate"
+    g0 = torch.Generator(device="cpu").manual_seed(5)
+    dH0 = torch.randn(H.shape, generator=g0).to(DEV) * 1e-3 if init else None
+    dHs = [dH0.clone() if init else torch.empty(H.shape, dtype=gdt, device=DEV) for _ in hs]
+    dW0 = [torch.randn(Wr.shape, generator=g0).to(DEV) * 1e-3 if init else None for Wr in Ws]
+    dWs = [dW0[r].clone() if init else torch.empty(Wr.shape, dtype=gdt, device=DEV) for r, Wr in enumerate(Ws)]
+    fw = [h.forward(H, Wr, y) for h, Wr in zip(hs, Ws)]
+    for h, dH, dW in zip(hs, dHs, dWs):
+        h.backward(dloss, dH, dW)
+    torch.cuda.synchronize()
+    valid = p["labels"] != -100
+    for h, (loss, lse, nv), dH in zip(hs, fw, dHs):
+        assert cce.cce_get_error(h.h) == 0
+        assert torch.equal(loss, fw[0][0]) and torch.equal(dH, dHs[0])
+    l0 = fw[0][0].cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(l0 - np.asarray(ref["loss"]))) <= TOL_LOSS
+    f64 = (lambda t: t.cpu().numpy().astype(np.float64)) if gdt == torch.float32 else (
+        lambda t: _bf(t.view(torch.int16).cpu().numpy()))
+    dH_ref = ref["dH"] + (dH0.cpu().numpy().astype(np.float64) if init else 0.0)
+    assert rel_fro(f64(dHs[0]), dH_ref) <= TOL_GRAD
+    dW_ref = ref["dW"] + (np.concatenate([d.cpu().numpy() for d in dW0]).astype(np.float64) if init else 0.0)
+    assert rel_fro(np.concatenate([f64(d) for d in dWs]), dW_ref) <= TOL_GRAD
+    if not init:
+        assert np.all(f64(dHs[0])[~valid] == 0)
+    for h in hs:
+        h.close()
