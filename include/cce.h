@@ -383,8 +383,9 @@ cce_status cce_p2p_attach(cce_handle *h, void *workspace, int64_t N, int64_t D, 
  * which CTA pairs [r p, (r + 1) p) run rank r's queue (p = (SMs / 2) / world; the RED items
  * reduce across the co-resident rank groups), then every rank's tail.  So call the forwards of
  * ranks 0 .. world-1 in order on one stream, then the backwards in order on the same stream
- * (CCE_ERR_NO_FORWARD otherwise).  Same kernels and arithmetic as cce_p2p_attach; the
- * handles must outlive one another's use (destroy them together).
+ * (CCE_ERR_NO_FORWARD otherwise).  Same kernels and arithmetic as cce_p2p_attach.  Destroy the
+ * handles together: once one member is destroyed, the others return CCE_ERR_INVALID_VALUE from
+ * cce_forward / cce_backward.
  */
 cce_status cce_p2p_attach_group(cce_handle *const *hs, void *const *workspaces, int32_t world, int64_t N, int64_t D);
 

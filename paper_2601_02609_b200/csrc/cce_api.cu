@@ -74,6 +74,7 @@ struct cce_handle {
   // until the group's last rank calls, which issues them for every rank (one backward launch)
   cce_handle* group[P2P_MAX] = {};
   int group_n = 0;
+  bool group_broken = false;  // another member was destroyed: this handle refuses further steps
   bool grp_fwd_pending = false, grp_bwd_pending = false;
   cudaStream_t grp_stream = nullptr;
   pairk::PairLaunch grp_launch;             // this rank's prepared backward launch (host copy)
@@ -487,6 +488,8 @@ cce_status cce_destroy(cce_handle* h) {
   for (auto p : h->opened)
     if (p) cudaIpcCloseMemHandle(p);
   if (h->grp_launch_dev) cudaFree(h->grp_launch_dev);
+  for (int q = 0; q < h->group_n; ++q)  // the other members must not reach this handle any more
+    if (h->group[q] && h->group[q] != h) h->group[q]->group_broken = true;
   delete h;
   return CCE_OK;
 }
@@ -575,7 +578,7 @@ static cce_status forward_impl(cce_handle* h, const void* H, int64_t N, int64_t 
                                int64_t V_local, int64_t ldw, const int32_t* labels, float* loss, float* lse,
                                int32_t* n_valid, void* workspace, size_t workspace_bytes, void* stream,
                                const NormArgs* norm) {
-  if (!h || !loss) return CCE_ERR_INVALID_VALUE;
+  if (!h || !loss || h->group_broken) return CCE_ERR_INVALID_VALUE;
   if (N < 0 || D <= 0 || V_local < 0 || ldh < D || ldw < D) return CCE_ERR_INVALID_VALUE;
   if (N > 0 && (!H || !labels)) return CCE_ERR_INVALID_VALUE;
   if (V_local > 0 && !W) return CCE_ERR_INVALID_VALUE;
@@ -922,7 +925,7 @@ static cce_status seq_rows_out(cce_handle* h, const Layout& L, void* dH, cudaStr
 
 static cce_status backward_impl(cce_handle* h, const float* dloss, void* dH, void* dW, const cce_adamw_params* opt,
                                 void* stream, void* dgamma, bool norm) {
-  if (!h) return CCE_ERR_INVALID_VALUE;
+  if (!h || h->group_broken) return CCE_ERR_INVALID_VALUE;
   if (!h->have_fwd) return CCE_ERR_NO_FORWARD;
   if (!dloss || (h->N > 0 && !dH) || (h->V_local > 0 && !dW)) return CCE_ERR_INVALID_VALUE;
   if ((dH && !aligned16(dH)) || (dW && !aligned16(dW))) return CCE_ERR_UNSUPPORTED;

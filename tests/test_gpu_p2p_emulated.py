@@ -169,6 +169,9 @@ def test_p2p_group_out_of_order_calls_are_refused():
     lone = cce.CCEHandle(vocab_total=1000, rank=0, world=2, flags=cce.FLAG_P2P_COMBINE)
     with pytest.raises(cce.CCEError):
         cce.cce_p2p_attach_group([lone.h, hs[1].h], [lone.workspace(300, 64, 500, DEV), hs[1]._ws], 300, 64)
+    hs[0].close()                   # a destroyed member: the others refuse further steps
+    with pytest.raises(cce.CCEError):
+        hs[1].forward(H, Ws[1], y)
     for h in hs + [lone]:
         h.close()
 
