@@ -4,6 +4,7 @@ head).  Each workload runs back to back for ~2 s while nvidia-smi samples power 
 every 20 ms; reported: executed TFLOP/s, median power, median SM clock, pJ per executed FLOP.
   forward  cce_forward only              (2 N_valid D V executed FLOPs per call)
   backward cce_backward only (one forward first; every call recomputes: 6 N_valid D V)
+  designb_forward / designb_backward  the same with CCE_FLAG_DESIGN_B (4 N_valid D V each)
   cublas   torch.matmul bf16 8192 x 8192 x 8192 (2 M N K)
 One JSON line."""
 from __future__ import annotations
@@ -42,9 +43,16 @@ def main():
     nvd = nv * c.D * c.V
     h.forward(H, W, y, want_lse=False)
     h.backward(one, dH, dW)
+    hb = cce.CCEHandle(vocab_total=c.V, flags=cce.FLAG_DESIGN_B)
+    hb.forward(H, W, y, want_lse=False)
+    hb.backward(one, dH, dW)
     work = {
         "forward": (lambda: h.forward(H, W, y, want_lse=False), 2 * nvd),
         "backward": (lambda: h.backward(one, dH, dW), 6 * nvd),
+        # design B: the forward also accumulates the dH numerator (4 N_valid D V), the backward
+        # recomputes the logits and forms dW (4 N_valid D V)
+        "designb_forward": (lambda: hb.forward(H, W, y, want_lse=False), 4 * nvd),
+        "designb_backward": (lambda: hb.backward(one, dH, dW), 4 * nvd),
         "cublas": (lambda: torch.matmul(a, b), 2 * 8192 ** 3),
     }
     out = {"config": "qwen05b", "n_valid": nv}
