@@ -25,6 +25,8 @@ def main():
 
     import paper_2601_02609_b200 as cce
     import workload
+    if os.environ.get("CCE_LIB"):  # another build of libcce.so
+        cce.LIB_PATH = os.environ["CCE_LIB"]
     from cce_testutil import to_dev
 
     dev = torch.device("cuda:0")
